@@ -1,0 +1,356 @@
+/* oracle/oracle.c — plain, slow, obviously-correct CPU oracle for the Flux
+ * hot path (arXiv 2508.19078).  fp64 throughout, OpenMP only over independent
+ * outer loops (tokens / output elements), no blocking, fusion or reordering.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code, header, table or constant with the CUDA path
+ * (paper_2508_19078_b200/), and never reads anything the CUDA path produced.
+ *
+ * Citations: "P:N" = line N of the paper text.  Where the paper is
+ * silent the reading used is the one listed in DESIGN.md §2 ("R#").
+ *
+ *  O1 orc_quantize       P:556-565, P:575-578 (quantized MoE, bit-level per
+ *                        participant); scheme = R1 (symmetric, per-row groups
+ *                        of g along K, s = fl32(max|w|/qmax), q = RNE(fl32(w/s))).
+ *  O2 orc_router         P:217-220 (a gating network assigns tokens to
+ *                        experts), R2 (z = x·W_rᵀ, softmax, top-k, lowest index
+ *                        wins ties, w = p or p renormalised over the top-k).
+ *  O3 orc_permute        P:579-584 (D_e: the tokens that pass through expert
+ *                        e), R3 (stable: ascending token id).
+ *  O4-O6 orc_moe_tokens  P:196-220 (MoE layer = experts selected by the gate),
+ *                        R4 (SwiGLU experts, bf16 storage points), R5 (shared
+ *                        experts), R6 (y = x + shared + Σ_j w_j o_j).
+ *  O8 statistics         P:296-298 (activation frequency = activated tokens /
+ *                        total tokens) — the histogram is orc_permute's hist.
+ *  O9 orc_layer_budget   eq.(1), R9.
+ *  O10 orc_merge         eq.(2), R10.
+ *
+ * Parity pins for every function live in tests/test_oracle_*.py.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ----------------------------------------------------------------------------
+ * bf16 round-to-nearest-even of a real number (the storage points of R4/R6/R10).
+ * A bf16 has 8 significant bits: write v = m·2^e with m in [0.5,1), round
+ * m·2^8 to the nearest integer (ties to even), scale back.  Values here are
+ * far inside bf16's normal range.
+ * -------------------------------------------------------------------------- */
+double orc_bf16_round(double v) {
+  if (v == 0.0 || !isfinite(v)) return v;
+  int e;
+  double m = frexp(v, &e);            /* v = m * 2^e, 0.5 <= |m| < 1 */
+  double r = nearbyint(ldexp(m, 8));  /* default rounding mode: to nearest, ties to even */
+  return ldexp(r, e - 8);
+}
+
+void orc_bf16_round_array(int64_t n, const double* in, double* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = orc_bf16_round(in[i]);
+}
+
+/* ----------------------------------------------------------------------------
+ * O1. Quantize (R1).  w: [R][K] real values; groups of g consecutive k in a row
+ * (g == K: per output channel).  qmax = 2^(b-1) - 1.
+ *   a = max_{k in group} |w|           (exact, the inputs are fp32 numbers)
+ *   s = fl32(a / qmax)                 (one IEEE fp32 division, RNE)
+ *   q = 0 if s == 0 else clamp(RNE(fl32(w / s)), -qmax-1, qmax)
+ * Outputs: q [R][K] int8 (unpacked), s [R][K/g] fp32.
+ * -------------------------------------------------------------------------- */
+int orc_quantize(int wbits, int64_t g, int64_t R, int64_t K, const float* w, int8_t* q, float* s) {
+  if ((wbits != 4 && wbits != 8) || g <= 0 || K % g != 0) return 1;
+  const int qmax = (1 << (wbits - 1)) - 1;
+  const int64_t G = K / g;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < R; ++r) {
+    for (int64_t grp = 0; grp < G; ++grp) {
+      const float* wg = w + r * K + grp * g;
+      float a = 0.0f;
+      for (int64_t i = 0; i < g; ++i) {
+        float m = fabsf(wg[i]);
+        if (m > a) a = m;
+      }
+      float sc = a / (float)qmax;
+      s[r * G + grp] = sc;
+      for (int64_t i = 0; i < g; ++i) {
+        int v = 0;
+        if (sc != 0.0f) {
+          float t = wg[i] / sc;
+          v = (int)nearbyintf(t);
+          if (v > qmax) v = qmax;
+          if (v < -qmax - 1) v = -qmax - 1;
+        }
+        q[r * K + grp * g + i] = (int8_t)v;
+      }
+    }
+  }
+  return 0;
+}
+
+/* Canonical INT4 storage (boundary, include/flux.h): two per byte, even k in
+ * the low nibble, two's complement. */
+void orc_pack_int4(int64_t R, int64_t K, const int8_t* q, uint8_t* packed) {
+  for (int64_t r = 0; r < R; ++r)
+    for (int64_t k = 0; k < K; k += 2)
+      packed[r * (K / 2) + k / 2] = (uint8_t)((q[r * K + k] & 0xF) | ((q[r * K + k + 1] & 0xF) << 4));
+}
+
+/* ----------------------------------------------------------------------------
+ * O2. Router / gating for one token (R2).
+ *   z_e = Σ_d x_d W_r[e][d]                         (fp64)
+ *   S   = the k largest z, taken one at a time; among equal z the lower e wins;
+ *         S is listed in descending z.
+ *   p   = softmax(z) = exp(z_e - max z) / Σ_e' exp(z_e' - max z)
+ *   w_j = p_{S_j}                  (norm = 0)
+ *       = p_{S_j} / Σ_{e in S} p_e (norm = 1)
+ *   margin = z_(k) - z_(k+1) (+inf when k == E): the parity contract's near-tie measure.
+ * -------------------------------------------------------------------------- */
+static void router_one(int H, int E, int k, int norm, const double* x, const double* wr, double* z, int32_t* ids,
+                       double* w, double* margin) {
+  for (int e = 0; e < E; ++e) {
+    double acc = 0.0;
+    for (int d = 0; d < H; ++d) acc += x[d] * wr[(int64_t)e * H + d];
+    z[e] = acc;
+  }
+  char taken[1024];
+  memset(taken, 0, (size_t)E);
+  for (int j = 0; j < k; ++j) {
+    int best = -1;
+    for (int e = 0; e < E; ++e)
+      if (!taken[e] && (best < 0 || z[e] > z[best])) best = e;
+    taken[best] = 1;
+    ids[j] = best;
+  }
+  if (k < E) {
+    int nxt = -1;
+    for (int e = 0; e < E; ++e)
+      if (!taken[e] && (nxt < 0 || z[e] > z[nxt])) nxt = e;
+    *margin = z[ids[k - 1]] - z[nxt];
+  } else {
+    *margin = INFINITY;
+  }
+  double zmax = z[0];
+  for (int e = 1; e < E; ++e)
+    if (z[e] > zmax) zmax = z[e];
+  double denom = 0.0;
+  for (int e = 0; e < E; ++e) denom += exp(z[e] - zmax);
+  double psel = 0.0;
+  for (int j = 0; j < k; ++j) {
+    w[j] = exp(z[ids[j]] - zmax) / denom;
+    psel += w[j];
+  }
+  if (norm)
+    for (int j = 0; j < k; ++j) w[j] /= psel;
+}
+
+int orc_router(int64_t T, int H, int E, int k, int norm, const double* x, const double* wr, double* z, int32_t* ids,
+               double* w, double* margin) {
+  if (E < 1 || E > 1024 || k < 1 || k > E) return 1;
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t)
+    router_one(H, E, k, norm, x + t * H, wr, z + t * E, ids + t * k, w + t * k, margin + t);
+  return 0;
+}
+
+/* ----------------------------------------------------------------------------
+ * O3. D_e as CSR (R3) + the histogram of O8.
+ *   hist[e]        += #{t : e in S_t}                    (P:296-298 numerator)
+ *   offsets        = exclusive prefix sum of this call's counts, offsets[E] = T·k
+ *   token_index[offsets[e] + r] = the r-th smallest t with e in S_t
+ *   inv_pos[t][j]  = that position for e = S_tj
+ * -------------------------------------------------------------------------- */
+void orc_permute(int64_t T, int E, int k, const int32_t* ids, int64_t* hist, int64_t* offsets, int64_t* token_index,
+                 int64_t* inv_pos) {
+  int64_t* cnt = (int64_t*)calloc((size_t)E, sizeof(int64_t));
+  for (int64_t t = 0; t < T; ++t)
+    for (int j = 0; j < k; ++j) cnt[ids[t * k + j]]++;
+  offsets[0] = 0;
+  for (int e = 0; e < E; ++e) {
+    offsets[e + 1] = offsets[e] + cnt[e];
+    if (hist) hist[e] += cnt[e];
+  }
+  int64_t* fill = (int64_t*)calloc((size_t)E, sizeof(int64_t));
+  for (int64_t t = 0; t < T; ++t)
+    for (int j = 0; j < k; ++j) {
+      int e = ids[t * k + j];
+      int64_t pos = offsets[e] + fill[e]++;
+      token_index[pos] = t;
+      inv_pos[t * k + j] = pos;
+    }
+  free(cnt);
+  free(fill);
+}
+
+/* ----------------------------------------------------------------------------
+ * O4. One SwiGLU expert on one token with dequantized weights ŵ = q·s (R4):
+ *   g_f = Σ_h x_h ŵgate[f][h],  u_f = Σ_h x_h ŵup[f][h]
+ *   a_f = bf16( SiLU(g_f) · u_f ),      SiLU(v) = v / (1 + e^{-v})
+ *   o_h = bf16( Σ_f a_f ŵdown[h][f] )
+ * Quantized weights: q int8 [rows][K] unpacked, s fp32 [rows][K/g].
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  const int8_t *q_gate, *q_up, *q_down;
+  const float *s_gate, *s_up, *s_down;
+} orc_expert;
+
+static double deq(const int8_t* q, const float* s, int64_t row, int64_t K, int64_t g, int64_t k) {
+  return (double)q[row * K + k] * (double)s[row * (K / g) + k / g];
+}
+
+static void swiglu_expert(int H, int F, int64_t g_h, int64_t g_f, const orc_expert* ex, const double* x, double* a,
+                          double* out) {
+  for (int f = 0; f < F; ++f) {
+    double gs = 0.0, us = 0.0;
+    for (int h = 0; h < H; ++h) {
+      gs += x[h] * deq(ex->q_gate, ex->s_gate, f, H, g_h, h);
+      us += x[h] * deq(ex->q_up, ex->s_up, f, H, g_h, h);
+    }
+    double silu = gs / (1.0 + exp(-gs));
+    a[f] = orc_bf16_round(silu * us);
+  }
+  for (int h = 0; h < H; ++h) {
+    double acc = 0.0;
+    for (int f = 0; f < F; ++f) acc += a[f] * deq(ex->q_down, ex->s_down, h, F, g_f, f);
+    out[h] = orc_bf16_round(acc);
+  }
+}
+
+/* ----------------------------------------------------------------------------
+ * O2+O4+O5+O6 for n independent tokens of one layer (tokens never interact
+ * on this attention-free path, R7):
+ *   (z, S, w, margin) = router(x_t)
+ *   o_{t,j}  = expert_{S_tj}(x_t)                       (O4)
+ *   sh_t     = shared SwiGLU(x_t), 0 if F_s == 0        (O5)
+ *   y_t      = bf16( x_t + sh_t + Σ_j w_tj · o_{t,j} )  (O6, residual = x_t)
+ * x, y: [n][H] real (bf16-valued) numbers.  experts: array of E routed experts;
+ * shared: NULL or one expert of width F_s.  group sizes: g (0 = per channel).
+ * -------------------------------------------------------------------------- */
+int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int norm, const double* x, const double* wr,
+                   const orc_expert* experts, const orc_expert* shared, double* y, int32_t* ids, double* w, double* z,
+                   double* margin) {
+  if (orc_router(n, H, E, k, norm, x, wr, z, ids, w, margin)) return 1;
+  const int64_t gh = g ? g : H;            /* gate/up groups run along H */
+  const int64_t gf = g ? g : F;            /* down groups run along F   */
+  const int64_t gfs = g ? g : (Fs ? Fs : 1);
+  int ok = 1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t t = 0; t < n; ++t) {
+    const double* xt = x + t * H;
+    int Fmax = F > Fs ? F : Fs;
+    double* a = (double*)malloc(sizeof(double) * (size_t)Fmax);
+    double* o = (double*)malloc(sizeof(double) * (size_t)H);
+    double* acc = (double*)malloc(sizeof(double) * (size_t)H);
+    if (!a || !o || !acc) {
+      ok = 0;
+    } else {
+      for (int h = 0; h < H; ++h) acc[h] = xt[h];
+      if (shared && Fs > 0) {
+        swiglu_expert(H, Fs, gh, gfs, shared, xt, a, o);
+        for (int h = 0; h < H; ++h) acc[h] += o[h];
+      }
+      for (int j = 0; j < k; ++j) {
+        swiglu_expert(H, F, gh, gf, &experts[ids[t * k + j]], xt, a, o);
+        for (int h = 0; h < H; ++h) acc[h] += w[t * k + j] * o[h];
+      }
+      for (int h = 0; h < H; ++h) y[t * H + h] = orc_bf16_round(acc[h]);
+    }
+    free(a);
+    free(o);
+    free(acc);
+  }
+  return ok ? 0 : 2;
+}
+
+/* ----------------------------------------------------------------------------
+ * O9. Adaptive expert layer size, eq.(1), reading R9:
+ *   f_l[e] = hist[l][e] / T
+ *   v_l    = (1/E) Σ_e (f_l[e] - mean_l)^2       (population variance)
+ *   b_l    = (L - l + 1) / max(v_l, 1e-12),  l = 1..L
+ *   B(l)   = floor( b_l / Σ_k b_k · B_non )
+ *   C_l    = clamp(B(l), 1, n_non[l])    (R9: never discard a layer's experts)
+ * Returns Σ_l C_l - B_non (> 0 = overrun forced by the clamp).
+ * -------------------------------------------------------------------------- */
+int64_t orc_layer_budget(int L, int E, const int64_t* hist, int64_t T, int64_t B_non, const int32_t* n_non,
+                         int32_t* C_out, double* b_out, double* v_out) {
+  double* b = (double*)malloc(sizeof(double) * (size_t)L);
+  double bsum = 0.0;
+  for (int l = 0; l < L; ++l) {
+    double mean = 0.0;
+    for (int e = 0; e < E; ++e) mean += (double)hist[(int64_t)l * E + e] / (double)T;
+    mean /= E;
+    double v = 0.0;
+    for (int e = 0; e < E; ++e) {
+      double d = (double)hist[(int64_t)l * E + e] / (double)T - mean;
+      v += d * d;
+    }
+    v /= E;
+    if (v_out) v_out[l] = v;
+    if (v < 1e-12) v = 1e-12;
+    b[l] = (double)(L - (l + 1) + 1) / v;
+    bsum += b[l];
+  }
+  int64_t total = 0;
+  for (int l = 0; l < L; ++l) {
+    int64_t B = (int64_t)floor(b[l] / bsum * (double)B_non);
+    if (B < 1) B = 1;
+    if (n_non && B > n_non[l]) B = n_non[l];
+    C_out[l] = (int32_t)B;
+    if (b_out) b_out[l] = b[l];
+    total += B;
+  }
+  free(b);
+  return total - B_non;
+}
+
+/* ----------------------------------------------------------------------------
+ * O10. Importance-based merge, eq.(2), reading R10:
+ *   for each cluster c:  E_c = {e : cluster_of[e] == c}
+ *     w_e = α_e / Σ_{e' in E_c} α_e'   (if Σ α = 0: w_e = 1/|E_c|)
+ *     W_c = Σ_{e in E_c} w_e · W_e      (element-wise, fp64; caller rounds once)
+ *   cluster_of[e] == -1: tuning expert, kept, not merged.
+ *   remap[e] = slot of e in the compact layer: tuning experts first in
+ *   ascending id, then clusters 0..C-1 (the per-layer expert count of
+ *   exps_config).
+ * experts: [E][numel] real; merged: [C][numel] real.  A cluster with no member
+ * is an error (returns 1).
+ * -------------------------------------------------------------------------- */
+int orc_merge(int E, int64_t numel, const double* experts, const int32_t* cluster_of, const double* alpha, int C,
+              double* merged, int32_t* remap) {
+  double* wsum = (double*)calloc((size_t)C, sizeof(double));
+  int* count = (int*)calloc((size_t)C, sizeof(int));
+  for (int e = 0; e < E; ++e) {
+    int c = cluster_of[e];
+    if (c < -1 || c >= C) { free(wsum); free(count); return 1; }
+    if (c >= 0) { wsum[c] += alpha[e]; count[c]++; }
+  }
+  for (int c = 0; c < C; ++c)
+    if (count[c] == 0) { free(wsum); free(count); return 1; }
+  double* we = (double*)malloc(sizeof(double) * (size_t)E);
+  for (int e = 0; e < E; ++e) {
+    int c = cluster_of[e];
+    we[e] = 0.0;
+    if (c >= 0) we[e] = wsum[c] > 0.0 ? alpha[e] / wsum[c] : 1.0 / count[c];
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < numel; ++i) {
+    for (int c = 0; c < C; ++c) merged[(int64_t)c * numel + i] = 0.0;
+    for (int e = 0; e < E; ++e) {
+      int c = cluster_of[e];
+      if (c >= 0) merged[(int64_t)c * numel + i] += we[e] * experts[(int64_t)e * numel + i];
+    }
+  }
+  if (remap) {
+    int slot = 0;
+    for (int e = 0; e < E; ++e)
+      if (cluster_of[e] == -1) remap[e] = slot++;
+    for (int e = 0; e < E; ++e)
+      if (cluster_of[e] >= 0) remap[e] = slot + cluster_of[e];
+  }
+  free(we);
+  free(wsum);
+  free(count);
+  return 0;
+}
