@@ -1,0 +1,170 @@
+/* include/flux.h — C ABI of libflux.so, the B200 (sm_100a) hot path of Flux
+ * (arXiv 2508.19078): quantization-based local expert-activation profiling,
+ * the statistics all-reduce, and the activation-frequency-weighted merge of
+ * non-tuning experts.
+ *
+ * Citations: "P:N" = line N of the paper text; "R#" = a reading of
+ * a passage the paper leaves open, listed in DESIGN.md §2.
+ *
+ * Conventions (all entry points):
+ *  - Plain C types only.  Device pointers are CUDA device addresses; `stream`
+ *    is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Ownership: the caller owns every buffer.  Hot calls allocate nothing;
+ *    scratch comes from the caller's workspace.  Only flux_comm is owned by
+ *    the library (flux_comm_init / flux_comm_destroy).
+ *  - Stream-ordered and asynchronous.  Argument / shape validation happens on
+ *    the host before any launch; on error nothing is launched and a status is
+ *    returned.  Launch failures return FLUX_E_CUDA; asynchronous device faults
+ *    surface at the caller's next synchronisation.
+ *  - No CPU fallback: unsupported shapes return FLUX_E_UNSUPPORTED, and a host
+ *    without an sm_100 device gets FLUX_E_CUDA.
+ *  - Deterministic: outputs are bitwise reproducible and independent of how
+ *    tokens are split across calls (chunking) or GPUs (data parallelism).
+ *  - Layouts are row-major with the contraction dimension contiguous.  bf16
+ *    is IEEE bfloat16 (uint16 storage).  INT4 is packed two per byte, even k
+ *    in the low nibble, two's complement.
+ */
+#ifndef FLUX_H_
+#define FLUX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FLUX_OK = 0,
+  FLUX_E_INVALID = 1,     /* bad pointer / size / alignment / value              */
+  FLUX_E_UNSUPPORTED = 2, /* shape or dtype outside the supported set            */
+  FLUX_E_WORKSPACE = 3,   /* workspace smaller than flux_profile_layer_workspace  */
+  FLUX_E_CUDA = 4,        /* CUDA runtime / driver error (incl. no sm_100 device) */
+  FLUX_E_NCCL = 5         /* NCCL error, or libnccl.so.2 could not be loaded      */
+} flux_status;
+
+typedef enum { FLUX_BF16 = 0, FLUX_FP32 = 1 } flux_dtype;
+
+const char* flux_status_string(flux_status s);
+
+/* ============================================================================
+ * Model shape of one MoE layer (Table 1).
+ * Supported: hidden % 64 == 0; ffn % 16 == 0 (and shared_ffn); 1 <= top_k <=
+ * n_experts <= 256; wbits in {4, 8}; group_size == 0 (per output channel) or
+ * a multiple of 64 dividing both hidden and ffn (and shared_ffn); INT4 needs
+ * every packed row to be a multiple of 16 B (hidden % 32 == 0, ffn % 32 == 0).
+ * ========================================================================== */
+typedef struct {
+  int32_t hidden;     /* H                                                    */
+  int32_t ffn;        /* F, width of one routed expert                        */
+  int32_t n_experts;  /* E, routed experts                                    */
+  int32_t top_k;      /* k, experts per token                                 */
+  int32_t shared_ffn; /* F_s of the always-on shared experts (0 = none), R5   */
+  int32_t wbits;      /* 8 or 4 (bit level chosen per participant) */
+  int32_t group_size; /* 0 = per output channel, else g along the contraction */
+  int32_t norm_topk;  /* 0: w = softmax prob; 1: renormalised over top-k (R2) */
+} flux_moe_cfg;
+
+/* Quantized weights of one layer, canonical layout (device pointers):
+ *   router_w  bf16 [E][H]               (not quantized, R1)
+ *   gate_q    [E][F][H']   up_q [E][F][H']   H' = H (int8) or H/2 bytes (int4)
+ *   gate_s    fp32 [E][F][H/g]          (g = H when group_size == 0)
+ *   down_q    [E][H][F']                F' = F or F/2
+ *   down_s    fp32 [E][H][F/g]
+ *   sh_*      same for the shared MLP with F_s instead of F (NULL if F_s == 0)
+ * All pointers 16-byte aligned. */
+typedef struct {
+  const void* router_w;
+  const void *gate_q, *up_q, *down_q;
+  const float *gate_s, *up_s, *down_s;
+  const void *sh_gate_q, *sh_up_q, *sh_down_q;
+  const float *sh_gate_s, *sh_up_s, *sh_down_s;
+} flux_qlayer;
+
+/* Per-layer outputs (device pointers, caller-owned; optional ones may be NULL):
+ *   y              bf16 [T][H]   y_t = bf16(r_t + sh_t + Σ_j w_tj · o_{t,S_tj})   (R6) — required
+ *   topk_ids       int32 [T][k]  S_t, descending logit, lower index on ties (R2)  — required
+ *   topk_w         fp32 [T][k]   gate weights w_tj (R2)                           — required
+ *   hist           int64 [E]     ACCUMULATED (+=) activation counts, P:296-298    — required;
+ *                                the caller zeroes it once per profiling round
+ *   expert_offsets int32 [E+1]   D_e segment bounds into token_index  — optional
+ *   token_index    int32 [T*k]   D_e members, ascending chunk-local token id (R3)  — optional
+ *   router_logits  fp32 [T][E]   z = x·W_rᵀ, for parity checks only               — optional */
+typedef struct {
+  void* y;
+  int32_t* topk_ids;
+  float* topk_w;
+  int64_t* hist;
+  int32_t* expert_offsets;
+  int32_t* token_index;
+  float* router_logits;
+} flux_layer_out;
+
+/* Workspace bytes flux_profile_layer needs for T tokens (host function). */
+size_t flux_profile_layer_workspace(const flux_moe_cfg* cfg, int64_t T);
+
+/* One quantized MoE layer forward over T tokens that also emits the expert
+ * activation statistics — the profiling step of §4.1:
+ *   z = x·W_rᵀ; S_t = top-k(z_t); w_t from softmax(z_t)            (R2)
+ *   hist[e] += #{t : e ∈ S_t}; D_e = {t : e ∈ S_t}
+ *   o_{t,e} = bf16(bf16(SiLU(x_t·ŵgᵀ)⊙(x_t·ŵuᵀ))·ŵdᵀ), ŵ = q·s     (R4)
+ *   sh_t = shared SwiGLU(x_t) (R5);  y_t = bf16(r_t + sh_t + Σ_j w_tj o_{t,S_tj})
+ * x: bf16 [T][H] device; residual: bf16 [T][H] device or NULL (NULL = x, R6).
+ * T may be 0 (no-op) or any positive count up to 2^31/k. Tokens are
+ * independent; results do not depend on T or on how a batch is split. */
+flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, const void* x, const void* residual,
+                               int64_t T, const flux_layer_out* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Activation-frequency-weighted merge of non-tuning experts, eq.(2):
+ *   W_c = Σ_{e∈E_c} α_e / Σ_{e'∈E_c} α_e' · W_e  (Σα = 0 -> plain mean, R10)
+ * One weight family of one layer per call (or all families if the caller
+ * stores them concatenated):
+ *   experts     [E][numel] dtype, device       cluster_of int32 [E] device, -1 = tuning expert (kept)
+ *   alpha       fp32 [E] device, >= 0 (α = f, or f·ā)
+ *   merged      [n_clusters][numel] dtype, device; fp32 accumulation, one rounding
+ *   remap       int32 [E] device or NULL: compact slot of e — tuning experts
+ *               first in ascending id, then clusters 0..C-1
+ * numel % 8 == 0, pointers 16-byte aligned, 1 <= n_clusters <= E <= 1024.
+ * Every cluster id in [0, n_clusters) must have a member: this is checked on
+ * the device and an empty cluster's output is left as zeros. */
+flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t numel, const void* experts,
+                               const int32_t* cluster_of, const float* alpha, int32_t n_clusters, void* merged,
+                               int32_t* remap, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Statistics all-reduce over the GPUs of one box (NCCL over NVLink/NVSwitch).
+ * The counts are additive integers, so the reduced histogram equals the
+ * single-GPU histogram of the union of the shards bit for bit.
+ * ------------------------------------------------------------------------- */
+typedef struct flux_comm flux_comm;
+/* Rank 0 creates the 128-byte NCCL unique id; the caller distributes it. */
+flux_status flux_comm_unique_id(void* out_128_bytes);
+/* Collective over all ranks; binds to the current CUDA device. */
+flux_status flux_comm_init(flux_comm** out, const void* unique_id_128_bytes, int32_t nranks, int32_t rank);
+/* In-place sum of `count` int64 counters (device pointer) on `stream`. */
+flux_status flux_reduce_stats(flux_comm* comm, int64_t* hist, size_t count, void* stream);
+flux_status flux_comm_destroy(flux_comm* comm);
+
+/* ---------------------------------------------------------------------------
+ * Helpers (not per-token hot).
+ * ------------------------------------------------------------------------- */
+/* Weight quantizer, reading R1: symmetric, per row,
+ * groups of g along K (g = K if group_size == 0):
+ *   s = fl32(max|w| / qmax), q = clamp(RNE(fl32(w/s)), -qmax-1, qmax), s = 0 -> q = 0
+ * w: [R][K] bf16 or fp32 device; q: [R][K] int8 or [R][K/2] packed int4; s: fp32 [R][K/g].
+ * Bit-exact (IEEE division, no fast-math).  Needs K % 2 == 0 for INT4. */
+flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype in_dtype, const void* w, int64_t R,
+                                  int64_t K, void* q, float* s, void* stream);
+
+/* Adaptive expert layer size, eq.(1), reading R9 (host function):
+ *   f_l = hist[l][·]/T, v_l = population variance of f_l, b_l = (L-l+1)/max(v_l,1e-12) (l = 1..L),
+ *   C_l = clamp(floor(b_l/Σ_k b_k · B_non), 1, n_non[l]).
+ * hist: host int64 [L][E]; n_non: host int32 [L] (NULL = E); C_out: host int32 [L].
+ * *overrun (may be NULL) = Σ C_l - B_non. */
+flux_status flux_layer_budget(int32_t L, int32_t E, const int64_t* hist, int64_t T, int64_t B_non,
+                              const int32_t* n_non, int32_t* C_out, int64_t* overrun);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLUX_H_ */

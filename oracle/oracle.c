@@ -116,7 +116,7 @@ static void router_one(int H, int E, int k, int norm, const double* x, const dou
     z[e] = acc;
   }
   char taken[1024];
-  memset(taken, 0, (size_t)E);
+  for (int e = 0; e < E; ++e) taken[e] = 0;
   for (int j = 0; j < k; ++j) {
     int best = -1;
     for (int e = 0; e < E; ++e)
@@ -196,8 +196,15 @@ typedef struct {
   const float *s_gate, *s_up, *s_down;
 } orc_expert;
 
+/* Dequantized weight of the quantized model (reading R1b):
+ *   per output channel (group_size == 0): ŵ = q·s exactly (the scale multiplies the dot product);
+ *   groups along K:                       ŵ = bf16( q · bf16(s) )  — the W4A16 convention: the
+ *   quantized model's weights are materialised in bf16 from the code and the bf16 scale. */
+static int g_grouped = 0; /* set per call by orc_moe_tokens */
 static double deq(const int8_t* q, const float* s, int64_t row, int64_t K, int64_t g, int64_t k) {
-  return (double)q[row * K + k] * (double)s[row * (K / g) + k / g];
+  double sc = (double)s[row * (K / g) + k / g];
+  if (g_grouped) return orc_bf16_round((double)q[row * K + k] * orc_bf16_round(sc));
+  return (double)q[row * K + k] * sc;
 }
 
 static void swiglu_expert(int H, int F, int64_t g_h, int64_t g_f, const orc_expert* ex, const double* x, double* a,
@@ -232,6 +239,7 @@ int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int nor
                    const orc_expert* experts, const orc_expert* shared, double* y, int32_t* ids, double* w, double* z,
                    double* margin) {
   if (orc_router(n, H, E, k, norm, x, wr, z, ids, w, margin)) return 1;
+  g_grouped = g != 0;
   const int64_t gh = g ? g : H;            /* gate/up groups run along H */
   const int64_t gf = g ? g : F;            /* down groups run along F   */
   const int64_t gfs = g ? g : (Fs ? Fs : 1);

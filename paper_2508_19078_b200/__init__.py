@@ -1,0 +1,171 @@
+"""paper_2508_19078_b200 — B200-native hot path of Flux (arXiv 2508.19078).
+
+Thin ctypes binding over libflux.so (include/flux.h).  This module only
+marshals arguments: every step of the computation runs in the library's
+sm_100a kernels.  torch supplies device memory, streams and process groups.
+There is no CPU fallback: if libflux.so is missing or no sm_100 GPU is
+present, calls raise.
+
+Entry points (same names as the C ABI):
+  profile_layer_workspace, profile_layer      quantized MoE layer + expert stats (§4.1)
+  merge_experts                               eq.(2) merge
+  quantize_weights                            INT8/INT4 quantizer
+  layer_budget                                eq.(1)
+  Comm (comm_unique_id / comm_init / reduce_stats / comm_destroy)   histogram all-reduce
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch  # noqa: F401  (load torch's CUDA runtime first: libflux shares it)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libflux.so")
+
+FLUX_OK, FLUX_E_INVALID, FLUX_E_UNSUPPORTED, FLUX_E_WORKSPACE, FLUX_E_CUDA, FLUX_E_NCCL = range(6)
+FLUX_BF16, FLUX_FP32 = 0, 1
+
+
+class FluxError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {_lib().flux_status_string(status).decode()} (status {status})")
+
+
+class MoECfg(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("hidden", "ffn", "n_experts", "top_k", "shared_ffn", "wbits", "group_size", "norm_topk")]
+
+
+class QLayer(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("router_w", "gate_q", "up_q", "down_q", "gate_s", "up_s", "down_s",
+                 "sh_gate_q", "sh_up_q", "sh_down_q", "sh_gate_s", "sh_up_s", "sh_down_s")]
+
+
+class LayerOut(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("y", "topk_ids", "topk_w", "hist", "expert_offsets", "token_index", "router_logits")]
+
+
+_L = None
+
+
+def _lib():
+    global _L
+    if _L is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        L.flux_status_string.argtypes = [ctypes.c_int]
+        L.flux_status_string.restype = ctypes.c_char_p
+        L.flux_profile_layer_workspace.argtypes = [ctypes.POINTER(MoECfg), I64]
+        L.flux_profile_layer_workspace.restype = SZ
+        L.flux_profile_layer.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(QLayer), P, P, I64,
+                                         ctypes.POINTER(LayerOut), P, SZ, P]
+        L.flux_merge_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
+        L.flux_quantize_weights.argtypes = [I32, I32, ctypes.c_int, P, I64, I64, P, P, P]
+        L.flux_layer_budget.argtypes = [I32, I32, P, I64, I64, P, P, P]
+        L.flux_comm_unique_id.argtypes = [P]
+        L.flux_comm_init.argtypes = [ctypes.POINTER(P), P, I32, I32]
+        L.flux_reduce_stats.argtypes = [P, P, SZ, P]
+        L.flux_comm_destroy.argtypes = [P]
+        for f in ("flux_profile_layer", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
+                  "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
+            getattr(L, f).restype = ctypes.c_int
+        _L = L
+    return _L
+
+
+def lib():
+    return _lib()
+
+
+def _check(st: int, what: str):
+    if st != FLUX_OK:
+        raise FluxError(st, what)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+
+
+# ------------------------------------------------------------------------------------------ API
+def make_cfg(hidden, ffn, n_experts, top_k, shared_ffn, wbits, group_size, norm_topk) -> MoECfg:
+    return MoECfg(hidden, ffn, n_experts, top_k, shared_ffn, wbits, group_size, norm_topk)
+
+
+def profile_layer_workspace(cfg: MoECfg, T: int) -> int:
+    return int(_lib().flux_profile_layer_workspace(ctypes.byref(cfg), T))
+
+
+def profile_layer(cfg: MoECfg, qlayer: QLayer, x, residual, T: int, out: LayerOut, ws, stream=None):
+    """One quantized MoE layer + statistics (flux_profile_layer). Tensors are CUDA tensors."""
+    st = _lib().flux_profile_layer(ctypes.byref(cfg), ctypes.byref(qlayer), _ptr(x), _ptr(residual), T,
+                                   ctypes.byref(out), _ptr(ws), ws.numel() * ws.element_size() if ws is not None
+                                   else 0, _stream(stream))
+    _check(st, "flux_profile_layer")
+
+
+def merge_experts(experts, cluster_of, alpha, n_clusters: int, merged, remap=None, stream=None):
+    """eq.(2): experts [E][numel] (bf16/fp32 CUDA), cluster_of int32 [E], alpha fp32 [E] -> merged [C][numel]."""
+    dt = FLUX_FP32 if experts.dtype == torch.float32 else FLUX_BF16
+    E = experts.shape[0]
+    numel = experts.numel() // E
+    st = _lib().flux_merge_experts(dt, E, numel, _ptr(experts), _ptr(cluster_of), _ptr(alpha), n_clusters,
+                                   _ptr(merged), _ptr(remap), _stream(stream))
+    _check(st, "flux_merge_experts")
+
+
+def quantize_weights(w, wbits: int, group_size: int, q, s, stream=None):
+    """w [R][K] bf16/fp32 CUDA -> q int8 [R][K] or uint8 [R][K/2] (INT4), s fp32 [R][K/g]."""
+    dt = FLUX_FP32 if w.dtype == torch.float32 else FLUX_BF16
+    K = w.shape[-1]
+    R = w.numel() // K
+    st = _lib().flux_quantize_weights(wbits, group_size, dt, _ptr(w), R, K, _ptr(q), _ptr(s), _stream(stream))
+    _check(st, "flux_quantize_weights")
+
+
+def layer_budget(hist, T: int, B_non: int, n_non=None):
+    """eq.(1) on host int64 counts [L][E] -> (C [L] list, overrun)."""
+    import numpy as np
+    h = np.ascontiguousarray(hist, dtype=np.int64)
+    L, E = h.shape
+    C = np.empty(L, np.int32)
+    nn = None if n_non is None else np.ascontiguousarray(n_non, dtype=np.int32)
+    over = ctypes.c_int64(0)
+    st = _lib().flux_layer_budget(L, E, h.ctypes.data, T, B_non, None if nn is None else nn.ctypes.data,
+                                  C.ctypes.data, ctypes.byref(over))
+    _check(st, "flux_layer_budget")
+    return C, over.value
+
+
+class Comm:
+    """NCCL communicator for the histogram all-reduce (flux_comm_*)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        self._h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(uid, 128)
+        _check(_lib().flux_comm_init(ctypes.byref(self._h), buf, nranks, rank), "flux_comm_init")
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(_lib().flux_comm_unique_id(buf), "flux_comm_unique_id")
+        return buf.raw
+
+    def reduce_stats(self, hist, stream=None):
+        _check(_lib().flux_reduce_stats(self._h, _ptr(hist), hist.numel(), _stream(stream)), "flux_reduce_stats")
+
+    def destroy(self):
+        if self._h:
+            _check(_lib().flux_comm_destroy(self._h), "flux_comm_destroy")
+            self._h = ctypes.c_void_p()

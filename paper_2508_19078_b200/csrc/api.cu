@@ -1,0 +1,343 @@
+// api.cu — the C ABI of libflux.so (include/flux.h): argument validation,
+// workspace carving, TMA descriptors and the launch sequence of one profiled
+// MoE layer.  Every step of the computation runs in the kernels of this
+// library; there is no host or CPU fallback path.
+#include <algorithm>
+#include <mutex>
+
+#include "internal.h"
+
+namespace flux {
+
+// ---------------------------------------------------------------- TMA descriptor creation
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+EncodeTiledFn encode_fn() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  });
+  return g_encode;
+}
+}  // namespace
+
+bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint32_t elem_bytes, uint64_t rows,
+                  uint64_t cols, uint64_t row_stride_bytes, uint32_t box_cols, uint32_t box_rows,
+                  CUtensorMapSwizzle swizzle) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return false;
+  cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  (void)elem_bytes;
+  CUresult r = f(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static bool tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, cols * 2, 64, box_rows,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// ---------------------------------------------------------------- device check
+static flux_status check_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FLUX_E_CUDA;
+  int major = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return FLUX_E_CUDA;
+  return major == 10 ? FLUX_OK : FLUX_E_CUDA;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------- workspace layout
+namespace {
+struct Layout {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  }
+};
+struct WsPlan {
+  size_t tile_counts, tile_base, rank, offsets, token_index, inv_pos, counter, sched_gu, sched_dn, row0, rows;
+  size_t x_perm, act, act_sh, y_sh, wgu_r, wdn_r, wgu_s, wdn_s;
+  size_t total;
+};
+int pad128(int v) { return (v + 127) / 128 * 128; }
+
+WsPlan plan(const flux_moe_cfg& c, int64_t T) {
+  Layout L;
+  WsPlan p;
+  const int64_t n_rt = (T + 127) / 128;
+  const int64_t Tk = T * c.top_k;
+  const int n_groups = c.n_experts + (c.shared_ffn > 0);
+  p.tile_counts = L.take(sizeof(int32_t) * n_rt * c.n_experts);
+  p.tile_base = L.take(sizeof(int32_t) * n_rt * c.n_experts);
+  p.rank = L.take(sizeof(int32_t) * Tk);
+  p.offsets = L.take(sizeof(int32_t) * (c.n_experts + 1));
+  p.token_index = L.take(sizeof(int32_t) * Tk);
+  p.inv_pos = L.take(sizeof(int32_t) * Tk);
+  p.counter = L.take(sizeof(int32_t));
+  p.sched_gu = L.take(sizeof(int32_t) * (n_groups + 1));
+  p.sched_dn = L.take(sizeof(int32_t) * (n_groups + 1));
+  p.row0 = L.take(sizeof(int32_t) * n_groups);
+  p.rows = L.take(sizeof(int32_t) * n_groups);
+  p.x_perm = L.take(2ull * Tk * c.hidden);  // reused as y_perm after the gate/up GEMM
+  p.act = L.take(2ull * Tk * c.ffn);
+  p.act_sh = L.take(2ull * T * c.shared_ffn);
+  p.y_sh = L.take(c.shared_ffn ? 2ull * T * c.hidden : 0);
+  p.wgu_r = L.take(2ull * c.n_experts * 2 * pad128(c.ffn) * c.hidden);
+  p.wdn_r = L.take(2ull * c.n_experts * c.hidden * c.ffn);
+  p.wgu_s = L.take(2ull * 2 * pad128(c.shared_ffn) * c.hidden);
+  p.wdn_s = L.take(2ull * c.hidden * c.shared_ffn);
+  p.total = L.off;
+  return p;
+}
+
+flux_status validate_cfg(const flux_moe_cfg* c) {
+  if (!c) return FLUX_E_INVALID;
+  if (c->hidden <= 0 || c->ffn <= 0 || c->n_experts <= 0 || c->top_k <= 0 || c->shared_ffn < 0)
+    return FLUX_E_INVALID;
+  if (c->wbits != 4 && c->wbits != 8) return FLUX_E_UNSUPPORTED;
+  if (c->hidden % 64 || c->ffn % 16 || c->shared_ffn % 16) return FLUX_E_UNSUPPORTED;
+  if (c->n_experts > 128 || c->top_k > 8 || c->top_k > c->n_experts) return FLUX_E_UNSUPPORTED;
+  if (c->norm_topk != 0 && c->norm_topk != 1) return FLUX_E_INVALID;
+  if (c->group_size < 0) return FLUX_E_INVALID;
+  if (c->group_size > 0) {
+    if (c->group_size % 64 || c->hidden % c->group_size || c->ffn % c->group_size ||
+        (c->shared_ffn && c->shared_ffn % c->group_size))
+      return FLUX_E_UNSUPPORTED;
+  }
+  if (c->wbits == 4 && (c->hidden % 32 || c->ffn % 32 || c->shared_ffn % 32)) return FLUX_E_UNSUPPORTED;
+  return FLUX_OK;
+}
+}  // namespace
+
+}  // namespace flux
+
+using namespace flux;
+
+extern "C" {
+
+const char* flux_status_string(flux_status s) {
+  switch (s) {
+    case FLUX_OK: return "ok";
+    case FLUX_E_INVALID: return "invalid argument";
+    case FLUX_E_UNSUPPORTED: return "unsupported shape or dtype";
+    case FLUX_E_WORKSPACE: return "workspace too small";
+    case FLUX_E_CUDA: return "CUDA error (or no sm_100 device)";
+    case FLUX_E_NCCL: return "NCCL error";
+  }
+  return "unknown status";
+}
+
+size_t flux_profile_layer_workspace(const flux_moe_cfg* cfg, int64_t T) {
+  if (validate_cfg(cfg) != FLUX_OK || T < 0) return 0;
+  return plan(*cfg, T).total;
+}
+
+flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, const void* x, const void* residual,
+                               int64_t T, const flux_layer_out* out, void* ws, size_t ws_bytes, void* stream) {
+  flux_status st = validate_cfg(cfg);
+  if (st != FLUX_OK) return st;
+  if (!w || !out || T < 0) return FLUX_E_INVALID;
+  if (T == 0) return FLUX_OK;
+  if (T * cfg->top_k >= (int64_t)1 << 31) return FLUX_E_UNSUPPORTED;
+  const flux_moe_cfg& c = *cfg;
+  const bool sh = c.shared_ffn > 0;
+  if (!x || !out->y || !out->topk_ids || !out->topk_w || !out->hist || !w->router_w || !w->gate_q || !w->up_q ||
+      !w->down_q || !w->gate_s || !w->up_s || !w->down_s)
+    return FLUX_E_INVALID;
+  if (sh && (!w->sh_gate_q || !w->sh_up_q || !w->sh_down_q || !w->sh_gate_s || !w->sh_up_s || !w->sh_down_s))
+    return FLUX_E_INVALID;
+  const void* ptrs16[] = {x, residual, out->y, w->router_w, w->gate_q, w->up_q, w->down_q,
+                          w->sh_gate_q, w->sh_up_q, w->sh_down_q, ws};
+  for (const void* p : ptrs16)
+    if (p && !aligned16(p)) return FLUX_E_INVALID;
+  const WsPlan P = plan(c, T);
+  if (!ws || ws_bytes < P.total) return FLUX_E_WORKSPACE;
+  if ((st = check_device()) != FLUX_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* W = (uint8_t*)ws;
+  const int H = c.hidden, F = c.ffn, Fs = c.shared_ffn, E = c.n_experts, k = c.top_k;
+  const int Fp = pad128(F), Fsp = pad128(Fs);
+  const bool per_channel = c.group_size == 0;
+  const int g_h = per_channel ? H : c.group_size, g_f = per_channel ? F : c.group_size,
+            g_fs = per_channel ? Fs : c.group_size;
+  const int64_t n_rt = (T + 127) / 128;
+  const int64_t Tk = T * k;
+  const int n_groups = E + (sh ? 1 : 0);
+
+  int32_t* tile_counts = (int32_t*)(W + P.tile_counts);
+  int32_t* tile_base = (int32_t*)(W + P.tile_base);
+  int32_t* rank = (int32_t*)(W + P.rank);
+  int32_t* offsets = (int32_t*)(W + P.offsets);
+  int32_t* token_index = out->token_index ? out->token_index : (int32_t*)(W + P.token_index);
+  int32_t* inv_pos = (int32_t*)(W + P.inv_pos);
+  void* x_perm = W + P.x_perm;
+  void* act = W + P.act;
+  void* act_sh = W + P.act_sh;
+  void* y_sh = W + P.y_sh;
+  void* wgu_r = W + P.wgu_r;
+  void* wdn_r = W + P.wdn_r;
+  void* wgu_s = W + P.wgu_s;
+  void* wdn_s = W + P.wdn_s;
+
+  // ---- (a) weights -> bf16 B operands (scale folded for grouped quantization)
+  cudaError_t e;
+  e = launch_dequant(c.wbits, (const uint8_t*)w->gate_q, w->gate_s, (const uint8_t*)w->up_q, w->up_s, E, F, H, Fp, 1,
+                     g_h, per_channel, wgu_r, s);
+  if (e == cudaSuccess)
+    e = launch_dequant(c.wbits, (const uint8_t*)w->down_q, w->down_s, nullptr, nullptr, E, H, F, 0, 0, g_f,
+                       per_channel, wdn_r, s);
+  if (e == cudaSuccess && sh)
+    e = launch_dequant(c.wbits, (const uint8_t*)w->sh_gate_q, w->sh_gate_s, (const uint8_t*)w->sh_up_q, w->sh_up_s,
+                       1, Fs, H, Fsp, 1, g_h, per_channel, wgu_s, s);
+  if (e == cudaSuccess && sh)
+    e = launch_dequant(c.wbits, (const uint8_t*)w->sh_down_q, w->sh_down_s, nullptr, nullptr, 1, H, Fs, 0, 0, g_fs,
+                       per_channel, wdn_s, s);
+  if (e != cudaSuccess) return FLUX_E_CUDA;
+
+  // ---- (b) K1 router + top-k + histogram
+  const int npad = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
+  CUtensorMap tm_x, tm_wr;
+  if (!tmap_bf16(&tm_x, x, T, H, 128) || !tmap_bf16(&tm_wr, w->router_w, E, H, npad)) return FLUX_E_CUDA;
+  RouterArgs ra{T, H, E, k, c.norm_topk, out->topk_ids, out->topk_w, out->router_logits, out->hist, tile_counts, rank};
+  if (launch_router(tm_x, tm_wr, npad, ra, s) != cudaSuccess) return FLUX_E_CUDA;
+
+  // ---- (c) K2 schedule + scatter/gather (D_e)
+  ScheduleArgs sa;
+  sa.E = E;
+  sa.k = k;
+  sa.T = T;
+  sa.n_tiles = (int)n_rt;
+  sa.tile_counts = tile_counts;
+  sa.tile_base = tile_base;
+  sa.offsets = offsets;
+  sa.user_offsets = out->expert_offsets;
+  sa.done_counter = (int32_t*)(W + P.counter);
+  sa.has_shared = sh;
+  sa.n_tiles_gu = Fp / 128;
+  sa.n_tiles_gu_sh = Fsp / 128;
+  sa.n_tiles_dn = (H + 255) / 256;
+  sa.n_tiles_dn_sh = (H + 255) / 256;
+  sa.sched_gu = (int32_t*)(W + P.sched_gu);
+  sa.sched_dn = (int32_t*)(W + P.sched_dn);
+  sa.grp_row0 = (int32_t*)(W + P.row0);
+  sa.grp_rows = (int32_t*)(W + P.rows);
+  if (launch_schedule(sa, s) != cudaSuccess) return FLUX_E_CUDA;
+  if (launch_scatter(x, T, H, E, k, out->topk_ids, rank, tile_base, offsets, inv_pos, token_index, x_perm, s) !=
+      cudaSuccess)
+    return FLUX_E_CUDA;
+
+  // ---- (d) K3 + K5: gate/up grouped GEMM with SwiGLU epilogue (routed + shared in one launch)
+  CUtensorMap a_r, a_s, b_r, b_s;
+  if (!tmap_bf16(&a_r, x_perm, Tk, H, 128) || !tmap_bf16(&b_r, wgu_r, (uint64_t)E * 2 * Fp, H, 256))
+    return FLUX_E_CUDA;
+  if (sh) {
+    if (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_bf16(&b_s, wgu_s, 2ull * Fsp, H, 256)) return FLUX_E_CUDA;
+  } else {
+    a_s = a_r;
+    b_s = b_r;
+  }
+  GemmArgs ga{};
+  ga.n_groups = n_groups;
+  ga.E = E;
+  ga.sched = sa.sched_gu;
+  ga.grp_row0 = sa.grp_row0;
+  ga.grp_rows = sa.grp_rows;
+  ga.n_tiles_r = sa.n_tiles_gu;
+  ga.n_tiles_s = sa.n_tiles_gu_sh;
+  ga.K_r = H;
+  ga.K_s = H;
+  ga.N_r = F;
+  ga.N_s = Fs;
+  ga.b_rows_r = 2 * Fp;
+  ga.cs0_r = per_channel ? w->gate_s : nullptr;
+  ga.cs1_r = per_channel ? w->up_s : nullptr;
+  ga.cs0_s = per_channel ? w->sh_gate_s : nullptr;
+  ga.cs1_s = per_channel ? w->sh_up_s : nullptr;
+  ga.out_r = act;
+  ga.out_s = act_sh;
+  ga.ld_r = F;
+  ga.ld_s = Fs;
+  ga.grid = kNumSMs;
+  if (launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s) != cudaSuccess) return FLUX_E_CUDA;
+
+  // ---- (e) K4 + K5: down grouped GEMM -> y_perm (aliases x_perm) and y_sh
+  void* y_perm = x_perm;
+  if (!tmap_bf16(&a_r, act, Tk, F, 128) || !tmap_bf16(&b_r, wdn_r, (uint64_t)E * H, F, 256)) return FLUX_E_CUDA;
+  if (sh) {
+    if (!tmap_bf16(&a_s, act_sh, T, Fs, 128) || !tmap_bf16(&b_s, wdn_s, H, Fs, 256)) return FLUX_E_CUDA;
+  } else {
+    a_s = a_r;
+    b_s = b_r;
+  }
+  GemmArgs gd = ga;
+  gd.sched = sa.sched_dn;
+  gd.n_tiles_r = sa.n_tiles_dn;
+  gd.n_tiles_s = sa.n_tiles_dn_sh;
+  gd.K_r = F;
+  gd.K_s = Fs;
+  gd.N_r = H;
+  gd.N_s = H;
+  gd.b_rows_r = H;
+  gd.cs0_r = per_channel ? w->down_s : nullptr;
+  gd.cs1_r = nullptr;
+  gd.cs0_s = per_channel ? w->sh_down_s : nullptr;
+  gd.cs1_s = nullptr;
+  gd.out_r = y_perm;
+  gd.out_s = y_sh;
+  gd.ld_r = H;
+  gd.ld_s = H;
+  if (launch_gemm(EPI_STORE, a_r, a_s, b_r, b_s, gd, s) != cudaSuccess) return FLUX_E_CUDA;
+
+  // ---- (f) K6 combine
+  if (launch_combine(T, H, k, residual ? residual : x, sh ? y_sh : nullptr, y_perm, out->topk_w, inv_pos, out->y,
+                     s) != cudaSuccess)
+    return FLUX_E_CUDA;
+  return FLUX_OK;
+}
+
+flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype in_dtype, const void* w, int64_t R,
+                                  int64_t K, void* q, float* s, void* stream) {
+  if (wbits != 4 && wbits != 8) return FLUX_E_UNSUPPORTED;
+  if (in_dtype != FLUX_BF16 && in_dtype != FLUX_FP32) return FLUX_E_INVALID;
+  if (R < 0 || K <= 0 || group_size < 0) return FLUX_E_INVALID;
+  const int64_t g = group_size ? group_size : K;
+  if (K % g || g % 8 || g > 4096) return FLUX_E_UNSUPPORTED;
+  if (R == 0) return FLUX_OK;
+  if (!w || !q || !s || !aligned16(w) || !aligned16(q) || (reinterpret_cast<uintptr_t>(s) & 3)) return FLUX_E_INVALID;
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  return cuda_status(launch_quantize(wbits, g, in_dtype == FLUX_FP32, w, R, K, q, s, (cudaStream_t)stream));
+}
+
+flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t numel, const void* experts,
+                               const int32_t* cluster_of, const float* alpha, int32_t n_clusters, void* merged,
+                               int32_t* remap, void* stream) {
+  if (dtype != FLUX_BF16 && dtype != FLUX_FP32) return FLUX_E_INVALID;
+  if (n_experts < 1 || n_experts > 1024 || n_clusters < 1 || n_clusters > n_experts || numel < 0)
+    return FLUX_E_INVALID;
+  if (numel % 8) return FLUX_E_UNSUPPORTED;
+  if (!experts || !cluster_of || !alpha || !merged || !aligned16(experts) || !aligned16(merged)) return FLUX_E_INVALID;
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  return cuda_status(launch_merge(dtype == FLUX_FP32, n_experts, numel, experts, cluster_of, alpha, n_clusters, merged,
+                                  remap, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// combine.cu — K6: the MoE layer output (reading R6):
+//   y_t = bf16( r_t + sh_t + Σ_j w_tj · o_{t,S_tj} )
+// gather-based (inv_pos from K2), fp32 accumulation in the fixed order
+// residual, shared, j = 0..k-1, one rounding.  One warp per token, 16-byte
+// vectors; every byte is read or written exactly once.
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace flux {
+namespace {
+
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 p = __bfloat1622float2(h[i]);
+    f[2 * i] = p.x;
+    f[2 * i + 1] = p.y;
+  }
+}
+
+__global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, const uint4* __restrict__ residual,
+                                                      const uint4* __restrict__ y_sh, const uint4* __restrict__ y_perm,
+                                                      const float* __restrict__ w, const int32_t* __restrict__ inv_pos,
+                                                      uint4* __restrict__ y) {
+  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const int nvec = H / 8;
+  int pos[8];
+  float wt[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    pos[j] = 0;
+    wt[j] = 0.f;
+    if (j < k) {
+      pos[j] = __ldg(&inv_pos[t * k + j]);
+      wt[j] = __ldg(&w[t * k + j]);
+    }
+  }
+  for (int c = lane; c < nvec; c += 32) {
+    float acc[8], f[8];
+    unpack8(__ldg(&residual[t * nvec + c]), acc);
+    if (y_sh) {
+      unpack8(__ldg(&y_sh[t * nvec + c]), f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += f[i];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < k) {
+        unpack8(__ldg(&y_perm[(int64_t)pos[j] * nvec + c]), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt[j], f[i], acc[i]);
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    y[t * nvec + c] = o;
+  }
+}
+}  // namespace
+
+cudaError_t launch_combine(int64_t T, int H, int k, const void* residual, const void* y_sh, const void* y_perm,
+                           const float* w, const int32_t* inv_pos, void* y, cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)((T + 7) / 8);
+  combine_kernel<<<grid, 256, 0, st>>>(T, H, k, (const uint4*)residual, (const uint4*)y_sh, (const uint4*)y_perm, w,
+                                       inv_pos, (uint4*)y);
+  return cudaGetLastError();
+}
+
+}  // namespace flux

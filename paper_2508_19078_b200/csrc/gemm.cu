@@ -1,0 +1,346 @@
+// gemm.cu — K3/K4/K5: the expert FFNs of the quantized MoE model
+// as grouped GEMMs on the 5th-generation tensor cores.
+//
+//   gate/up (EPI_SWIGLU):  act[r][f] = bf16( SiLU(x_r·ŵg_fᵀ) · (x_r·ŵu_fᵀ) )     (R4)
+//   down    (EPI_STORE):   o[r][h]   = bf16( act_r·ŵd_hᵀ )
+// Groups 0..E-1 are the routed experts (A rows = the expert's D_e segment of
+// x_perm / act, K2), group E the shared MLP (A rows = every token, R5), all in
+// ONE persistent launch per GEMM.  Tile = 128 rows x 256 output columns x 64-K
+// slices; for gate/up the 256 B-rows of a tile are 128 gate rows followed by
+// the 128 matching up rows, so one accumulator holds g and u of the same
+// (row, feature) and SwiGLU is applied in the epilogue.
+//
+// Warp roles (256 threads, 1 CTA/SM, grid = #SMs, static round-robin tiles):
+//   warp 0: TMA producer — A and B 64-wide K slices, 128-byte swizzle, 4-stage ring
+//   warp 1: MMA issuer   — tcgen05.mma M=128 N=256 K=16, fp32 accumulator in TMEM
+//   warp 2: TMEM allocator (512 columns = 2 accumulator stages)
+//   warps 4-7: epilogue  — tcgen05.ld, per-channel scale (INT8), SwiGLU, bf16 store
+// The accumulator is double-buffered so the epilogue of tile i overlaps the
+// MMAs of tile i+1.  Tile shape and K order never depend on the number of
+// tokens, so every output row is computed identically however the batch is
+// split (batch invariance).
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace flux {
+namespace {
+
+constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
+constexpr int kABytes = kBM * kBK * 2;   // 16 KB
+constexpr int kBBytes = kBN * kBK * 2;   // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kMaxGroups = 257;
+constexpr int kThreads = 256;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64;
+
+struct Params {
+  int n_groups, E;
+  const int32_t* sched;
+  const int32_t* grp_row0;
+  const int32_t* grp_rows;
+  int n_tiles_r, n_tiles_s;
+  int K_r, K_s;
+  int N_r, N_s;
+  int b_rows_r;                 // B rows per routed group in the B tensor
+  const float *cs0_r, *cs1_r, *cs0_s, *cs1_s;  // per-channel scales [group][N] or null
+  void *out_r, *out_s;
+  int64_t ld_r, ld_s;
+};
+
+struct TileInfo {
+  int g, m, n;
+};
+
+__device__ __forceinline__ TileInfo decode(int tile, const int32_t* s_sched, int n_groups, int nt_r, int nt_s, int E) {
+  int lo = 0, hi = n_groups - 1;  // largest g with sched[g] <= tile
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_sched[mid] <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  const int nt = lo < E ? nt_r : nt_s;
+  const int local = tile - s_sched[lo];
+  return {lo, local / nt, local % nt};
+}
+
+__device__ __forceinline__ float silu(float v) { return v / (1.0f + expf(-v)); }
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tm_a_r, const __grid_constant__ CUtensorMap tm_a_s,
+                        const __grid_constant__ CUtensorMap tm_b_r, const __grid_constant__ CUtensorMap tm_b_s,
+                        Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;   // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* s_sched = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 256);
+  int32_t* s_row0 = s_sched + kMaxGroups;
+  int32_t* s_rows = s_row0 + kMaxGroups;
+
+  const int warp = warp_id();
+  for (int i = threadIdx.x; i <= p.n_groups; i += kThreads) s_sched[i] = p.sched[i];
+  for (int i = threadIdx.x; i < p.n_groups; i += kThreads) {
+    s_row0[i] = p.grp_row0[i];
+    s_rows[i] = p.grp_rows[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int total = s_sched[p.n_groups];
+  const int nkb_r = (p.K_r + kBK - 1) / kBK, nkb_s = (p.K_s + kBK - 1) / kBK;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch(&tm_a_r);
+      tma_prefetch(&tm_b_r);
+      tma_prefetch(&tm_a_s);
+      tma_prefetch(&tm_b_s);
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+        const bool routed = ti.g < p.E;
+        const int arow = s_row0[ti.g] + ti.m * kBM;
+        const int brow = (routed ? ti.g * p.b_rows_r : 0) + ti.n * kBN;
+        const CUtensorMap* ta = routed ? &tm_a_r : &tm_a_s;
+        const CUtensorMap* tb = routed ? &tm_b_r : &tm_b_s;
+        const int nkb = routed ? nkb_r : nkb_s;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * kStageBytes;
+          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          tma_load_2d(st, ta, &full[s], kb * kBK, arow);
+          tma_load_2d(st + kABytes, tb, &full[s], kb * kBK, brow);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = umma_idesc_bf16(kBM, kBN);
+    uint32_t it = 0, tc = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+      const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+      const int nkb = ti.g < p.E ? nkb_r : nkb_s;
+      const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * kBN;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % kStages;
+        const uint32_t ph = (it / kStages) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + s * kStageBytes);
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + kABytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          umma_commit(&empty[s]);
+          if (kb == nkb - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint32_t tc = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+      const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+      const bool routed = ti.g < p.E;
+      const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int r_local = ti.m * kBM + q * 32 + (int)lane_id();
+      const bool valid = r_local < s_rows[ti.g];
+      const int64_t orow = (int64_t)s_row0[ti.g] + r_local;
+      const int N = routed ? p.N_r : p.N_s;
+      const int64_t ld = routed ? p.ld_r : p.ld_s;
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(routed ? p.out_r : p.out_s) + orow * ld;
+      const float* cs0 = routed ? p.cs0_r : p.cs0_s;
+      const float* cs1 = routed ? p.cs1_r : p.cs1_s;
+      const int64_t cs_base = routed ? (int64_t)ti.g * N : 0;
+      const uint32_t taddr = tmem + acc * kBN + lane_base;
+      if constexpr (EPI == EPI_SWIGLU) {
+        for (int j = 0; j < kBN / 2; j += 16) {
+          const int f0 = ti.n * (kBN / 2) + j;
+          float gv[16], uv[16];
+          tmem_ld16(taddr + j, gv);
+          tmem_ld16(taddr + kBN / 2 + j, uv);
+          tmem_ld_wait();
+          if (f0 >= N) continue;  // warp-uniform (N % 16 == 0)
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            float g0 = gv[i], g1 = gv[i + 1], u0 = uv[i], u1 = uv[i + 1];
+            if (cs0) {
+              g0 *= __ldg(&cs0[cs_base + f0 + i]);
+              g1 *= __ldg(&cs0[cs_base + f0 + i + 1]);
+              u0 *= __ldg(&cs1[cs_base + f0 + i]);
+              u1 *= __ldg(&cs1[cs_base + f0 + i + 1]);
+            }
+            pk[i / 2] = pack_bf16x2(silu(g0) * u0, silu(g1) * u1);
+          }
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(out + f0);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+      } else {
+        for (int j = 0; j < kBN; j += 16) {
+          const int c0 = ti.n * kBN + j;
+          float v[16];
+          tmem_ld16(taddr + j, v);
+          tmem_ld_wait();
+          if (c0 >= N) continue;
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            float a0 = v[i], a1 = v[i + 1];
+            if (cs0) {
+              a0 *= __ldg(&cs0[cs_base + c0 + i]);
+              a1 *= __ldg(&cs0[cs_base + c0 + i + 1]);
+            }
+            pk[i / 2] = pack_bf16x2(a0, a1);
+          }
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(out + c0);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// Dequantization of one weight family into the bf16 B operand layout.
+//   interleave == 1 (gate/up): out[g][2*Fp][K], rows [256n, 256n+128) = gate
+//     features [128n, 128n+128), rows [256n+128, 256n+256) = up features; rows
+//     of features >= F are zero.
+//   interleave == 0: out[g][N][K] = the family as stored.
+//   value = bf16(q) when per_channel (the scale is applied in the GEMM
+//   epilogue, exact), else bf16(q · s[group]).
+// ---------------------------------------------------------------------------
+template <int WBITS>
+__global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict__ q0, const float* __restrict__ s0,
+                                                      const uint8_t* __restrict__ q1, const float* __restrict__ s1,
+                                                      int G, int N, int K, int Fp, int interleave, int gsz,
+                                                      int per_channel, uint4* __restrict__ out) {
+  const int64_t rows_out = interleave ? 2LL * Fp : N;
+  const int64_t vec_per_row = K / 8;
+  const int64_t total = (int64_t)G * rows_out * vec_per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / vec_per_row;
+    const int kv = (int)(i - row * vec_per_row);
+    const int g = (int)(row / rows_out);
+    const int r = (int)(row - (int64_t)g * rows_out);
+    const uint8_t* q = q0;
+    const float* s = s0;
+    int src_row = r;
+    if (interleave) {
+      const int blk = r / 256, w = r % 256;
+      src_row = blk * 128 + (w & 127);
+      if (w >= 128) { q = q1; s = s1; }
+    }
+    uint4 o = make_uint4(0, 0, 0, 0);
+    if (src_row < N) {
+      const int64_t srow = (int64_t)g * N + src_row;
+      int qi[8];
+      if (WBITS == 8) {
+        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(q + srow * K + kv * 8));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          qi[j] = (int)(int8_t)((raw.x >> (8 * j)) & 0xFF);
+          qi[4 + j] = (int)(int8_t)((raw.y >> (8 * j)) & 0xFF);
+        }
+      } else {
+        const uint32_t raw = __ldg(reinterpret_cast<const uint32_t*>(q + srow * (K / 2) + kv * 4));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) qi[j] = ((int)((raw >> (4 * j)) & 0xF) ^ 8) - 8;
+      }
+      // R1b: grouped scales -> ŵ = bf16(q · bf16(s)); q·bf16(s) is exact in fp32 (4-8 bit x 8 bit),
+      // so pack_bf16x2 performs the single rounding.  Per-channel: ŵ = q, scale in the epilogue.
+      const float sc =
+          per_channel ? 1.0f : __bfloat162float(__float2bfloat16_rn(__ldg(&s[srow * (K / gsz) + (kv * 8) / gsz])));
+      o.x = pack_bf16x2((float)qi[0] * sc, (float)qi[1] * sc);
+      o.y = pack_bf16x2((float)qi[2] * sc, (float)qi[3] * sc);
+      o.z = pack_bf16x2((float)qi[4] * sc, (float)qi[5] * sc);
+      o.w = pack_bf16x2((float)qi[6] * sc, (float)qi[7] * sc);
+    }
+    out[i] = o;
+  }
+}
+}  // namespace
+
+cudaError_t launch_dequant(int wbits, const uint8_t* q0, const float* s0, const uint8_t* q1, const float* s1, int G,
+                           int N, int K, int Fp, int interleave, int gsz, int per_channel, void* out,
+                           cudaStream_t st) {
+  const int64_t rows_out = interleave ? 2LL * Fp : N;
+  const int64_t total = (int64_t)G * rows_out * (K / 8);
+  if (total == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+  if (wbits == 8)
+    dequant_kernel<8><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
+  else
+    dequant_kernel<4><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
+                        const CUtensorMap& b_s, const GemmArgs& g, cudaStream_t st) {
+  Params p;
+  p.n_groups = g.n_groups;
+  p.E = g.E;
+  p.sched = g.sched;
+  p.grp_row0 = g.grp_row0;
+  p.grp_rows = g.grp_rows;
+  p.n_tiles_r = g.n_tiles_r;
+  p.n_tiles_s = g.n_tiles_s;
+  p.K_r = g.K_r;
+  p.K_s = g.K_s;
+  p.N_r = g.N_r;
+  p.N_s = g.N_s;
+  p.b_rows_r = g.b_rows_r;
+  p.cs0_r = g.cs0_r;
+  p.cs1_r = g.cs1_r;
+  p.cs0_s = g.cs0_s;
+  p.cs1_s = g.cs1_s;
+  p.out_r = g.out_r;
+  p.out_s = g.out_s;
+  p.ld_r = g.ld_r;
+  p.ld_s = g.ld_s;
+  if (g.n_groups > kMaxGroups - 1) return cudaErrorInvalidValue;
+  auto kern = epi == EPI_SWIGLU ? grouped_gemm_kernel<EPI_SWIGLU> : grouped_gemm_kernel<EPI_STORE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<g.grid, kThreads, kSmemBytes, st>>>(a_r, a_s, b_r, b_s, p);
+  return cudaGetLastError();
+}
+
+}  // namespace flux

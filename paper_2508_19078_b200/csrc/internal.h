@@ -1,0 +1,95 @@
+// internal.h — host-side declarations shared by the libflux translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/flux.h"
+
+namespace flux {
+
+constexpr int kNumSMs = 148;
+
+// TMA descriptor for a row-major 2D tensor [rows][cols] of `elem_bytes` elements,
+// box = box_cols x box_rows, 128-byte swizzle (box_cols * elem_bytes must be 128 or
+// the swizzle must be NONE), out-of-bounds elements read as zero.
+bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint32_t elem_bytes, uint64_t rows,
+                  uint64_t cols, uint64_t row_stride_bytes, uint32_t box_cols, uint32_t box_rows,
+                  CUtensorMapSwizzle swizzle);
+
+inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_OK : FLUX_E_CUDA; }
+
+// ---------------------------------------------------------------- launchers
+// K0 (quantize.cu)
+cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, int64_t R, int64_t K, void* q, float* s,
+                            cudaStream_t st);
+// K7 (merge.cu)
+cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
+                         const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st);
+
+// K1 (router.cu)
+struct RouterArgs {
+  int64_t T;
+  int H, E, k, norm;
+  int32_t* ids;         // [T][k]
+  float* w;             // [T][k]
+  float* logits;        // [T][E] or null
+  int64_t* hist;        // [E] (+=)
+  int32_t* tile_counts; // [n_tiles][E]
+  int32_t* rank;        // [T][k] rank of t inside its 128-token tile among tokens choosing the same expert
+};
+cudaError_t launch_router(const CUtensorMap& tmap_x, const CUtensorMap& tmap_wr, int npad, const RouterArgs& a,
+                          cudaStream_t st);
+
+// K2 (permute.cu)
+struct ScheduleArgs {
+  int E, k;
+  int64_t T;
+  int n_tiles;              // router tiles (128 tokens)
+  const int32_t* tile_counts;
+  int32_t* tile_base;       // [n_tiles][E]
+  int32_t* offsets;         // [E+1] internal
+  int32_t* user_offsets;    // [E+1] or null
+  int32_t* done_counter;    // 1 int, zeroed by the launcher
+  int has_shared;
+  int n_tiles_gu, n_tiles_gu_sh;  // n-tiles of the gate/up GEMM (routed, shared)
+  int n_tiles_dn, n_tiles_dn_sh;  // n-tiles of the down GEMM
+  int32_t* sched_gu;        // [n_groups+1] tile prefix of the gate/up GEMM
+  int32_t* sched_dn;        // [n_groups+1]
+  int32_t* grp_row0;        // [n_groups] first A row of each group
+  int32_t* grp_rows;        // [n_groups] rows of each group
+};
+cudaError_t launch_schedule(const ScheduleArgs& a, cudaStream_t st);
+cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const int32_t* ids, const int32_t* rank,
+                           const int32_t* tile_base, const int32_t* offsets, int32_t* inv_pos, int32_t* token_index,
+                           void* x_perm, cudaStream_t st);
+
+// K6 (combine.cu)
+cudaError_t launch_combine(int64_t T, int H, int k, const void* residual, const void* y_sh, const void* y_perm,
+                           const float* w, const int32_t* inv_pos, void* y, cudaStream_t st);
+
+// K3/K4/K5 (gemm.cu)
+enum GemmEpi { EPI_SWIGLU = 0, EPI_STORE = 1 };
+struct GemmArgs {
+  // groups 0..E-1: routed experts (A = tm_a_r rows grp_row0.., B = tm_b_r rows g*b_rows_r..);
+  // group E (if n_groups > E): the shared MLP (A = tm_a_s, B = tm_b_s)
+  int n_groups, E;
+  const int32_t* sched;     // [n_groups+1] tile prefix (device, written by K2)
+  const int32_t* grp_row0;  // [n_groups] first A row per group (device)
+  const int32_t* grp_rows;  // [n_groups] rows per group (device)
+  int n_tiles_r, n_tiles_s; // n-tiles per group (routed, shared)
+  int K_r, K_s;             // contraction length (routed, shared)
+  int N_r, N_s;             // output features per group
+  int b_rows_r;             // rows of one routed group in the B tensor
+  const float *cs0_r, *cs1_r, *cs0_s, *cs1_s;  // per-channel scales [group][N] or null
+  void *out_r, *out_s;      // bf16 [rows][ld]
+  int64_t ld_r, ld_s;
+  int grid;
+};
+cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
+                        const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);
+cudaError_t launch_dequant(int wbits, const uint8_t* q0, const float* s0, const uint8_t* q1, const float* s1, int G,
+                           int N, int K, int Fp, int interleave, int gsz, int per_channel, void* out,
+                           cudaStream_t st);
+
+}  // namespace flux

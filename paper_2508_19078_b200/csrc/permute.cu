@@ -1,0 +1,165 @@
+// permute.cu — K2: D_e (the tokens routed to each expert) as a
+// deterministic, stable permutation, plus the grouped-GEMM tile schedule.
+//
+//  schedule_kernel  (one CTA per expert): exclusive scan over the router's
+//                   per-tile counts -> tile_base[tile][e]; the last CTA to
+//                   finish (atomic ticket) scans the per-expert totals ->
+//                   offsets[e] and builds the tile prefix of both grouped GEMMs.
+//  scatter_kernel   (one warp per token): pos = offsets[e] + tile_base[tile][e]
+//                   + rank (rank from K1) -> token_index[pos] = t (ascending t
+//                   inside every segment: reading R3), inv_pos[t][j] = pos, and
+//                   the gather x[t] -> x_perm[pos] (16-byte vectors, x read
+//                   once, written k times).
+// No atomics decide positions, so D_e is bitwise reproducible.
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace flux {
+
+namespace {
+constexpr int kGemmBM = 128;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* sh, int& total) {
+  // 256 threads
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < 8 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < 8) sh[lane] = s;
+  }
+  __syncthreads();
+  const int warp_prefix = wid ? sh[wid - 1] : 0;
+  total = sh[7];
+  __syncthreads();
+  return warp_prefix + x - v;
+}
+
+__global__ void __launch_bounds__(256) schedule_kernel(ScheduleArgs a) {
+  __shared__ int sh[8];
+  __shared__ int is_last;
+  const int e = blockIdx.x;
+  // ---- per-expert scan over router tiles (chunks of 256 tiles)
+  int carry = 0;
+  for (int base = 0; base < a.n_tiles; base += 256) {
+    const int tile = base + threadIdx.x;
+    const int v = tile < a.n_tiles ? a.tile_counts[(int64_t)tile * a.E + e] : 0;
+    int tot;
+    const int ex = block_exclusive_scan(v, sh, tot);
+    if (tile < a.n_tiles) a.tile_base[(int64_t)tile * a.E + e] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    a.offsets[e + 1] = carry;  // temporarily the count of expert e
+    __threadfence();
+    const int ticket = atomicAdd(a.done_counter, 1);
+    is_last = ticket == a.E - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // ---- last CTA: offsets (exclusive scan of counts) and GEMM tile schedules
+  const int n_groups = a.E + (a.has_shared ? 1 : 0);
+  int carry_rows = 0, carry_gu = 0, carry_dn = 0;
+  for (int base = 0; base < n_groups; base += 256) {
+    const int g = base + threadIdx.x;
+    int rows = 0, row0 = 0;
+    if (g < a.E) rows = __ldcg(&a.offsets[g + 1]);
+    else if (g < n_groups) rows = (int)a.T;
+    int tot_rows;
+    const int ex_rows = block_exclusive_scan(g < a.E ? rows : 0, sh, tot_rows);
+    row0 = g < a.E ? carry_rows + ex_rows : 0;
+    const int mt = (rows + kGemmBM - 1) / kGemmBM;
+    const int ngu = mt * (g < a.E ? a.n_tiles_gu : a.n_tiles_gu_sh);
+    const int ndn = mt * (g < a.E ? a.n_tiles_dn : a.n_tiles_dn_sh);
+    int tot_gu, tot_dn;
+    const int ex_gu = block_exclusive_scan(g < n_groups ? ngu : 0, sh, tot_gu);
+    const int ex_dn = block_exclusive_scan(g < n_groups ? ndn : 0, sh, tot_dn);
+    if (g < n_groups) {
+      a.grp_row0[g] = row0;
+      a.grp_rows[g] = rows;
+      a.sched_gu[g] = carry_gu + ex_gu;
+      a.sched_dn[g] = carry_dn + ex_dn;
+    }
+    carry_rows += tot_rows;
+    carry_gu += tot_gu;
+    carry_dn += tot_dn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.sched_gu[n_groups] = carry_gu;
+    a.sched_dn[n_groups] = carry_dn;
+  }
+  for (int g = threadIdx.x; g <= a.E; g += 256) {
+    const int off = g < a.E ? a.grp_row0[g] : carry_rows;
+    a.offsets[g] = off;
+    if (a.user_offsets) a.user_offsets[g] = off;
+  }
+}
+
+__global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ x, int64_t T, int H, int E, int k,
+                                                      const int32_t* __restrict__ ids, const int32_t* __restrict__ rank,
+                                                      const int32_t* __restrict__ tile_base,
+                                                      const int32_t* __restrict__ offsets, int32_t* __restrict__ inv_pos,
+                                                      int32_t* __restrict__ token_index, uint4* __restrict__ x_perm) {
+  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const int tile = (int)(t / 128);
+  int pos[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    pos[j] = 0;
+    if (j < k) {
+      const int e = __ldg(&ids[t * k + j]);
+      pos[j] = __ldg(&offsets[e]) + __ldg(&tile_base[(int64_t)tile * E + e]) + __ldg(&rank[t * k + j]);
+    }
+  }
+  if (lane < k) {
+    int p = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j == lane) p = pos[j];
+    inv_pos[t * k + lane] = p;
+    token_index[p] = (int32_t)t;
+  }
+  const int nvec = H / 8;  // 16-byte vectors per row
+  const uint4* src = x + t * nvec;
+  for (int c = lane; c < nvec; c += 32) {
+    const uint4 v = __ldg(&src[c]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < k) x_perm[(int64_t)pos[j] * nvec + c] = v;
+  }
+}
+}  // namespace
+
+cudaError_t launch_schedule(const ScheduleArgs& a, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(a.done_counter, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return e;
+  schedule_kernel<<<a.E, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const int32_t* ids, const int32_t* rank,
+                           const int32_t* tile_base, const int32_t* offsets, int32_t* inv_pos, int32_t* token_index,
+                           void* x_perm, cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)((T + 7) / 8);
+  scatter_kernel<<<grid, 256, 0, st>>>((const uint4*)x, T, H, E, k, ids, rank, tile_base, offsets, inv_pos,
+                                       token_index, (uint4*)x_perm);
+  return cudaGetLastError();
+}
+
+}  // namespace flux

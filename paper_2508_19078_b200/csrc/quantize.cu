@@ -1,0 +1,129 @@
+// quantize.cu — K0: the participant's low-bit copy of the model (P:556-565,
+// "quantize and profile the latest MoE model ... in each round" P:613-615),
+// bit level chosen per participant.  Reading R1: symmetric, per
+// row, groups of g along K:
+//   s = fl32(max|w| / qmax),  q = clamp(RNE(fl32(w / s)), -qmax-1, qmax),  s == 0 -> q = 0
+// IEEE division (__fdiv_rn) and round-to-nearest-even conversion, so the
+// result is bit-identical to any correct implementation of that definition.
+// INT4 output is packed two per byte, even k in the low nibble.
+//
+// HBM-bound: a team of lanes owns one (row, group); every lane loads 16 B
+// vectors of the group once into registers, the team max-reduces with
+// shuffles, then each lane writes its 4 (INT4) or 8 (INT8) output bytes.
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace flux {
+namespace {
+
+template <bool F32IN>
+__device__ __forceinline__ void load8(const void* w, int64_t elem, float (&f)[8]) {
+  if constexpr (F32IN) {
+    const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(w) + elem);
+    float4 a = __ldg(p), b = __ldg(p + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  } else {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(w) + elem));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 p = __bfloat1622float2(h[i]);
+      f[2 * i] = p.x;
+      f[2 * i + 1] = p.y;
+    }
+  }
+}
+
+// TS lanes per (row, group), CPL 8-element chunks per lane.
+template <int WBITS, bool F32IN, int TS, int CPL>
+__global__ void __launch_bounds__(256) quantize_kernel(const void* __restrict__ w, int64_t R, int64_t K, int64_t g,
+                                                       uint8_t* __restrict__ q, float* __restrict__ s) {
+  constexpr int qmax = (1 << (WBITS - 1)) - 1;
+  const int64_t G = K / g;
+  const int64_t n_items = R * G;
+  const int nchunks = (int)(g / 8);
+  const int lane_t = threadIdx.x % TS;
+  const int64_t team0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TS;
+  const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) / TS;
+  for (int64_t item = team0; item < n_items; item += nteams) {
+    const int64_t row = item / G, grp = item - row * G;
+    const int64_t base = row * K + grp * g;
+    float v[CPL][8];
+    float amax = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = lane_t + i * TS;
+      if (c < nchunks) {
+        load8<F32IN>(w, base + c * 8, v[i]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fabsf(v[i][j]));
+      }
+    }
+#pragma unroll
+    for (int o = TS / 2; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o, TS));
+    const float sc = __fdiv_rn(amax, (float)qmax);
+    if (lane_t == 0) s[item] = sc;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = lane_t + i * TS;
+      if (c >= nchunks) continue;
+      int qi[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int t = 0;
+        if (sc != 0.f) {
+          t = __float2int_rn(__fdiv_rn(v[i][j], sc));
+          t = max(-qmax - 1, min(qmax, t));
+        }
+        qi[j] = t;
+      }
+      if constexpr (WBITS == 8) {
+        uint2 o;
+        o.x = (qi[0] & 0xFF) | ((qi[1] & 0xFF) << 8) | ((qi[2] & 0xFF) << 16) | ((uint32_t)(qi[3] & 0xFF) << 24);
+        o.y = (qi[4] & 0xFF) | ((qi[5] & 0xFF) << 8) | ((qi[6] & 0xFF) << 16) | ((uint32_t)(qi[7] & 0xFF) << 24);
+        *reinterpret_cast<uint2*>(q + base + c * 8) = o;
+      } else {
+        uint32_t o = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o |= (uint32_t)(qi[j] & 0xF) << (4 * j);
+        *reinterpret_cast<uint32_t*>(q + (base + c * 8) / 2) = o;
+      }
+    }
+  }
+}
+
+template <int WBITS, bool F32IN>
+cudaError_t dispatch(int64_t g, const void* w, int64_t R, int64_t K, void* q, float* s, cudaStream_t st) {
+  const int64_t nch = g / 8;
+  const int64_t items = R * (K / g);
+  auto grid_for = [&](int ts) {
+    int64_t teams_per_block = 256 / ts;
+    int64_t b = (items + teams_per_block - 1) / teams_per_block;
+    return (unsigned)std::min<int64_t>(b, (int64_t)kNumSMs * 16);
+  };
+  uint8_t* qq = (uint8_t*)q;
+#define QLAUNCH(TS, CPL) \
+  quantize_kernel<WBITS, F32IN, TS, CPL><<<grid_for(TS), 256, 0, st>>>(w, R, K, g, qq, s)
+  if (nch == 8) QLAUNCH(8, 1);
+  else if (nch == 16) QLAUNCH(16, 1);
+  else if (nch <= 32) QLAUNCH(32, 1);
+  else if (nch <= 64) QLAUNCH(32, 2);
+  else if (nch <= 128) QLAUNCH(32, 4);
+  else if (nch <= 256) QLAUNCH(32, 8);
+  else if (nch <= 512) QLAUNCH(32, 16);
+  else return cudaErrorInvalidValue;
+#undef QLAUNCH
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, int64_t R, int64_t K, void* q, float* s,
+                            cudaStream_t st) {
+  if (R == 0) return cudaSuccess;
+  if (wbits == 8)
+    return in_fp32 ? dispatch<8, true>(g, w, R, K, q, s, st) : dispatch<8, false>(g, w, R, K, q, s, st);
+  return in_fp32 ? dispatch<4, true>(g, w, R, K, q, s, st) : dispatch<4, false>(g, w, R, K, q, s, st);
+}
+
+}  // namespace flux

@@ -1,0 +1,187 @@
+"""driver — the participant-side round of the Flux hot path on one GPU (H2).
+
+One profiling round (paper §4.1-4.2, §5.3; Fig. 7):
+  a0  quantize the current model   flux_quantize_weights
+  a1-a6  profile local tokens through all layers   flux_profile_layer per layer
+  a7  reduce the expert histograms over the box   flux_reduce_stats
+  a8-pre per-layer merge budget, eq.(1)   flux_layer_budget (optional)
+  a8  merge the non-tuning experts, eq.(2)   flux_merge_experts
+This module owns buffers and sequencing only; all arithmetic is in libflux.
+Layer chaining (R7): x_{l+1} = y_l (the path carries no attention/norm weights).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import (FLUX_OK, Comm, LayerOut, QLayer, layer_budget, make_cfg, merge_experts, profile_layer,
+               profile_layer_workspace, quantize_weights)
+
+
+@dataclass
+class ModelShape:
+    n_layers: int
+    hidden: int
+    n_experts: int
+    top_k: int
+    ffn: int
+    shared_ffn: int
+    wbits: int
+    group_size: int
+    norm_topk: int
+
+    @staticmethod
+    def of(cfg) -> "ModelShape":
+        return ModelShape(cfg.n_layers, cfg.hidden, cfg.n_experts, cfg.top_k, cfg.ffn, cfg.shared_ffn, cfg.wbits,
+                          cfg.group_size, cfg.norm_topk)
+
+    def ccfg(self):
+        return make_cfg(self.hidden, self.ffn, self.n_experts, self.top_k, self.shared_ffn, self.wbits,
+                        self.group_size, self.norm_topk)
+
+
+@dataclass
+class MasterWeights:
+    """Full-precision (bf16) model on the device, family-major:
+    router [L][E][H]; gate/up [L][E][F][H]; down [L][E][H][F]; sh_gate/sh_up [L][Fs][H]; sh_down [L][H][Fs]."""
+    shape: ModelShape
+    router: torch.Tensor
+    gate: torch.Tensor
+    up: torch.Tensor
+    down: torch.Tensor
+    sh_gate: torch.Tensor | None = None
+    sh_up: torch.Tensor | None = None
+    sh_down: torch.Tensor | None = None
+
+    @staticmethod
+    def empty(shape: ModelShape, device="cuda", dtype=torch.bfloat16) -> "MasterWeights":
+        L, E, H, F, Fs = shape.n_layers, shape.n_experts, shape.hidden, shape.ffn, shape.shared_ffn
+        mk = lambda *s: torch.empty(*s, dtype=dtype, device=device)  # noqa: E731
+        return MasterWeights(shape, mk(L, E, H), mk(L, E, F, H), mk(L, E, F, H), mk(L, E, H, F),
+                             mk(L, Fs, H) if Fs else None, mk(L, Fs, H) if Fs else None,
+                             mk(L, H, Fs) if Fs else None)
+
+
+class QuantizedModel:
+    """Canonical quantized weights (include/flux.h flux_qlayer) for all layers, on the device."""
+
+    def __init__(self, shape: ModelShape, device="cuda"):
+        self.shape = s = shape
+        L, E, H, F, Fs = s.n_layers, s.n_experts, s.hidden, s.ffn, s.shared_ffn
+        qdiv = 2 if s.wbits == 4 else 1
+        qdt = torch.uint8 if s.wbits == 4 else torch.int8
+        gh = s.group_size or H
+        gf = s.group_size or F
+        gfs = s.group_size or (Fs or 1)
+        self.router = torch.empty(L, E, H, dtype=torch.bfloat16, device=device)
+        self.gate_q = torch.empty(L, E, F, H // qdiv, dtype=qdt, device=device)
+        self.up_q = torch.empty(L, E, F, H // qdiv, dtype=qdt, device=device)
+        self.down_q = torch.empty(L, E, H, F // qdiv, dtype=qdt, device=device)
+        self.gate_s = torch.empty(L, E, F, H // gh, dtype=torch.float32, device=device)
+        self.up_s = torch.empty(L, E, F, H // gh, dtype=torch.float32, device=device)
+        self.down_s = torch.empty(L, E, H, F // gf, dtype=torch.float32, device=device)
+        if Fs:
+            self.sh_gate_q = torch.empty(L, Fs, H // qdiv, dtype=qdt, device=device)
+            self.sh_up_q = torch.empty(L, Fs, H // qdiv, dtype=qdt, device=device)
+            self.sh_down_q = torch.empty(L, H, Fs // qdiv, dtype=qdt, device=device)
+            self.sh_gate_s = torch.empty(L, Fs, H // gh, dtype=torch.float32, device=device)
+            self.sh_up_s = torch.empty(L, Fs, H // gh, dtype=torch.float32, device=device)
+            self.sh_down_s = torch.empty(L, H, Fs // gfs, dtype=torch.float32, device=device)
+        else:
+            self.sh_gate_q = self.sh_up_q = self.sh_down_q = None
+            self.sh_gate_s = self.sh_up_s = self.sh_down_s = None
+
+    def quantize_from(self, m: MasterWeights, stream=None):
+        """a0: quantize every expert matrix of the master model (router copied: not quantized, R1)."""
+        s = self.shape
+        self.router.copy_(m.router)
+        pairs = [(m.gate, self.gate_q, self.gate_s), (m.up, self.up_q, self.up_s), (m.down, self.down_q, self.down_s)]
+        if s.shared_ffn:
+            pairs += [(m.sh_gate, self.sh_gate_q, self.sh_gate_s), (m.sh_up, self.sh_up_q, self.sh_up_s),
+                      (m.sh_down, self.sh_down_q, self.sh_down_s)]
+        for w, q, sc in pairs:
+            quantize_weights(w, s.wbits, s.group_size, q, sc, stream)
+
+    def qlayer(self, l: int) -> QLayer:
+        p = lambda t: None if t is None else t[l].data_ptr()  # noqa: E731
+        return QLayer(p(self.router), p(self.gate_q), p(self.up_q), p(self.down_q), p(self.gate_s), p(self.up_s),
+                      p(self.down_s), p(self.sh_gate_q), p(self.sh_up_q), p(self.sh_down_q), p(self.sh_gate_s),
+                      p(self.sh_up_s), p(self.sh_down_s))
+
+
+class Profiler:
+    """Buffers for profiling T tokens through all layers (a1-a6) on one GPU."""
+
+    def __init__(self, shape: ModelShape, T: int, device="cuda", with_de: bool = True, with_logits: bool = False):
+        s = self.shape = shape
+        self.T = T
+        L, E, H, k = s.n_layers, s.n_experts, s.hidden, s.top_k
+        self.cfg = s.ccfg()
+        self.ws = torch.empty(max(profile_layer_workspace(self.cfg, T), 1), dtype=torch.uint8, device=device)
+        self.y = torch.empty(2, T, H, dtype=torch.bfloat16, device=device)
+        self.ids = torch.empty(L, T, k, dtype=torch.int32, device=device)
+        self.w = torch.empty(L, T, k, dtype=torch.float32, device=device)
+        self.hist = torch.zeros(L, E, dtype=torch.int64, device=device)
+        self.offsets = torch.empty(L, E + 1, dtype=torch.int32, device=device) if with_de else None
+        self.token_index = torch.empty(L, T * k, dtype=torch.int32, device=device) if with_de else None
+        self.logits = torch.empty(L, T, E, dtype=torch.float32, device=device) if with_logits else None
+
+    def out(self, l: int) -> LayerOut:
+        p = lambda t: None if t is None else t[l].data_ptr()  # noqa: E731
+        return LayerOut(self.y[l % 2].data_ptr(), p(self.ids), p(self.w), p(self.hist), p(self.offsets),
+                        p(self.token_index), p(self.logits))
+
+    def run(self, qm: QuantizedModel, x: torch.Tensor, stream=None, on_layer=None, zero_hist: bool = True):
+        """Profile x [T][H] (bf16, device) through every layer; returns the last layer's y."""
+        if zero_hist:
+            self.hist.zero_()
+        cur = x
+        for l in range(self.shape.n_layers):
+            profile_layer(self.cfg, qm.qlayer(l), cur, None, self.T, self.out(l), self.ws, stream)
+            cur = self.y[l % 2]
+            if on_layer is not None:
+                on_layer(l, cur)
+        return cur
+
+
+def frequencies(hist_host: np.ndarray, T_total: int) -> np.ndarray:
+    """Activation frequency f = activated tokens / total tokens, fp64 on the host."""
+    return hist_host.astype(np.float64) / float(T_total)
+
+
+@dataclass
+class MergedModel:
+    gate: torch.Tensor
+    up: torch.Tensor
+    down: torch.Tensor
+    remap: torch.Tensor
+
+
+def merge_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tensor, n_clusters: int,
+                out: MergedModel | None = None, stream=None) -> MergedModel:
+    """a8: eq.(2) for every layer and weight family. alpha fp32 [L][E], cluster_of int32 [L][E] (device)."""
+    s = m.shape
+    L, E, F, H, C = s.n_layers, s.n_experts, s.ffn, s.hidden, n_clusters
+    if out is None:
+        dev = m.gate.device
+        out = MergedModel(torch.empty(L, C, F, H, dtype=m.gate.dtype, device=dev),
+                          torch.empty(L, C, F, H, dtype=m.gate.dtype, device=dev),
+                          torch.empty(L, C, H, F, dtype=m.gate.dtype, device=dev),
+                          torch.empty(L, E, dtype=torch.int32, device=dev))
+    for l in range(L):
+        merge_experts(m.gate[l].view(E, -1), cluster_of[l], alpha[l], C, out.gate[l].view(C, -1), out.remap[l],
+                      stream)
+        merge_experts(m.up[l].view(E, -1), cluster_of[l], alpha[l], C, out.up[l].view(C, -1), None, stream)
+        merge_experts(m.down[l].view(E, -1), cluster_of[l], alpha[l], C, out.down[l].view(C, -1), None, stream)
+    return out
+
+
+def budgets(hist_host: np.ndarray, T_total: int, B_non: int, n_non=None):
+    """a8-pre: eq.(1) layer budgets from the reduced histogram (host, libflux)."""
+    return layer_budget(hist_host, T_total, B_non, n_non)
+
+
+__all__ = ["ModelShape", "MasterWeights", "QuantizedModel", "Profiler", "MergedModel", "merge_model", "frequencies",
+           "budgets", "Comm", "FLUX_OK"]

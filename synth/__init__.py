@@ -129,6 +129,23 @@ def spec_expert(cfg: MoEConfig, layer: int, expert: int, which: str):
     raise ValueError(which)
 
 
+def cluster_assignment(cfg: MoEConfig, n_clusters: int, n_tuning: int = 0) -> np.ndarray:
+    """Seeded balanced partition of every layer's experts into n_clusters (cluster_of [L][E] int32).
+
+    The clustering step itself (§5.2, PCA + K-Means) is not on this path: cluster_of is an
+    input of the merge.  The first n_tuning experts of each layer's random order are tuning
+    experts (-1), the rest are dealt round-robin to clusters 0..C-1 (M4: 64 -> 16, 4 per cluster).
+    """
+    rng = np.random.default_rng(cfg.seed ^ 0x5EED)
+    out = np.empty((cfg.n_layers, cfg.n_experts), np.int32)
+    for l in range(cfg.n_layers):
+        order = rng.permutation(cfg.n_experts)
+        out[l, order[:n_tuning]] = -1
+        rest = order[n_tuning:]
+        out[l, rest] = np.arange(len(rest)) % n_clusters
+    return out
+
+
 # --------------------------------------------------------------------------------------
 # CPU twin
 # --------------------------------------------------------------------------------------

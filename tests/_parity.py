@@ -1,0 +1,102 @@
+"""Shared helpers for the GPU-vs-oracle parity tests.
+
+The parity contract (from BASELINE.json's north_star):
+  * quantized weights: bit-exact
+  * router logits: per token ||z_gpu - z_ref||_inf <= 1e-3 * ||z_ref||_inf
+  * routing: margin m_t = z_(k) - z_(k+1) (oracle fp64 logits).  m_t > 1e-3: the
+    GPU's set equals the oracle's; otherwise the GPU set must be valid:
+    min chosen z_ref >= max unchosen z_ref - 1e-3
+  * gate weights: relative 1e-3 on margin-clear tokens
+  * layer outputs (bf16): per token ||y_gpu - y_ref||_2 <= 2e-2 ||y_ref||_2 on
+    margin-clear tokens
+  * histograms: hist == bincount(GPU ids) exactly; equal to the oracle's on
+    margin-clear tokens
+Tokens are followed free-running through the layers: the oracle sees only x_0
+and the weights.  A token whose (valid, near-tie) routing differs from the
+oracle's stops being compared at the following layers.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+MARGIN = 1e-3
+LOGIT_TOL = 1e-3
+W_TOL = 1e-3
+Y_TOL = 2e-2
+
+
+class LayerReport:
+    def __init__(self):
+        self.n_cmp = 0
+        self.n_tie = 0
+        self.n_div = 0
+
+
+def input_bound(x_gpu, x_ref, wr):
+    """Free-running layers: the router is linear, so a difference in its input (the previous
+    layer's bf16 output, within the 2e-2 output tolerance) moves logit e by at most
+    Σ_d |W_r[e][d]|·|x_gpu[d] - x_ref[d]|.  Zero at layer 0 (identical generated inputs)."""
+    if x_gpu is None:
+        return np.zeros((x_ref.shape[0], wr.shape[0]))
+    return np.abs(x_gpu.astype(np.float64) - x_ref) @ np.abs(wr.astype(np.float64)).T
+
+
+def compare_layer(l, ref, gpu, alive, dz=None):
+    """ref: oracle dict (x, z, ids, w, y, margin); gpu: dict of numpy arrays (logits, ids, w, y) for the
+    same tokens; dz: input_bound() [T][E] or None.  alive: bool mask, updated in place."""
+    rep = LayerReport()
+    z_ref, z_gpu = ref["z"], gpu["logits"]
+    k = ref["ids"].shape[1]
+    if dz is None:
+        dz = np.zeros_like(z_ref)
+    idx = np.nonzero(alive)[0]
+    rep.n_cmp = len(idx)
+    for t in idx:
+        zr = z_ref[t]
+        err = np.abs(z_gpu[t] - zr)
+        assert np.all(err <= LOGIT_TOL * max(np.max(np.abs(zr)), 1e-30) + dz[t]), (l, t, err.max(), dz[t].max())
+        s_ref, s_gpu = set(ref["ids"][t]), set(gpu["ids"][t].tolist())
+        assert len(s_gpu) == k, (l, t, gpu["ids"][t])
+        eff = MARGIN + 2 * dz[t].max()
+        clear = ref["margin"][t] > eff
+        if clear:
+            assert s_gpu == s_ref, (l, t, s_gpu, s_ref, ref["margin"][t])
+            order = np.argsort(ref["ids"][t])
+            order_g = np.argsort(gpu["ids"][t])
+            wr = ref["w"][t][order]
+            wg = gpu["w"][t][order_g]
+            assert np.all(np.abs(wg - wr) <= (W_TOL + 2 * dz[t].max()) * np.abs(wr) + 1e-9), (l, t, wg, wr)
+            yr, yg = ref["y"][t], gpu["y"][t]
+            assert np.linalg.norm(yg - yr) <= Y_TOL * np.linalg.norm(yr), (l, t, np.linalg.norm(yg - yr) /
+                                                                          np.linalg.norm(yr))
+        else:
+            rep.n_tie += 1
+            chosen = [zr[e] for e in s_gpu]
+            unchosen = [zr[e] for e in range(len(zr)) if e not in s_gpu]
+            if unchosen:
+                assert min(chosen) >= max(unchosen) - eff, (l, t)
+            if s_gpu != s_ref:
+                rep.n_div += 1
+                alive[t] = False
+            else:
+                yr, yg = ref["y"][t], gpu["y"][t]
+                assert np.linalg.norm(yg - yr) <= Y_TOL * np.linalg.norm(yr)
+    return rep
+
+
+def check_hist_and_de(ids_gpu, hist_gpu, offsets_gpu, token_index_gpu, E):
+    """Properties that hold at any size: hist == bincount(ids), D_e CSR is the stable grouping."""
+    T, k = ids_gpu.shape
+    cnt = np.bincount(ids_gpu.ravel(), minlength=E)
+    assert np.array_equal(hist_gpu, cnt)
+    assert hist_gpu.sum() == T * k
+    # every token's k experts are distinct
+    s = np.sort(ids_gpu, axis=1)
+    assert np.all(s[:, 1:] != s[:, :-1]) if k > 1 else True
+    if offsets_gpu is None:
+        return
+    assert offsets_gpu[0] == 0 and np.array_equal(np.diff(offsets_gpu), cnt)
+    # stable grouping: for each expert, the ascending token ids that chose it
+    order = np.argsort(ids_gpu.ravel(), kind="stable")
+    want = (order // k).astype(np.int32)
+    assert np.array_equal(token_index_gpu, want)

@@ -1,0 +1,170 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Inputs reach the oracle only through the CPU twin of the
+generator; nothing the CUDA path computes is fed to the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import oracle.model as om
+import synth
+
+from _parity import check_hist_and_de, compare_layer, input_bound
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _bits_bf16(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+# small configs the oracle finishes in seconds that still span several tiles + ragged tails
+SMALL = {
+    "toy": synth.CONFIGS["toy"],
+    "int4_shared": synth.MoEConfig("mid_int4_shared", 2, 256, 16, 4, 192, 384, 4, 64, 0, 1000, synth.BASE_SEED + 11),
+    "int8_ragged": synth.MoEConfig("mid_int8", 2, 128, 12, 3, 80, 0, 8, 0, 1, 777, synth.BASE_SEED + 12),
+    "int4_e64": synth.MoEConfig("e64_int4", 1, 128, 64, 6, 128, 256, 4, 128, 0, 650, synth.BASE_SEED + 13),
+}
+
+
+def _run_gpu(cfg, T=None):
+    import paper_2508_19078_b200 as F  # noqa: F401
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
+    from paper_2508_19078_b200 import synthetic
+    T = T or cfg.tokens
+    masters = synthetic.master_weights(cfg)
+    qm = QuantizedModel(ModelShape.of(cfg))
+    qm.quantize_from(masters)
+    prof = Profiler(ModelShape.of(cfg), T, with_logits=True)
+    x = synthetic.tokens(cfg, 0, T)
+    ys = []
+    prof.run(qm, x, on_layer=lambda l, y: ys.append(y.float().cpu().numpy()))
+    torch.cuda.synchronize()
+    return masters, qm, prof, ys
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_quantized_weights_bit_exact(name):
+    cfg = SMALL[name]
+    masters, qm, prof, ys = _run_gpu(cfg, T=1)
+    for l in range(cfg.n_layers):
+        for e in [0, cfg.n_experts - 1]:
+            for fam, q_t, s_t in (("gate", qm.gate_q, qm.gate_s), ("up", qm.up_q, qm.up_s),
+                                  ("down", qm.down_q, qm.down_s)):
+                w = om.master_f32(synth.spec_expert(cfg, l, e, fam))
+                q, s = oracle.quantize(w, cfg.wbits, cfg.group_size)
+                qq = oracle.pack_int4(q) if cfg.wbits == 4 else q
+                assert np.array_equal(q_t[l, e].cpu().numpy().view(np.uint8), qq.view(np.uint8)), (l, e, fam)
+                assert np.array_equal(s_t[l, e].cpu().numpy(), s), (l, e, fam)
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_profile_pass_parity(name):
+    cfg = SMALL[name]
+    masters, qm, prof, ys = _run_gpu(cfg)
+    ref = om.profile_all(cfg)
+    T = cfg.tokens
+    alive = np.ones(T, bool)
+    for l in range(cfg.n_layers):
+        gpu = dict(logits=prof.logits[l].cpu().numpy(), ids=prof.ids[l].cpu().numpy(), w=prof.w[l].cpu().numpy(),
+                   y=ys[l])
+        wr = om.master_f32(synth.spec_router(cfg, l))
+        dz = input_bound(ys[l - 1] if l else None, ref[l]["x"], wr)
+        rep = compare_layer(l, ref[l], gpu, alive, dz)
+        assert rep.n_cmp > 0.9 * T
+        check_hist_and_de(gpu["ids"], prof.hist[l].cpu().numpy(), prof.offsets[l].cpu().numpy(),
+                          prof.token_index[l].cpu().numpy(), cfg.n_experts)
+        if rep.n_div == 0 and np.all(alive):
+            assert np.array_equal(prof.hist[l].cpu().numpy(), ref[l]["hist"])
+            assert np.array_equal(prof.token_index[l].cpu().numpy(), ref[l]["token_index"])
+            assert np.array_equal(prof.offsets[l].cpu().numpy(), ref[l]["offsets"])
+
+
+def test_chunk_and_run_invariance():
+    """Batch invariance: hist/ids/y do not depend on how the tokens are split; reruns are bitwise equal."""
+    cfg = SMALL["int4_shared"]
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
+    from paper_2508_19078_b200 import synthetic
+    shape = ModelShape.of(cfg)
+    qm = QuantizedModel(shape)
+    qm.quantize_from(synthetic.master_weights(cfg))
+    T = cfg.tokens
+    full = Profiler(shape, T, with_logits=True)
+    full.run(qm, synthetic.tokens(cfg, 0, T))
+    y_full = full.y[(cfg.n_layers - 1) % 2].clone()
+    again = Profiler(shape, T, with_logits=True)
+    again.run(qm, synthetic.tokens(cfg, 0, T))
+    assert torch.equal(full.ids, again.ids) and torch.equal(full.hist, again.hist)
+    assert torch.equal(y_full, again.y[(cfg.n_layers - 1) % 2])
+    cut = 389  # ragged split, not a multiple of 128
+    a = Profiler(shape, cut)
+    b = Profiler(shape, T - cut)
+    a.run(qm, synthetic.tokens(cfg, 0, cut))
+    b.run(qm, synthetic.tokens(cfg, cut, T - cut))
+    assert torch.equal(a.hist + b.hist, full.hist)
+    assert torch.equal(torch.cat([a.ids, b.ids], 1), full.ids)
+    ya, yb = a.y[(cfg.n_layers - 1) % 2], b.y[(cfg.n_layers - 1) % 2]
+    assert torch.equal(torch.cat([ya, yb]), y_full)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("variant", ["balanced", "tuning", "zero_alpha", "singletons"])
+def test_merge_parity(dtype, variant):
+    import paper_2508_19078_b200 as F
+    rng = np.random.default_rng(hash((dtype, variant)) % 2**32)
+    cfg = synth.CONFIGS["toy"]
+    E, C = 12, 4
+    numel = 64 * 96
+    W = np.stack([synth.cpu_matrix(synth.Spec(64, 96, cfg.seed, synth.stream_id(synth.KIND_MASTER_F32, 0, e),
+                                              synth.scale_c(1.0), 0, 0.0), dtype=dtype) for e in range(E)])
+    Wf = W.astype(np.float32) if dtype == "f32" else synth.bf16_bits_to_f32(W)
+    cl = (np.arange(E) % C).astype(np.int32)
+    alpha = rng.uniform(0.01, 1.0, E).astype(np.float32)
+    if variant == "tuning":
+        cl[[1, 7]] = -1
+    if variant == "zero_alpha":
+        alpha[cl == 2] = 0
+    if variant == "singletons":
+        C = E
+        cl = np.arange(E, dtype=np.int32)
+    ref, remap_ref = oracle.merge(Wf.reshape(E, numel).astype(np.float64), cl, alpha.astype(np.float64), C)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    dev_W = torch.from_numpy(Wf.reshape(E, numel)).to("cuda", tdt)
+    out = torch.empty(C, numel, dtype=tdt, device="cuda")
+    remap = torch.empty(E, dtype=torch.int32, device="cuda")
+    F.merge_experts(dev_W, torch.from_numpy(cl).cuda(), torch.from_numpy(alpha).cuda(), C, out, remap)
+    got = out.float().cpu().numpy().astype(np.float64)
+    assert np.array_equal(remap.cpu().numpy(), remap_ref)
+    # condition-aware bound: |Δ| <= tol * Σ_e w_e |W_e|
+    absw = np.zeros_like(ref)
+    for c in range(C):
+        mem = np.nonzero(cl == c)[0]
+        a = alpha[mem].astype(np.float64)
+        wts = a / a.sum() if a.sum() > 0 else np.full(len(mem), 1.0 / len(mem))
+        absw[c] = (wts[:, None] * np.abs(Wf.reshape(E, numel)[mem].astype(np.float64))).sum(0)
+    tol = 1e-5 if dtype == "f32" else 2e-2
+    assert np.all(np.abs(got - ref) <= tol * absw + 1e-30)
+    if dtype == "bf16":  # expected within one bf16 rounding of the exact value
+        assert np.mean(got == oracle.bf16_round(ref)) > 0.99
+    if variant == "singletons":
+        assert torch.equal(out, dev_W)  # |E_c| = 1 -> identity, bit for bit
+
+
+def test_quantizer_direct_bit_exact():
+    import paper_2508_19078_b200 as F
+    rng = np.random.default_rng(3)
+    for wbits, g, dt in [(8, 0, "bf16"), (4, 128, "bf16"), (4, 64, "f32"), (8, 64, "f32"), (4, 0, "bf16")]:
+        R, K = 37, 640
+        w = (rng.standard_normal((R, K)) * rng.uniform(0.001, 10, (R, 1))).astype(np.float32)
+        w[5] = 0
+        if dt == "bf16":
+            w = oracle.bf16_round(w).astype(np.float32)
+        q_ref, s_ref = oracle.quantize(w, wbits, g)
+        tw = torch.from_numpy(w).cuda().to(torch.bfloat16 if dt == "bf16" else torch.float32)
+        q = torch.empty(R, K // (2 if wbits == 4 else 1), dtype=torch.uint8, device="cuda")
+        s = torch.empty(R, K // (g or K), dtype=torch.float32, device="cuda")
+        F.quantize_weights(tw, wbits, g, q, s)
+        qq = oracle.pack_int4(q_ref) if wbits == 4 else q_ref.view(np.uint8)
+        assert np.array_equal(q.cpu().numpy(), qq), (wbits, g, dt)
+        assert np.array_equal(s.cpu().numpy(), s_ref), (wbits, g, dt)

@@ -32,9 +32,14 @@ def _rand_expert(rng, H, F, wbits, g, scale=1.0):
     return oracle.QExpert(*mats)
 
 
-def _deq(q, s):
+def _deq(q, s, grouped):
+    """Reading R1b, restated with torch's own bf16 conversions: grouped -> bf16(q * bf16(s)); per channel -> q*s."""
     g = q.shape[1] // s.shape[1]
-    return q.astype(np.float64) * np.repeat(s.astype(np.float64), g, axis=1)
+    srep = np.repeat(s, g, axis=1)
+    if not grouped:
+        return q.astype(np.float64) * srep.astype(np.float64)
+    sb = torch.from_numpy(srep).to(torch.bfloat16).to(torch.float32)
+    return (torch.from_numpy(q.astype(np.float32)) * sb).to(torch.bfloat16).to(torch.float64).numpy()
 
 
 def _bf16_x(rng, n, H):
@@ -59,7 +64,7 @@ def test_single_expert_is_dense_swiglu(wbits, g):
     assert np.all(ids == 0) and np.allclose(w, 1.0)
     qg, sg, qu, su, qd, sd = [ex.arrs[i] for i in (0, 3, 1, 4, 2, 5)]
     X = torch.from_numpy(x)
-    Wg, Wu, Wd = (torch.from_numpy(_deq(a, b)) for a, b in ((qg, sg), (qu, su), (qd, sd)))
+    Wg, Wu, Wd = (torch.from_numpy(_deq(a, b, g != 0)) for a, b in ((qg, sg), (qu, su), (qd, sd)))
     a = _bf16_torch(torch.nn.functional.silu(X @ Wg.T) * (X @ Wu.T))
     o = _bf16_torch(a @ Wd.T)
     ref = _bf16_torch(X + o).numpy()
