@@ -1,0 +1,313 @@
+"""bench.py — profiled tokens/s/box of the Flux hot path on B200 (BASELINE.json metric).
+
+One step = one participant round of the hot path (all rows):
+  a0 quantize the model (INT4 g128 / INT8)   flux_quantize_weights
+  a1-a6 profile the rank's tokens through all layers: router+top-k+histogram,
+        D_e permutation, grouped SwiGLU expert GEMMs (routed + shared), combine
+                                             flux_profile_layer x L
+  a7 all-reduce the int64 histograms         flux_reduce_stats (NCCL)
+  a8-pre eq.(1) layer budgets (host)         flux_layer_budget
+  a8 eq.(2) merge 64 -> 16 experts per layer, α = f (bf16)   flux_merge_experts
+Data parallel over tokens, weak scaling: every rank profiles its own shard of
+`tokens` tokens (the N=8 run is BASELINE.json's 2M-token DP config).
+
+usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config deepseek_moe|llama_moe]
+       python bench.py --impl reference ...   (the CPU oracle, timed on the host cores)
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "profiled tokens/sec/box (quantized MoE fwd + expert stats) at 1/2/4/8 B200; % roofline"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def workload_config(cfg, tokens_per_gpu, n_gpus):
+    return {
+        "workload": f"{cfg.name}: INT{cfg.wbits}{'-g' + str(cfg.group_size) if cfg.group_size else ' per-channel'} "
+                    f"quantize + profile {cfg.n_layers} layers + NCCL hist all-reduce + eq.(2) merge "
+                    f"{cfg.n_experts}->{max(1, cfg.n_experts // 4)} bf16",
+        "layers": cfg.n_layers, "hidden": cfg.hidden, "experts": cfg.n_experts, "shared_ffn": cfg.shared_ffn,
+        "top_k": cfg.top_k, "ffn": cfg.ffn, "wbits": cfg.wbits, "group_size": cfg.group_size,
+        "tokens_per_gpu": tokens_per_gpu, "tokens_total": tokens_per_gpu * n_gpus,
+        "parallelism": f"dp{n_gpus}",
+        "l2": "inputs larger than L2 (x shard = %.2f GiB, weights %.1f GiB)" % (
+            tokens_per_gpu * cfg.hidden * 2 / 2**30,
+            cfg.n_layers * (cfg.n_experts * 3 * cfg.ffn + 3 * cfg.shared_ffn) * cfg.hidden * 2 / 2**30),
+    }
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self, gpus):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9 or not p[0].isdigit() or int(p[0]) not in gpus:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ reference arm
+def oracle_rate(cfg, n_tok, n_layers, T_full):
+    """Time the oracle (as it stands) on n_tok tokens through n_layers layers; returns (tokens/s scaled to a full
+    L-layer pass, threads, sample description, seconds)."""
+    import oracle.model as om
+    t0 = time.perf_counter()
+    q = [om.quantized_layer(cfg, l) for l in range(n_layers)]
+    om.profile_tokens(cfg, np.arange(n_tok), layers=n_layers, quantized=q)
+    dt = time.perf_counter() - t0
+    per_tok = dt / n_tok * (cfg.n_layers / n_layers)
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = (f"{n_tok} tokens x {n_layers} of {cfg.n_layers} layers (oracle quantization of those layers + "
+              f"free-running fp64 layer forward), scaled to a {cfg.n_layers}-layer pass; merge not included")
+    return 1.0 / per_tok, threads, sample, dt
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    n_tok, n_layers = (args.ref_tokens, args.ref_layers)
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r, threads, sample, dt = oracle_rate(cfg, n_tok, n_layers, cfg.tokens)
+        if i >= args.warmup:
+            rates.append(r)
+    v = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg.tokens / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, cfg.tokens, 1),
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="flux", choices=["flux", "reference"])
+    ap.add_argument("--config", default="deepseek_moe")
+    ap.add_argument("--tokens", type=int, default=0, help="tokens per GPU (default: the config's)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-tokens", type=int, default=16)
+    ap.add_argument("--ref-layers", type=int, default=1)
+    ap.add_argument("--clusters", type=int, default=0)
+    args = ap.parse_args()
+
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2508_19078_b200 as F
+    from paper_2508_19078_b200 import synthetic
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel, budgets, merge_model
+
+    T = args.tokens or cfg.tokens
+    T_total = T * world
+    C = args.clusters or max(1, cfg.n_experts // 4)
+    shape = ModelShape.of(cfg)
+    L, E, H, k = cfg.n_layers, cfg.n_experts, cfg.hidden, cfg.top_k
+    stream = torch.cuda.current_stream()
+
+    # ---- setup (not timed): synthetic master weights, this rank's token shard, buffers, NCCL comm
+    masters = synthetic.master_weights(cfg)
+    qm = QuantizedModel(shape)
+    prof = Profiler(shape, T, with_de=True)
+    x = synthetic.tokens(cfg, rank * T, T)
+    cluster_of = torch.from_numpy(synth.cluster_assignment(cfg, C)).cuda()
+    alpha = torch.empty(L, E, dtype=torch.float32, device="cuda")
+    alpha_host = torch.empty(L, E, dtype=torch.float32).pin_memory()
+    hist_host = torch.empty(L, E, dtype=torch.int64).pin_memory()
+    merged = None
+    uid = F.Comm.unique_id() if rank == 0 else None
+    if world > 1:
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    comm = F.Comm(uid, world, rank)
+    budget_out = {}
+
+    def step(x_in):
+        nonlocal merged
+        qm.quantize_from(masters)                                   # a0
+        prof.run(qm, x_in)                                          # a1-a6 (hist zeroed first)
+        comm.reduce_stats(prof.hist)                                # a7
+        hist_host.copy_(prof.hist, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h = hist_host.numpy()
+        alpha_host.copy_(torch.from_numpy((h / float(T_total)).astype(np.float32)))  # f
+        Cl, over = budgets(h, T_total, C * L)                       # a8-pre, eq.(1)
+        budget_out["C"] = Cl
+        alpha.copy_(alpha_host, non_blocking=True)
+        merged = merge_model(masters, alpha, cluster_of, C, merged)  # a8, eq.(2)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(x)
+    barrier()
+
+    clocks = ClockSampler(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
+                                       else "/tmp", f"clocks_rank{rank}.csv"))
+    if rank == 0:
+        clocks.start()
+    F.timing_read(reset=True)
+    F.timing_enable(True)
+    launches0 = F.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(x)
+    ev1.record(stream)
+    barrier()
+    F.timing_enable(False)
+    launches = F.launch_count() - launches0
+    kern = F.timing_read(reset=True)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clk = clocks.stop(gpus=set(range(world))) if rank == 0 else None
+
+    # ---- e2e: the same step through the public API with host buffers (pinned H2D of the tokens,
+    #      D2H of the profiling result: reduced histogram + D_e CSR of every layer)
+    x_host = x.cpu().pin_memory()
+    off_host = torch.empty_like(prof.offsets, device="cpu").pin_memory()
+    ti_host = torch.empty_like(prof.token_index, device="cpu").pin_memory()
+    x_dev = torch.empty_like(x)
+    h2d = x_host.numel() * x_host.element_size()
+    d2h = hist_host.numel() * 8 + off_host.numel() * 4 + ti_host.numel() * 4
+
+    def e2e_step():
+        x_dev.copy_(x_host, non_blocking=True)
+        step(x_dev)
+        off_host.copy_(prof.offsets, non_blocking=True)
+        ti_host.copy_(prof.token_index, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    e2e_step()
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    ev1.record(stream)
+    barrier()
+    ms_e2e = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        value = T_total * args.steps / (ms / 1000.0)
+        # dominant kernel: the gate/up grouped GEMM (routed + shared in one launch, once per layer)
+        gu_ms, gu_n = kern.get("gemm_gate_up", (0.0, 0))
+        flop_gu = 2.0 * T * (k * H * 2 * cfg.ffn + H * 2 * cfg.shared_ffn)  # per launch (one layer)
+        achieved = flop_gu / (gu_ms / gu_n / 1000.0) / 1e12 if gu_n else None
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(f"{args.config}:gemm_gate_up:{T}")
+        kernels = {n: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+                   for n, v in kern.items() if v[1]}
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": workload_config(cfg, T, world),
+            "roofline": {"bound": "tensor", "kernel": "gemm_gate_up (K3+K5)", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "peak_source": peak_src + ", bf16 sustained",
+                         "flop_per_launch": flop_gu},
+            "e2e": {"value": T_total * args.steps / (ms_e2e / 1000.0), "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "kernels": kernels,
+            "budget_C": [int(c) for c in budget_out.get("C", [])][:4],
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            r, threads, sample, dt = oracle_rate(cfg, args.ref_tokens, args.ref_layers, T)
+            line["cpu_baseline"] = {"value": r, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+                                    "sample": sample, "seconds": dt}
+        print(json.dumps(line), flush=True)
+    comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -49,8 +49,8 @@ const char* flux_status_string(flux_status s);
 
 /* ============================================================================
  * Model shape of one MoE layer (Table 1).
- * Supported: hidden % 64 == 0; ffn % 16 == 0 (and shared_ffn); 1 <= top_k <=
- * n_experts <= 256; wbits in {4, 8}; group_size == 0 (per output channel) or
+ * Supported: hidden % 64 == 0; ffn % 16 == 0 (and shared_ffn); 1 <= top_k <= 8,
+ * top_k <= n_experts <= 128; wbits in {4, 8}; group_size == 0 (per output channel) or
  * a multiple of 64 dividing both hidden and ffn (and shared_ffn); INT4 needs
  * every packed row to be a multiple of 16 B (hidden % 32 == 0, ffn % 32 == 0).
  * ========================================================================== */
@@ -163,6 +163,19 @@ flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype 
  * *overrun (may be NULL) = Σ C_l - B_non. */
 flux_status flux_layer_budget(int32_t L, int32_t E, const int64_t* hist, int64_t T, int64_t B_non,
                               const int32_t* n_non, int32_t* C_out, int64_t* overrun);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics (benchmarking only).
+ * ------------------------------------------------------------------------- */
+/* Opt-in: while on, every hot launch records a CUDA event pair on its own stream. */
+void flux_timing_enable(int on);
+/* Synchronises pending events and returns per-kernel totals: ms_out[i] (milliseconds) and
+ * count_out[i] (launches) for kernel kind i (names: flux_kernel_name); reset != 0 clears them.
+ * Returns the number of kernel kinds. */
+int flux_timing_read(double* ms_out, long long* count_out, int n, int reset);
+const char* flux_kernel_name(int kind);
+/* Total kernels this library has launched in the process (monotonic). */
+long long flux_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -185,42 +185,67 @@ void orc_permute(int64_t T, int E, int k, const int32_t* ids, int64_t* hist, int
 }
 
 /* ----------------------------------------------------------------------------
- * O4. One SwiGLU expert on one token with dequantized weights ŵ = q·s (R4):
+ * O4. SwiGLU expert with dequantized weights ŵ (R4):
  *   g_f = Σ_h x_h ŵgate[f][h],  u_f = Σ_h x_h ŵup[f][h]
  *   a_f = bf16( SiLU(g_f) · u_f ),      SiLU(v) = v / (1 + e^{-v})
  *   o_h = bf16( Σ_f a_f ŵdown[h][f] )
  * Quantized weights: q int8 [rows][K] unpacked, s fp32 [rows][K/g].
+ * Dequantized weight of the quantized model (reading R1b):
+ *   per output channel (group_size == 0): ŵ = q·s exactly;
+ *   groups along K: ŵ = bf16( q · bf16(s) ) — the W4A16 convention: the quantized
+ *   model's weights are materialised in bf16 from the code and the bf16 scale.
  * -------------------------------------------------------------------------- */
 typedef struct {
   const int8_t *q_gate, *q_up, *q_down;
   const float *s_gate, *s_up, *s_down;
 } orc_expert;
 
-/* Dequantized weight of the quantized model (reading R1b):
- *   per output channel (group_size == 0): ŵ = q·s exactly (the scale multiplies the dot product);
- *   groups along K:                       ŵ = bf16( q · bf16(s) )  — the W4A16 convention: the
- *   quantized model's weights are materialised in bf16 from the code and the bf16 scale. */
-static int g_grouped = 0; /* set per call by orc_moe_tokens */
-static double deq(const int8_t* q, const float* s, int64_t row, int64_t K, int64_t g, int64_t k) {
-  double sc = (double)s[row * (K / g) + k / g];
-  if (g_grouped) return orc_bf16_round((double)q[row * K + k] * orc_bf16_round(sc));
-  return (double)q[row * K + k] * sc;
+/* ŵ for a whole [rows][K] matrix (g = group length along K, grouped = g came from group_size). */
+static void dequantize(const int8_t* q, const float* s, int64_t rows, int64_t K, int64_t g, int grouped,
+                       double* out) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t k = 0; k < K; ++k) {
+      double sc = (double)s[r * (K / g) + k / g];
+      double qv = (double)q[r * K + k];
+      out[r * K + k] = grouped ? orc_bf16_round(qv * orc_bf16_round(sc)) : qv * sc;
+    }
 }
 
-static void swiglu_expert(int H, int F, int64_t g_h, int64_t g_f, const orc_expert* ex, const double* x, double* a,
-                          double* out) {
+typedef struct {
+  double *gate, *up, *down; /* [F][H], [F][H], [H][F] */
+} deq_expert;
+
+static int deq_alloc(deq_expert* d, int H, int F) {
+  d->gate = (double*)malloc(sizeof(double) * (size_t)F * H);
+  d->up = (double*)malloc(sizeof(double) * (size_t)F * H);
+  d->down = (double*)malloc(sizeof(double) * (size_t)F * H);
+  return d->gate && d->up && d->down;
+}
+static void deq_free(deq_expert* d) {
+  free(d->gate);
+  free(d->up);
+  free(d->down);
+}
+static void deq_fill(deq_expert* d, const orc_expert* ex, int H, int F, int g) {
+  const int grouped = g != 0;
+  dequantize(ex->q_gate, ex->s_gate, F, H, grouped ? g : H, grouped, d->gate);
+  dequantize(ex->q_up, ex->s_up, F, H, grouped ? g : H, grouped, d->up);
+  dequantize(ex->q_down, ex->s_down, H, F, grouped ? g : F, grouped, d->down);
+}
+
+static void swiglu_expert(int H, int F, const deq_expert* w, const double* x, double* a, double* out) {
   for (int f = 0; f < F; ++f) {
     double gs = 0.0, us = 0.0;
     for (int h = 0; h < H; ++h) {
-      gs += x[h] * deq(ex->q_gate, ex->s_gate, f, H, g_h, h);
-      us += x[h] * deq(ex->q_up, ex->s_up, f, H, g_h, h);
+      gs += x[h] * w->gate[(int64_t)f * H + h];
+      us += x[h] * w->up[(int64_t)f * H + h];
     }
     double silu = gs / (1.0 + exp(-gs));
     a[f] = orc_bf16_round(silu * us);
   }
   for (int h = 0; h < H; ++h) {
     double acc = 0.0;
-    for (int f = 0; f < F; ++f) acc += a[f] * deq(ex->q_down, ex->s_down, h, F, g_f, f);
+    for (int f = 0; f < F; ++f) acc += a[f] * w->down[(int64_t)h * F + f];
     out[h] = orc_bf16_round(acc);
   }
 }
@@ -229,46 +254,60 @@ static void swiglu_expert(int H, int F, int64_t g_h, int64_t g_f, const orc_expe
  * O2+O4+O5+O6 for n independent tokens of one layer (tokens never interact
  * on this attention-free path, R7):
  *   (z, S, w, margin) = router(x_t)
- *   o_{t,j}  = expert_{S_tj}(x_t)                       (O4)
+ *   o_{t,j}  = expert_{S_tj}(x_t)                       (O4; for e, for t in D_e)
  *   sh_t     = shared SwiGLU(x_t), 0 if F_s == 0        (O5)
- *   y_t      = bf16( x_t + sh_t + Σ_j w_tj · o_{t,j} )  (O6, residual = x_t)
+ *   y_t      = bf16( x_t + sh_t + Σ_j w_tj · o_{t,j} )  (O6, residual = x_t, j in order)
  * x, y: [n][H] real (bf16-valued) numbers.  experts: array of E routed experts;
- * shared: NULL or one expert of width F_s.  group sizes: g (0 = per channel).
+ * shared: NULL or one expert of width F_s.  g: group size (0 = per channel).
+ * Work order: each expert's weights are dequantized once, then its tokens run.
  * -------------------------------------------------------------------------- */
 int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int norm, const double* x, const double* wr,
                    const orc_expert* experts, const orc_expert* shared, double* y, int32_t* ids, double* w, double* z,
                    double* margin) {
   if (orc_router(n, H, E, k, norm, x, wr, z, ids, w, margin)) return 1;
-  g_grouped = g != 0;
-  const int64_t gh = g ? g : H;            /* gate/up groups run along H */
-  const int64_t gf = g ? g : F;            /* down groups run along F   */
-  const int64_t gfs = g ? g : (Fs ? Fs : 1);
+  double* o = (double*)malloc(sizeof(double) * (size_t)n * k * H);   /* o[t][j][h] */
+  double* sh = (double*)calloc((size_t)n * H, sizeof(double));       /* sh[t][h]   */
+  if (!o || !sh) { free(o); free(sh); return 2; }
   int ok = 1;
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t t = 0; t < n; ++t) {
-    const double* xt = x + t * H;
-    int Fmax = F > Fs ? F : Fs;
-    double* a = (double*)malloc(sizeof(double) * (size_t)Fmax);
-    double* o = (double*)malloc(sizeof(double) * (size_t)H);
-    double* acc = (double*)malloc(sizeof(double) * (size_t)H);
-    if (!a || !o || !acc) {
-      ok = 0;
-    } else {
-      for (int h = 0; h < H; ++h) acc[h] = xt[h];
-      if (shared && Fs > 0) {
-        swiglu_expert(H, Fs, gh, gfs, shared, xt, a, o);
-        for (int h = 0; h < H; ++h) acc[h] += o[h];
-      }
-      for (int j = 0; j < k; ++j) {
-        swiglu_expert(H, F, gh, gf, &experts[ids[t * k + j]], xt, a, o);
-        for (int h = 0; h < H; ++h) acc[h] += w[t * k + j] * o[h];
-      }
-      for (int h = 0; h < H; ++h) y[t * H + h] = orc_bf16_round(acc[h]);
-    }
+  for (int e = 0; e < E; ++e) {
+    int used = 0;
+    for (int64_t i = 0; i < n * k; ++i) used |= ids[i] == e;
+    if (!used) continue;
+    deq_expert d;
+    double* a = (double*)malloc(sizeof(double) * (size_t)F);
+    if (!deq_alloc(&d, H, F) || !a) { ok = 0; deq_free(&d); free(a); continue; }
+    deq_fill(&d, &experts[e], H, F, g);
+    for (int64_t t = 0; t < n; ++t)
+      for (int j = 0; j < k; ++j)
+        if (ids[t * k + j] == e) swiglu_expert(H, F, &d, x + t * H, a, o + (t * k + j) * (int64_t)H);
+    deq_free(&d);
     free(a);
-    free(o);
-    free(acc);
   }
+  if (shared && Fs > 0) {
+    deq_expert d;
+    if (!deq_alloc(&d, H, Fs)) { ok = 0; }
+    else {
+      deq_fill(&d, shared, H, Fs, g);
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int64_t t = 0; t < n; ++t) {
+        double* a = (double*)malloc(sizeof(double) * (size_t)Fs);
+        swiglu_expert(H, Fs, &d, x + t * H, a, sh + t * H);
+        free(a);
+      }
+    }
+    deq_free(&d);
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < n; ++t)
+    for (int h = 0; h < H; ++h) {
+      double acc = x[t * H + h];
+      acc += sh[t * H + h];
+      for (int j = 0; j < k; ++j) acc += w[t * k + j] * o[(t * k + j) * (int64_t)H + h];
+      y[t * H + h] = orc_bf16_round(acc);
+    }
+  free(o);
+  free(sh);
   return ok ? 0 : 2;
 }
 

@@ -75,8 +75,34 @@ def _lib():
         for f in ("flux_profile_layer", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
                   "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
             getattr(L, f).restype = ctypes.c_int
+        L.flux_timing_enable.argtypes = [ctypes.c_int]
+        L.flux_timing_enable.restype = None
+        L.flux_timing_read.argtypes = [P, P, ctypes.c_int, ctypes.c_int]
+        L.flux_timing_read.restype = ctypes.c_int
+        L.flux_kernel_name.argtypes = [ctypes.c_int]
+        L.flux_kernel_name.restype = ctypes.c_char_p
+        L.flux_launch_count.argtypes = []
+        L.flux_launch_count.restype = ctypes.c_longlong
         _L = L
     return _L
+
+
+# ------------------------------------------------------------------------------------------ diagnostics
+def timing_enable(on: bool = True):
+    _lib().flux_timing_enable(1 if on else 0)
+
+
+def timing_read(reset: bool = True) -> dict:
+    """{kernel name: (total ms, launches)} of the launches recorded while timing was enabled."""
+    n = 32
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_longlong * n)()
+    k = _lib().flux_timing_read(ms, cnt, n, 1 if reset else 0)
+    return {_lib().flux_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(k)}
+
+
+def launch_count() -> int:
+    return int(_lib().flux_launch_count())
 
 
 def lib():

@@ -198,6 +198,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
 
   // ---- (a) weights -> bf16 B operands (scale folded for grouped quantization)
   cudaError_t e;
+  {
+  KernelTimer kt(K_DEQUANT, s);
   e = launch_dequant(c.wbits, (const uint8_t*)w->gate_q, w->gate_s, (const uint8_t*)w->up_q, w->up_s, E, F, H, Fp, 1,
                      g_h, per_channel, wgu_r, s);
   if (e == cudaSuccess)
@@ -209,6 +211,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   if (e == cudaSuccess && sh)
     e = launch_dequant(c.wbits, (const uint8_t*)w->sh_down_q, w->sh_down_s, nullptr, nullptr, 1, H, Fs, 0, 0, g_fs,
                        per_channel, wdn_s, s);
+  }
   if (e != cudaSuccess) return FLUX_E_CUDA;
 
   // ---- (b) K1 router + top-k + histogram
@@ -216,7 +219,10 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   CUtensorMap tm_x, tm_wr;
   if (!tmap_bf16(&tm_x, x, T, H, 128) || !tmap_bf16(&tm_wr, w->router_w, E, H, npad)) return FLUX_E_CUDA;
   RouterArgs ra{T, H, E, k, c.norm_topk, out->topk_ids, out->topk_w, out->router_logits, out->hist, tile_counts, rank};
-  if (launch_router(tm_x, tm_wr, npad, ra, s) != cudaSuccess) return FLUX_E_CUDA;
+  {
+    KernelTimer kt(K_ROUTER, s);
+    if (launch_router(tm_x, tm_wr, npad, ra, s) != cudaSuccess) return FLUX_E_CUDA;
+  }
 
   // ---- (c) K2 schedule + scatter/gather (D_e)
   ScheduleArgs sa;
@@ -238,10 +244,16 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   sa.sched_dn = (int32_t*)(W + P.sched_dn);
   sa.grp_row0 = (int32_t*)(W + P.row0);
   sa.grp_rows = (int32_t*)(W + P.rows);
-  if (launch_schedule(sa, s) != cudaSuccess) return FLUX_E_CUDA;
-  if (launch_scatter(x, T, H, E, k, out->topk_ids, rank, tile_base, offsets, inv_pos, token_index, x_perm, s) !=
-      cudaSuccess)
-    return FLUX_E_CUDA;
+  {
+    KernelTimer kt(K_SCHEDULE, s);
+    if (launch_schedule(sa, s) != cudaSuccess) return FLUX_E_CUDA;
+  }
+  {
+    KernelTimer kt(K_SCATTER, s);
+    if (launch_scatter(x, T, H, E, k, out->topk_ids, rank, tile_base, offsets, inv_pos, token_index, x_perm, s) !=
+        cudaSuccess)
+      return FLUX_E_CUDA;
+  }
 
   // ---- (d) K3 + K5: gate/up grouped GEMM with SwiGLU epilogue (routed + shared in one launch)
   CUtensorMap a_r, a_s, b_r, b_s;
@@ -275,7 +287,10 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.ld_r = F;
   ga.ld_s = Fs;
   ga.grid = kNumSMs;
-  if (launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s) != cudaSuccess) return FLUX_E_CUDA;
+  {
+    KernelTimer kt(K_GEMM_GU, s);
+    if (launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s) != cudaSuccess) return FLUX_E_CUDA;
+  }
 
   // ---- (e) K4 + K5: down grouped GEMM -> y_perm (aliases x_perm) and y_sh
   void* y_perm = x_perm;
@@ -303,12 +318,18 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   gd.out_s = y_sh;
   gd.ld_r = H;
   gd.ld_s = H;
-  if (launch_gemm(EPI_STORE, a_r, a_s, b_r, b_s, gd, s) != cudaSuccess) return FLUX_E_CUDA;
+  {
+    KernelTimer kt(K_GEMM_DN, s);
+    if (launch_gemm(EPI_STORE, a_r, a_s, b_r, b_s, gd, s) != cudaSuccess) return FLUX_E_CUDA;
+  }
 
   // ---- (f) K6 combine
-  if (launch_combine(T, H, k, residual ? residual : x, sh ? y_sh : nullptr, y_perm, out->topk_w, inv_pos, out->y,
-                     s) != cudaSuccess)
-    return FLUX_E_CUDA;
+  {
+    KernelTimer kt(K_COMBINE, s);
+    if (launch_combine(T, H, k, residual ? residual : x, sh ? y_sh : nullptr, y_perm, out->topk_w, inv_pos, out->y,
+                       s) != cudaSuccess)
+      return FLUX_E_CUDA;
+  }
   return FLUX_OK;
 }
 
@@ -323,6 +344,7 @@ flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype 
   if (!w || !q || !s || !aligned16(w) || !aligned16(q) || (reinterpret_cast<uintptr_t>(s) & 3)) return FLUX_E_INVALID;
   flux_status st = check_device();
   if (st != FLUX_OK) return st;
+  KernelTimer kt(K_QUANTIZE, (cudaStream_t)stream);
   return cuda_status(launch_quantize(wbits, g, in_dtype == FLUX_FP32, w, R, K, q, s, (cudaStream_t)stream));
 }
 
@@ -336,6 +358,7 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
   if (!experts || !cluster_of || !alpha || !merged || !aligned16(experts) || !aligned16(merged)) return FLUX_E_INVALID;
   flux_status st = check_device();
   if (st != FLUX_OK) return st;
+  KernelTimer kt(K_MERGE, (cudaStream_t)stream);
   return cuda_status(launch_merge(dtype == FLUX_FP32, n_experts, numel, experts, cluster_of, alpha, n_clusters, merged,
                                   remap, (cudaStream_t)stream));
 }

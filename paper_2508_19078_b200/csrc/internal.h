@@ -19,6 +19,25 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype,
 
 inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_OK : FLUX_E_CUDA; }
 
+// ---------------------------------------------------------------- per-kernel timing (timing.cpp)
+enum KernelKind {
+  K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_SCHEDULE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
+  FLUX_NUM_KERNELS
+};
+// RAII: counts one launch; when timing is enabled records CUDA events around it on `st`.
+class KernelTimer {
+ public:
+  KernelTimer(int kind, cudaStream_t st);
+  ~KernelTimer();
+  KernelTimer(const KernelTimer&) = delete;
+  KernelTimer& operator=(const KernelTimer&) = delete;
+
+ private:
+  int kind_;
+  cudaStream_t st_;
+  cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
+
 // ---------------------------------------------------------------- launchers
 // K0 (quantize.cu)
 cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, int64_t R, int64_t K, void* q, float* s,

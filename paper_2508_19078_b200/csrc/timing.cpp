@@ -1,0 +1,94 @@
+// timing.cpp — opt-in per-kernel CUDA-event timing and a launch counter, so a
+// benchmark can report the live duration of each hot kernel on the stream it
+// is launched on (the events are recorded on that stream around the launch).
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace flux {
+namespace {
+std::atomic<int> g_enabled{0};
+std::atomic<long long> g_launches{0};
+struct Pending {
+  int kind;
+  cudaEvent_t a, b;
+};
+std::mutex g_mu;
+std::vector<Pending> g_pending;
+std::vector<cudaEvent_t> g_pool;
+double g_ms[FLUX_NUM_KERNELS] = {0};
+long long g_cnt[FLUX_NUM_KERNELS] = {0};
+
+cudaEvent_t get_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+KernelTimer::KernelTimer(int kind, cudaStream_t st) : kind_(kind), st_(st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_enabled.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  a_ = get_event();
+  b_ = get_event();
+  cudaEventRecord(a_, st_);
+}
+
+KernelTimer::~KernelTimer() {
+  if (!a_) return;
+  cudaEventRecord(b_, st_);
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_pending.push_back({kind_, a_, b_});
+}
+
+}  // namespace flux
+
+using namespace flux;
+
+extern "C" {
+
+void flux_timing_enable(int on) { g_enabled.store(on ? 1 : 0); }
+
+long long flux_launch_count(void) { return g_launches.load(); }
+
+// Synchronises the recorded events, folds them into per-kind totals, and
+// copies totals (ms) and counts out; clears them if reset != 0.
+int flux_timing_read(double* ms_out, long long* count_out, int n, int reset) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& p : g_pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      g_ms[p.kind] += ms;
+      g_cnt[p.kind] += 1;
+    }
+    g_pool.push_back(p.a);
+    g_pool.push_back(p.b);
+  }
+  g_pending.clear();
+  for (int i = 0; i < n && i < FLUX_NUM_KERNELS; ++i) {
+    if (ms_out) ms_out[i] = g_ms[i];
+    if (count_out) count_out[i] = g_cnt[i];
+  }
+  if (reset)
+    for (int i = 0; i < FLUX_NUM_KERNELS; ++i) {
+      g_ms[i] = 0;
+      g_cnt[i] = 0;
+    }
+  return FLUX_NUM_KERNELS;
+}
+
+const char* flux_kernel_name(int kind) {
+  static const char* names[FLUX_NUM_KERNELS] = {"quantize", "dequant", "router", "schedule", "scatter",
+                                                "gemm_gate_up", "gemm_down", "combine", "merge"};
+  return kind >= 0 && kind < FLUX_NUM_KERNELS ? names[kind] : "?";
+}
+
+}  // extern "C"
