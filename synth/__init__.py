@@ -15,7 +15,8 @@ layers more balanced):
   x_0[t][0] = 1.0 (bias feature), x_0[t][d>0] ~ IH4(σ=1)
   W_r[l][e][0] = β_{l,e} ~ IH4(σ=s_l), s_l linear 0.35 (l=0) → 0.10 (l=L-1)
   W_r[l][e][d>0] ~ IH4(σ=1/√H)
-  W_gate, W_up [F][H] ~ IH4(σ=1/√H);  W_down [H][F] ~ IH4(σ=0.5/√F), row 0 = 0
+  W_gate, W_up [F][H] ~ IH4(σ=1/√H);  W_down [H][F] ~ IH4(σ=0.1/√F), row 0 = 0
+  (0.1 keeps the norm-free residual stream at rms ≈ 1.06 over 28 layers; 0.5 diverges)
   shared experts: one SwiGLU MLP of width F_s (expert slot 1023)
 IH4 = Irwin–Hall(4) of 12-bit uniforms, centred and scaled to std σ.
 """
@@ -125,7 +126,7 @@ def spec_expert(cfg: MoEConfig, layer: int, expert: int, which: str):
     if which == "up":
         return Spec(F, H, s, stream_id(KIND_UP, layer, expert), scale_c(1.0 / math.sqrt(H)), 0, 0.0)
     if which == "down":
-        return Spec(H, F, s, stream_id(KIND_DOWN, layer, expert), scale_c(0.5 / math.sqrt(F)), ROW0_ZERO, 0.0)
+        return Spec(H, F, s, stream_id(KIND_DOWN, layer, expert), scale_c(0.1 / math.sqrt(F)), ROW0_ZERO, 0.0)
     raise ValueError(which)
 
 
