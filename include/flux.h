@@ -174,6 +174,10 @@ void flux_timing_enable(int on);
  * Returns the number of kernel kinds. */
 int flux_timing_read(double* ms_out, long long* count_out, int n, int reset);
 const char* flux_kernel_name(int kind);
+/* Text of the last CUDA error this thread's calls saw ("" if none).  With the
+ * environment variable FLUX_DEBUG_SYNC=1 every launch is synchronised and a
+ * failure names the kernel that raised it. */
+const char* flux_last_error(void);
 /* Total kernels this library has launched in the process (monotonic). */
 long long flux_launch_count(void);
 

@@ -30,7 +30,9 @@ FLUX_BF16, FLUX_FP32 = 0, 1
 class FluxError(RuntimeError):
     def __init__(self, status: int, what: str):
         self.status = status
-        super().__init__(f"{what}: {_lib().flux_status_string(status).decode()} (status {status})")
+        detail = _lib().flux_last_error().decode()
+        super().__init__(f"{what}: {_lib().flux_status_string(status).decode()} (status {status})"
+                         + (f" [{detail}]" if detail else ""))
 
 
 class MoECfg(ctypes.Structure):
@@ -81,6 +83,8 @@ def _lib():
         L.flux_timing_read.restype = ctypes.c_int
         L.flux_kernel_name.argtypes = [ctypes.c_int]
         L.flux_kernel_name.restype = ctypes.c_char_p
+        L.flux_last_error.argtypes = []
+        L.flux_last_error.restype = ctypes.c_char_p
         L.flux_launch_count.argtypes = []
         L.flux_launch_count.restype = ctypes.c_longlong
         _L = L

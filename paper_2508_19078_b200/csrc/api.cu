@@ -61,6 +61,13 @@ static flux_status check_device() {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Grouped-GEMM tile rows: 256 = CTA-pair kernel (default), 128 = 1-CTA kernel (FLUX_GEMM_1SM=1,
+// kept for A/B measurements).  Both are deterministic and batch-invariant.
+static int gemm_bm() {
+  const char* e = getenv("FLUX_GEMM_1SM");
+  return (e && e[0] == '1') ? 128 : 256;
+}
+
 // ---------------------------------------------------------------- workspace layout
 namespace {
 struct Layout {
@@ -212,16 +219,16 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
     e = launch_dequant(c.wbits, (const uint8_t*)w->sh_down_q, w->sh_down_s, nullptr, nullptr, 1, H, Fs, 0, 0, g_fs,
                        per_channel, wdn_s, s);
   }
-  if (e != cudaSuccess) return FLUX_E_CUDA;
+  if (e != cudaSuccess) { set_last_error("dequant", e); return FLUX_E_CUDA; }
 
   // ---- (b) K1 router + top-k + histogram
   const int npad = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
   CUtensorMap tm_x, tm_wr;
-  if (!tmap_bf16(&tm_x, x, T, H, 128) || !tmap_bf16(&tm_wr, w->router_w, E, H, npad)) return FLUX_E_CUDA;
+  if (!tmap_bf16(&tm_x, x, T, H, 128) || !tmap_bf16(&tm_wr, w->router_w, E, H, npad)) { set_last_error("router tensor map", cudaErrorInvalidValue); return FLUX_E_CUDA; }
   RouterArgs ra{T, H, E, k, c.norm_topk, out->topk_ids, out->topk_w, out->router_logits, out->hist, tile_counts, rank};
   {
     KernelTimer kt(K_ROUTER, s);
-    if (launch_router(tm_x, tm_wr, npad, ra, s) != cudaSuccess) return FLUX_E_CUDA;
+    if ((e = launch_router(tm_x, tm_wr, npad, ra, s)) != cudaSuccess) { set_last_error("router", e); return FLUX_E_CUDA; }
   }
 
   // ---- (c) K2 schedule + scatter/gather (D_e)
@@ -244,9 +251,10 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   sa.sched_dn = (int32_t*)(W + P.sched_dn);
   sa.grp_row0 = (int32_t*)(W + P.row0);
   sa.grp_rows = (int32_t*)(W + P.rows);
+  sa.gemm_bm = gemm_bm();
   {
     KernelTimer kt(K_SCHEDULE, s);
-    if (launch_schedule(sa, s) != cudaSuccess) return FLUX_E_CUDA;
+    if ((e = launch_schedule(sa, s)) != cudaSuccess) { set_last_error("schedule", e); return FLUX_E_CUDA; }
   }
   {
     KernelTimer kt(K_SCATTER, s);
@@ -257,10 +265,11 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
 
   // ---- (d) K3 + K5: gate/up grouped GEMM with SwiGLU epilogue (routed + shared in one launch)
   CUtensorMap a_r, a_s, b_r, b_s;
-  if (!tmap_bf16(&a_r, x_perm, Tk, H, 128) || !tmap_bf16(&b_r, wgu_r, (uint64_t)E * 2 * Fp, H, 256))
+  const uint32_t bbox = sa.gemm_bm == 256 ? 128 : 256;  // B rows per TMA box: half the tile for CTA pairs
+  if (!tmap_bf16(&a_r, x_perm, Tk, H, 128) || !tmap_bf16(&b_r, wgu_r, (uint64_t)E * 2 * Fp, H, bbox))
     return FLUX_E_CUDA;
   if (sh) {
-    if (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_bf16(&b_s, wgu_s, 2ull * Fsp, H, 256)) return FLUX_E_CUDA;
+    if (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_bf16(&b_s, wgu_s, 2ull * Fsp, H, bbox)) return FLUX_E_CUDA;
   } else {
     a_s = a_r;
     b_s = b_r;
@@ -287,16 +296,17 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.ld_r = F;
   ga.ld_s = Fs;
   ga.grid = kNumSMs;
+  ga.bm = sa.gemm_bm;
   {
     KernelTimer kt(K_GEMM_GU, s);
-    if (launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s) != cudaSuccess) return FLUX_E_CUDA;
+    if ((e = launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s)) != cudaSuccess) { set_last_error("gemm_gate_up", e); return FLUX_E_CUDA; }
   }
 
   // ---- (e) K4 + K5: down grouped GEMM -> y_perm (aliases x_perm) and y_sh
   void* y_perm = x_perm;
-  if (!tmap_bf16(&a_r, act, Tk, F, 128) || !tmap_bf16(&b_r, wdn_r, (uint64_t)E * H, F, 256)) return FLUX_E_CUDA;
+  if (!tmap_bf16(&a_r, act, Tk, F, 128) || !tmap_bf16(&b_r, wdn_r, (uint64_t)E * H, F, bbox)) return FLUX_E_CUDA;
   if (sh) {
-    if (!tmap_bf16(&a_s, act_sh, T, Fs, 128) || !tmap_bf16(&b_s, wdn_s, H, Fs, 256)) return FLUX_E_CUDA;
+    if (!tmap_bf16(&a_s, act_sh, T, Fs, 128) || !tmap_bf16(&b_s, wdn_s, H, Fs, bbox)) return FLUX_E_CUDA;
   } else {
     a_s = a_r;
     b_s = b_r;
@@ -320,7 +330,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   gd.ld_s = H;
   {
     KernelTimer kt(K_GEMM_DN, s);
-    if (launch_gemm(EPI_STORE, a_r, a_s, b_r, b_s, gd, s) != cudaSuccess) return FLUX_E_CUDA;
+    if ((e = launch_gemm(EPI_STORE, a_r, a_s, b_r, b_s, gd, s)) != cudaSuccess) { set_last_error("gemm_down", e); return FLUX_E_CUDA; }
   }
 
   // ---- (f) K6 combine

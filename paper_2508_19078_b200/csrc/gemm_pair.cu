@@ -1,0 +1,167 @@
+// gemm_pair.cu — K3/K4/K5 grouped expert GEMMs on CTA pairs (tcgen05 cta_group::2).
+//
+// Same math and tile schedule semantics as gemm.cu, but each tile is 256 rows
+// x 256 output columns computed by a cluster of two CTAs on the two SMs of a
+// TPC: every CTA TMA-loads its own 128 A rows and its half (128 rows) of the
+// 256-row B tile per 64-wide K slice; the leader CTA issues
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16), which reads A and B from both
+// CTAs' shared memory and writes each CTA's 128 accumulator rows to its own
+// TMEM.  Versus the 1-CTA kernel this cuts the shared-memory operand traffic
+// per MMA FLOP by a third (each SM stages 32 KB per K slice instead of 48 KB).
+//
+// Synchronisation: full[s] lives in the leader (TMA bytes of both CTAs complete
+// on it; the leader's producer arms it with the pair's byte count); empty[s] and
+// tfull[a] exist in both CTAs and are signalled by a multicast tcgen05.commit;
+// tempty[a] lives in the leader and collects one arrive per epilogue warp of
+// both CTAs.  The tile loop runs per cluster (static round-robin over 74 pairs).
+#include "gemm_common.cuh"
+
+namespace flux {
+namespace {
+using namespace gemm;
+
+constexpr int kHalfM = 128, kPairM = 256, kStages = 6;
+constexpr int kABytes = kHalfM * kBK * 2;     // 16 KB: this CTA's A rows
+constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 256;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64;
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tm_a_r, const __grid_constant__ CUtensorMap tm_a_s,
+                             const __grid_constant__ CUtensorMap tm_b_r, const __grid_constant__ CUtensorMap tm_b_s,
+                             Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* s_sched = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 256);
+  int32_t* s_row0 = s_sched + kMaxGroups;
+  int32_t* s_rows = s_row0 + kMaxGroups;
+
+  const int warp = warp_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  for (int i = threadIdx.x; i <= p.n_groups; i += kThreads) s_sched[i] = p.sched[i];
+  for (int i = threadIdx.x; i < p.n_groups; i += kThreads) {
+    s_row0[i] = p.grp_row0[i];
+    s_rows[i] = p.grp_rows[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int total = s_sched[p.n_groups];
+  const int nkb_r = (p.K_r + kBK - 1) / kBK, nkb_s = (p.K_s + kBK - 1) / kBK;
+  const int cid = (int)cluster_id_x(), ncl = (int)ncluster_x();
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch(&tm_a_r);
+      tma_prefetch(&tm_b_r);
+      tma_prefetch(&tm_a_s);
+      tma_prefetch(&tm_b_s);
+      uint32_t it = 0;
+      for (int tile = cid; tile < total; tile += ncl) {
+        const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+        const bool routed = ti.g < p.E;
+        const int arow = s_row0[ti.g] + ti.m * kPairM + (int)rank * kHalfM;
+        const int brow = (routed ? ti.g * p.b_rows_r : 0) + ti.n * kBN + (int)rank * (kBN / 2);
+        const CUtensorMap* ta = routed ? &tm_a_r : &tm_a_s;
+        const CUtensorMap* tb = routed ? &tm_b_r : &tm_b_s;
+        const int nkb = routed ? nkb_r : nkb_s;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * kStageBytes;
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+          tma_load_2d_pair(st, ta, &full[s], kb * kBK, arow);
+          tma_load_2d_pair(st + kABytes, tb, &full[s], kb * kBK, brow);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(kPairM, kBN);
+      uint32_t it = 0, tc = 0;
+      for (int tile = cid; tile < total; tile += ncl, ++tc) {
+        const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+        const int nkb = ti.g < p.E ? nkb_r : nkb_s;
+        const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * kBN;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + s * kStageBytes);
+            const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + kABytes);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            umma_commit_pair_mc(&empty[s], 0x3);
+            if (kb == nkb - 1) umma_commit_pair_mc(&tfull[acc], 0x3);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    uint32_t tc = 0;
+    for (int tile = cid; tile < total; tile += ncl, ++tc) {
+      const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+      const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int r_local = ti.m * kPairM + (int)rank * kHalfM + q * 32 + (int)lane_id();
+      epilogue_slice<EPI>(p, tmem + acc * kBN + lane_base, ti, r_local < s_rows[ti.g],
+                          (int64_t)s_row0[ti.g] + r_local);
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) tmem_dealloc_pair<512>(tmem);
+}
+}  // namespace
+
+cudaError_t launch_gemm_1sm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
+                            const CUtensorMap& b_s, const GemmArgs& g, cudaStream_t st);
+
+cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
+                        const CUtensorMap& b_s, const GemmArgs& g, cudaStream_t st) {
+  if (g.bm == 128) return launch_gemm_1sm(epi, a_r, a_s, b_r, b_s, g, st);
+  if (g.bm != 256 || g.n_groups > kMaxGroups - 1) return cudaErrorInvalidValue;
+  const Params p = make_params(g);
+  auto kern = epi == EPI_SWIGLU ? grouped_gemm_pair_kernel<EPI_SWIGLU> : grouped_gemm_pair_kernel<EPI_STORE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<(g.grid / 2) * 2, kThreads, kSmemBytes, st>>>(a_r, a_s, b_r, b_s, p);
+  return cudaGetLastError();
+}
+
+}  // namespace flux

@@ -38,6 +38,9 @@ class KernelTimer {
   cudaEvent_t a_ = nullptr, b_ = nullptr;
 };
 
+void set_last_error(const char* what, cudaError_t e);
+const char* last_error();
+
 // ---------------------------------------------------------------- launchers
 // K0 (quantize.cu)
 cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, int64_t R, int64_t K, void* q, float* s,
@@ -77,6 +80,7 @@ struct ScheduleArgs {
   int32_t* sched_dn;        // [n_groups+1]
   int32_t* grp_row0;        // [n_groups] first A row of each group
   int32_t* grp_rows;        // [n_groups] rows of each group
+  int gemm_bm;              // GEMM tile rows (128 or 256)
 };
 cudaError_t launch_schedule(const ScheduleArgs& a, cudaStream_t st);
 cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const int32_t* ids, const int32_t* rank,
@@ -104,6 +108,7 @@ struct GemmArgs {
   void *out_r, *out_s;      // bf16 [rows][ld]
   int64_t ld_r, ld_s;
   int grid;
+  int bm;                   // rows per tile: 128 (1-CTA kernel) or 256 (CTA-pair kernel)
 };
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);

@@ -17,7 +17,7 @@
 namespace flux {
 
 namespace {
-constexpr int kGemmBM = 128;
+
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int* sh, int& total) {
   // 256 threads
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) schedule_kernel(ScheduleArgs a) {
     int tot_rows;
     const int ex_rows = block_exclusive_scan(g < a.E ? rows : 0, sh, tot_rows);
     row0 = g < a.E ? carry_rows + ex_rows : 0;
-    const int mt = (rows + kGemmBM - 1) / kGemmBM;
+    const int mt = (rows + a.gemm_bm - 1) / a.gemm_bm;
     const int ngu = mt * (g < a.E ? a.n_tiles_gu : a.n_tiles_gu_sh);
     const int ndn = mt * (g < a.E ? a.n_tiles_dn : a.n_tiles_dn_sh);
     int tot_gu, tot_dn;

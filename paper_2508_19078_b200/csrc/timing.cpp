@@ -1,6 +1,9 @@
 // timing.cpp — opt-in per-kernel CUDA-event timing and a launch counter, so a
 // benchmark can report the live duration of each hot kernel on the stream it
 // is launched on (the events are recorded on that stream around the launch).
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -8,6 +11,11 @@
 #include "internal.h"
 
 namespace flux {
+static const char* kernel_name(int kind) {
+  static const char* names[FLUX_NUM_KERNELS] = {"quantize", "dequant", "router", "schedule", "scatter",
+                                                "gemm_gate_up", "gemm_down", "combine", "merge"};
+  return kind >= 0 && kind < FLUX_NUM_KERNELS ? names[kind] : "?";
+}
 namespace {
 std::atomic<int> g_enabled{0};
 std::atomic<long long> g_launches{0};
@@ -42,12 +50,34 @@ KernelTimer::KernelTimer(int kind, cudaStream_t st) : kind_(kind), st_(st) {
   cudaEventRecord(a_, st_);
 }
 
+static const char* kernel_name(int kind);
+static thread_local char g_last_error[512] = "";
+static int debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FLUX_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 KernelTimer::~KernelTimer() {
+  if (debug_sync()) {  // diagnostics: surface the failing kernel instead of a later, anonymous error
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st_);
+    if (e != cudaSuccess)
+      snprintf(g_last_error, sizeof(g_last_error), "%s: %s", kernel_name(kind_), cudaGetErrorString(e));
+  }
   if (!a_) return;
   cudaEventRecord(b_, st_);
   std::lock_guard<std::mutex> lk(g_mu);
   g_pending.push_back({kind_, a_, b_});
 }
+
+void set_last_error(const char* what, cudaError_t e) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, cudaGetErrorString(e));
+}
+const char* last_error() { return g_last_error; }
 
 }  // namespace flux
 
@@ -85,10 +115,8 @@ int flux_timing_read(double* ms_out, long long* count_out, int n, int reset) {
   return FLUX_NUM_KERNELS;
 }
 
-const char* flux_kernel_name(int kind) {
-  static const char* names[FLUX_NUM_KERNELS] = {"quantize", "dequant", "router", "schedule", "scatter",
-                                                "gemm_gate_up", "gemm_down", "combine", "merge"};
-  return kind >= 0 && kind < FLUX_NUM_KERNELS ? names[kind] : "?";
-}
+const char* flux_kernel_name(int kind) { return flux::kernel_name(kind); }
+
+const char* flux_last_error(void) { return flux::last_error(); }
 
 }  // extern "C"
