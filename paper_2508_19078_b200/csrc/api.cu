@@ -63,9 +63,28 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 // Grouped-GEMM tile rows: 256 = CTA-pair kernel (default), 128 = 1-CTA kernel (FLUX_GEMM_1SM=1,
 // kept for A/B measurements).  Both are deterministic and batch-invariant.
-static int gemm_bm() {
-  const char* e = getenv("FLUX_GEMM_1SM");
-  return (e && e[0] == '1') ? 128 : 256;
+static bool env_on(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '1';
+}
+// Where the bf16 B operand of the expert GEMMs comes from.  Both choices produce bit-identical
+// weights (bf16(q·bf16(s)) or exact q) and the same MMA order, so results never depend on it:
+//  * fused: dequant warps inside the GEMM convert each B tile per m-tile -- best when few tokens
+//    reach each expert (the weights dominate traffic);
+//  * pass: one dequantization per layer into bf16 buffers the GEMM streams with TMA -- best when
+//    every B tile is reused by many m-tiles (e.g. 262,144 tokens: ~96 m-tiles per expert).
+// Policy: pass when the average routed rows per expert reach 8 tile rows (2048); overrides:
+// FLUX_GEMM_DEQUANT_PASS=1 / FLUX_GEMM_FUSED_DEQUANT=1 (FLUX_GEMM_1SM=1 implies the pass).
+static bool dequant_pass(const flux_moe_cfg& c, int64_t T) {
+  if (env_on("FLUX_GEMM_DEQUANT_PASS") || env_on("FLUX_GEMM_1SM")) return true;
+  if (env_on("FLUX_GEMM_FUSED_DEQUANT")) return false;
+  return T * c.top_k >= (int64_t)2048 * c.n_experts;
+}
+static int gemm_bm() { return env_on("FLUX_GEMM_1SM") ? 128 : 256; }
+
+static bool tmap_u8(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_bytes, uint32_t box_cols) {
+  return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rows, cols_bytes, cols_bytes, box_cols, 128,
+                      CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 // ---------------------------------------------------------------- workspace layout
@@ -106,10 +125,11 @@ WsPlan plan(const flux_moe_cfg& c, int64_t T) {
   p.act = L.take(2ull * Tk * c.ffn);
   p.act_sh = L.take(2ull * T * c.shared_ffn);
   p.y_sh = L.take(c.shared_ffn ? 2ull * T * c.hidden : 0);
-  p.wgu_r = L.take(2ull * c.n_experts * 2 * pad128(c.ffn) * c.hidden);
-  p.wdn_r = L.take(2ull * c.n_experts * c.hidden * c.ffn);
-  p.wgu_s = L.take(2ull * 2 * pad128(c.shared_ffn) * c.hidden);
-  p.wdn_s = L.take(2ull * c.hidden * c.shared_ffn);
+  const size_t pass = dequant_pass(c, T) ? 1 : 0;  // bf16 B operands only for the separate-pass path
+  p.wgu_r = L.take(pass * 2ull * c.n_experts * 2 * pad128(c.ffn) * c.hidden);
+  p.wdn_r = L.take(pass * 2ull * c.n_experts * c.hidden * c.ffn);
+  p.wgu_s = L.take(pass * 2ull * 2 * pad128(c.shared_ffn) * c.hidden);
+  p.wdn_s = L.take(pass * 2ull * c.hidden * c.shared_ffn);
   p.total = L.off;
   return p;
 }
@@ -204,8 +224,9 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   void* wdn_s = W + P.wdn_s;
 
   // ---- (a) weights -> bf16 B operands (scale folded for grouped quantization)
-  cudaError_t e;
-  {
+  cudaError_t e = cudaSuccess;
+  const bool pass = dequant_pass(c, T);
+  if (pass) {
   KernelTimer kt(K_DEQUANT, s);
   e = launch_dequant(c.wbits, (const uint8_t*)w->gate_q, w->gate_s, (const uint8_t*)w->up_q, w->up_s, E, F, H, Fp, 1,
                      g_h, per_channel, wgu_r, s);
@@ -264,16 +285,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   }
 
   // ---- (d) K3 + K5: gate/up grouped GEMM with SwiGLU epilogue (routed + shared in one launch)
-  CUtensorMap a_r, a_s, b_r, b_s;
-  const uint32_t bbox = sa.gemm_bm == 256 ? 128 : 256;  // B rows per TMA box: half the tile for CTA pairs
-  if (!tmap_bf16(&a_r, x_perm, Tk, H, 128) || !tmap_bf16(&b_r, wgu_r, (uint64_t)E * 2 * Fp, H, bbox))
-    return FLUX_E_CUDA;
-  if (sh) {
-    if (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_bf16(&b_s, wgu_s, 2ull * Fsp, H, bbox)) return FLUX_E_CUDA;
-  } else {
-    a_s = a_r;
-    b_s = b_r;
-  }
+  // ---- (e) K4 + K5: down grouped GEMM -> y_perm (aliases x_perm) and y_sh
+  void* y_perm = x_perm;
   GemmArgs ga{};
   ga.n_groups = n_groups;
   ga.E = E;
@@ -297,20 +310,6 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.ld_s = Fs;
   ga.grid = kNumSMs;
   ga.bm = sa.gemm_bm;
-  {
-    KernelTimer kt(K_GEMM_GU, s);
-    if ((e = launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s)) != cudaSuccess) { set_last_error("gemm_gate_up", e); return FLUX_E_CUDA; }
-  }
-
-  // ---- (e) K4 + K5: down grouped GEMM -> y_perm (aliases x_perm) and y_sh
-  void* y_perm = x_perm;
-  if (!tmap_bf16(&a_r, act, Tk, F, 128) || !tmap_bf16(&b_r, wdn_r, (uint64_t)E * H, F, bbox)) return FLUX_E_CUDA;
-  if (sh) {
-    if (!tmap_bf16(&a_s, act_sh, T, Fs, 128) || !tmap_bf16(&b_s, wdn_s, H, Fs, bbox)) return FLUX_E_CUDA;
-  } else {
-    a_s = a_r;
-    b_s = b_r;
-  }
   GemmArgs gd = ga;
   gd.sched = sa.sched_dn;
   gd.n_tiles_r = sa.n_tiles_dn;
@@ -328,9 +327,82 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   gd.out_s = y_sh;
   gd.ld_r = H;
   gd.ld_s = H;
-  {
-    KernelTimer kt(K_GEMM_DN, s);
-    if ((e = launch_gemm(EPI_STORE, a_r, a_s, b_r, b_s, gd, s)) != cudaSuccess) { set_last_error("gemm_down", e); return FLUX_E_CUDA; }
+
+  CUtensorMap a_r, a_s, b_r, b_s;
+  if (pass) {
+    const uint32_t bbox = sa.gemm_bm == 256 ? 128 : 256;  // B rows per TMA box: half the tile for CTA pairs
+    if (!tmap_bf16(&a_r, x_perm, Tk, H, 128) || !tmap_bf16(&b_r, wgu_r, (uint64_t)E * 2 * Fp, H, bbox) ||
+        (sh && (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_bf16(&b_s, wgu_s, 2ull * Fsp, H, bbox)))) {
+      set_last_error("gate/up tensor maps", cudaErrorInvalidValue);
+      return FLUX_E_CUDA;
+    }
+    if (!sh) { a_s = a_r; b_s = b_r; }
+    {
+      KernelTimer kt(K_GEMM_GU, s);
+      if ((e = launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s)) != cudaSuccess) { set_last_error("gemm_gate_up", e); return FLUX_E_CUDA; }
+    }
+    if (!tmap_bf16(&a_r, act, Tk, F, 128) || !tmap_bf16(&b_r, wdn_r, (uint64_t)E * H, F, bbox) ||
+        (sh && (!tmap_bf16(&a_s, act_sh, T, Fs, 128) || !tmap_bf16(&b_s, wdn_s, H, Fs, bbox)))) {
+      set_last_error("down tensor maps", cudaErrorInvalidValue);
+      return FLUX_E_CUDA;
+    }
+    if (!sh) { a_s = a_r; b_s = b_r; }
+    {
+      KernelTimer kt(K_GEMM_DN, s);
+      if ((e = launch_gemm(EPI_STORE, a_r, a_s, b_r, b_s, gd, s)) != cudaSuccess) { set_last_error("gemm_down", e); return FLUX_E_CUDA; }
+    }
+  } else {
+    // fused dequant: B tiles are built on chip from the canonical quantized weights
+    const uint32_t qb = c.wbits == 4 ? 32 : 64;       // raw bytes per row per 64-wide K slice
+    const uint64_t Hq = c.wbits == 4 ? H / 2 : H, Fq = c.wbits == 4 ? F / 2 : F, Fsq = c.wbits == 4 ? Fs / 2 : Fs;
+    CUtensorMap q_r0, q_r1, q_s0, q_s1;
+    QGemmArgs qa{};
+    qa.wbits = c.wbits;
+    qa.gsz = c.group_size;
+    // gate/up
+    if (!tmap_bf16(&a_r, x_perm, Tk, H, 128) || !tmap_u8(&q_r0, w->gate_q, (uint64_t)E * F, Hq, qb) ||
+        !tmap_u8(&q_r1, w->up_q, (uint64_t)E * F, Hq, qb) ||
+        (sh && (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_u8(&q_s0, w->sh_gate_q, Fs, Hq, qb) ||
+                !tmap_u8(&q_s1, w->sh_up_q, Fs, Hq, qb)))) {
+      set_last_error("gate/up tensor maps", cudaErrorInvalidValue);
+      return FLUX_E_CUDA;
+    }
+    if (!sh) { a_s = a_r; q_s0 = q_r0; q_s1 = q_r1; }
+    qa.base = ga;
+    qa.gate_up = 1;
+    qa.qrows_r = F;
+    qa.qrows_s = Fs;
+    qa.qtotal_r = (int64_t)E * F;
+    qa.qtotal_s = Fs;
+    qa.gs_r0 = w->gate_s;
+    qa.gs_r1 = w->up_s;
+    qa.gs_s0 = w->sh_gate_s;
+    qa.gs_s1 = w->sh_up_s;
+    {
+      KernelTimer kt(K_GEMM_GU, s);
+      if ((e = launch_gemm_q(EPI_SWIGLU, a_r, a_s, q_r0, q_r1, q_s0, q_s1, qa, s)) != cudaSuccess) { set_last_error("gemm_gate_up", e); return FLUX_E_CUDA; }
+    }
+    // down
+    if (!tmap_bf16(&a_r, act, Tk, F, 128) || !tmap_u8(&q_r0, w->down_q, (uint64_t)E * H, Fq, qb) ||
+        (sh && (!tmap_bf16(&a_s, act_sh, T, Fs, 128) || !tmap_u8(&q_s0, w->sh_down_q, H, Fsq, qb)))) {
+      set_last_error("down tensor maps", cudaErrorInvalidValue);
+      return FLUX_E_CUDA;
+    }
+    if (!sh) { a_s = a_r; q_s0 = q_r0; }
+    q_r1 = q_r0;
+    q_s1 = q_s0;
+    qa.base = gd;
+    qa.gate_up = 0;
+    qa.qrows_r = H;
+    qa.qrows_s = H;
+    qa.qtotal_r = (int64_t)E * H;
+    qa.qtotal_s = H;
+    qa.gs_r0 = qa.gs_r1 = w->down_s;
+    qa.gs_s0 = qa.gs_s1 = w->sh_down_s;
+    {
+      KernelTimer kt(K_GEMM_DN, s);
+      if ((e = launch_gemm_q(EPI_STORE, a_r, a_s, q_r0, q_r1, q_s0, q_s1, qa, s)) != cudaSuccess) { set_last_error("gemm_down", e); return FLUX_E_CUDA; }
+    }
   }
 
   // ---- (f) K6 combine

@@ -161,48 +161,45 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
                                                       const uint8_t* __restrict__ q1, const float* __restrict__ s1,
                                                       int G, int N, int K, int Fp, int interleave, int gsz,
                                                       int per_channel, uint4* __restrict__ out) {
+  // one warp per output row; lanes walk the row in 8-element (16-byte) vectors
   const int64_t rows_out = interleave ? 2LL * Fp : N;
-  const int64_t vec_per_row = K / 8;
-  const int64_t total = (int64_t)G * rows_out * vec_per_row;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / vec_per_row;
-    const int kv = (int)(i - row * vec_per_row);
-    const int g = (int)(row / rows_out);
-    const int r = (int)(row - (int64_t)g * rows_out);
+  const int64_t n_rows = (int64_t)G * rows_out;
+  const int lane = threadIdx.x & 31;
+  const int vec_per_row = K / 8;
+  const int64_t wid0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t orow = wid0; orow < n_rows; orow += nw) {
+    const int g = (int)(orow / rows_out);
+    const int r = (int)(orow - (int64_t)g * rows_out);
     const uint8_t* q = q0;
     const float* s = s0;
     int src_row = r;
     if (interleave) {
-      const int blk = r / 256, w = r % 256;
+      const int blk = r >> 8, w = r & 255;
       src_row = blk * 128 + (w & 127);
       if (w >= 128) { q = q1; s = s1; }
     }
-    uint4 o = make_uint4(0, 0, 0, 0);
-    if (src_row < N) {
-      const int64_t srow = (int64_t)g * N + src_row;
-      int qi[8];
-      if (WBITS == 8) {
-        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(q + srow * K + kv * 8));
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          qi[j] = (int)(int8_t)((raw.x >> (8 * j)) & 0xFF);
-          qi[4 + j] = (int)(int8_t)((raw.y >> (8 * j)) & 0xFF);
-        }
-      } else {
-        const uint32_t raw = __ldg(reinterpret_cast<const uint32_t*>(q + srow * (K / 2) + kv * 4));
-#pragma unroll
-        for (int j = 0; j < 8; ++j) qi[j] = ((int)((raw >> (4 * j)) & 0xF) ^ 8) - 8;
-      }
-      // R1b: grouped scales -> ŵ = bf16(q · bf16(s)); q·bf16(s) is exact in fp32 (4-8 bit x 8 bit),
-      // so pack_bf16x2 performs the single rounding.  Per-channel: ŵ = q, scale in the epilogue.
-      const float sc =
-          per_channel ? 1.0f : __bfloat162float(__float2bfloat16_rn(__ldg(&s[srow * (K / gsz) + (kv * 8) / gsz])));
-      o.x = pack_bf16x2((float)qi[0] * sc, (float)qi[1] * sc);
-      o.y = pack_bf16x2((float)qi[2] * sc, (float)qi[3] * sc);
-      o.z = pack_bf16x2((float)qi[4] * sc, (float)qi[5] * sc);
-      o.w = pack_bf16x2((float)qi[6] * sc, (float)qi[7] * sc);
+    uint4* dst = out + orow * vec_per_row;
+    if (src_row >= N) {  // padding rows of the interleaved layout
+      for (int v = lane; v < vec_per_row; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
+      continue;
     }
-    out[i] = o;
+    const int64_t srow = (int64_t)g * N + src_row;
+    const float* srow_s = s + (per_channel ? 0 : srow * (K / gsz));
+    const int vec_per_grp = per_channel ? vec_per_row : gsz / 8;
+    for (int v = lane; v < vec_per_row; v += 32) {
+      const float sc = per_channel ? 0.f : __bfloat162float(__float2bfloat16_rn(__ldg(&srow_s[v / vec_per_grp])));
+      if (WBITS == 4) {
+        const uint32_t raw = __ldg(reinterpret_cast<const uint32_t*>(q + srow * (K / 2)) + v);
+        dst[v] = per_channel ? deq_int4x8<false>(raw, __floats2bfloat162_rn(0.f, 0.f))
+                             : deq_int4x8<true>(raw, __floats2bfloat162_rn(sc, sc));
+      } else {
+        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(q + srow * K) + v);
+        const uint2 a = per_channel ? deq_int8x4<false>(raw.x, 0.f) : deq_int8x4<true>(raw.x, sc);
+        const uint2 b = per_channel ? deq_int8x4<false>(raw.y, 0.f) : deq_int8x4<true>(raw.y, sc);
+        dst[v] = make_uint4(a.x, a.y, b.x, b.y);
+      }
+    }
   }
 }
 }  // namespace
@@ -211,9 +208,9 @@ cudaError_t launch_dequant(int wbits, const uint8_t* q0, const float* s0, const 
                            int N, int K, int Fp, int interleave, int gsz, int per_channel, void* out,
                            cudaStream_t st) {
   const int64_t rows_out = interleave ? 2LL * Fp : N;
-  const int64_t total = (int64_t)G * rows_out * (K / 8);
-  if (total == 0) return cudaSuccess;
-  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+  const int64_t n_rows = (int64_t)G * rows_out;
+  if (n_rows == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<int64_t>((n_rows + 7) / 8, (int64_t)kNumSMs * 16);
   if (wbits == 8)
     dequant_kernel<8><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
   else

@@ -41,7 +41,11 @@ __device__ __forceinline__ TileInfo decode(int tile, const int32_t* s_sched, int
   return {lo, local / nt, local % nt};
 }
 
-__device__ __forceinline__ float silu(float v) { return v / (1.0f + expf(-v)); }
+// SiLU(v) = v / (1 + e^-v) with the SFU exp and the fast reciprocal-divide: ~2 ulp fp32 (far below
+// the bf16 rounding of a that follows), and ~5x fewer issue slots than expf + IEEE division, which
+// matters because the epilogue shares the SM's issue bandwidth with the next tile's producers.
+// For v << 0, e^-v = inf and __fdividef(v, inf) = 0 = SiLU's limit.
+__device__ __forceinline__ float silu(float v) { return __fdividef(v, 1.0f + __expf(-v)); }
 
 // Epilogue of one accumulator slice: this thread owns TMEM lane (row) `taddr`'s lane, i.e. output
 // row `orow` (valid = inside the group).  EPI_SWIGLU: columns [0,128) = gate, [128,256) = up of
@@ -106,6 +110,48 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// In-register weight dequantization (reading R1b): exact codes, one rounding.
+// ---------------------------------------------------------------------------
+// 8 INT4 codes (one 32-bit word, even k in the low nibble) -> 8 bf16 in k order.
+template <bool GROUPED>
+__device__ __forceinline__ uint4 deq_int4x8(uint32_t w, __nv_bfloat162 s2) {
+  const uint32_t x = w ^ 0x88888888u;  // two's complement -> offset binary (q + 8)
+  uint32_t p[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) p[i] = ((x >> (4 * i)) & 0x000F000Fu) | 0x43004300u;  // bf16 {136+q_i, 136+q_{i+4}}
+  const __nv_bfloat162 off = __floats2bfloat162_rn(136.0f, 136.0f);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&p[i]);
+    v = __hsub2(v, off);               // exact q
+    if (GROUPED) v = __hmul2(v, s2);   // bf16(q * bf16(s)): exact product, one rounding
+    p[i] = *reinterpret_cast<uint32_t*>(&v);
+  }
+  uint4 o;
+  o.x = __byte_perm(p[0], p[1], 0x5410);  // (k0, k1)
+  o.y = __byte_perm(p[2], p[3], 0x5410);  // (k2, k3)
+  o.z = __byte_perm(p[0], p[1], 0x7632);  // (k4, k5)
+  o.w = __byte_perm(p[2], p[3], 0x7632);  // (k6, k7)
+  return o;
+}
+
+// 4 INT8 codes (one word, k order) -> 2 bf16x2 words; q exact via the fp32 2^23 magic.
+template <bool GROUPED>
+__device__ __forceinline__ uint2 deq_int8x4(uint32_t w, float s) {
+  const uint32_t x = w ^ 0x80808080u;
+  float f[4];
+  f[0] = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7650)) - 8388736.0f;
+  f[1] = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7651)) - 8388736.0f;
+  f[2] = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7652)) - 8388736.0f;
+  f[3] = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7653)) - 8388736.0f;
+  if (GROUPED) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] *= s;  // q·bf16(s) exact in fp32 (8 x 8 bits)
+  }
+  return make_uint2(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]));
 }
 
 inline Params make_params(const GemmArgs& g) {

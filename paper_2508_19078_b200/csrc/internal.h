@@ -112,6 +112,21 @@ struct GemmArgs {
 };
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);
+
+// Fused-dequant variant (CTA pairs): B comes straight from the quantized weights.
+struct QGemmArgs {
+  GemmArgs base;                 // bm must be 256
+  int wbits;                     // 4 or 8
+  int gsz;                       // group size along K; 0 = per output channel (scale in the epilogue)
+  int gate_up;                   // 1: CTA rank 0 dequantizes gate rows, rank 1 the matching up rows
+                                 // 0: rank r dequantizes rows [128r, 128r+128) of the 256-row tile
+  int qrows_r, qrows_s;          // rows of one group in the quantized tensor (routed, shared)
+  int64_t qtotal_r, qtotal_s;    // total rows of the quantized tensors
+  const float *gs_r0, *gs_r1, *gs_s0, *gs_s1;  // group scales [rows][K/gsz] of the rank-0 / rank-1 sources
+};
+cudaError_t launch_gemm_q(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& q_r0,
+                          const CUtensorMap& q_r1, const CUtensorMap& q_s0, const CUtensorMap& q_s1,
+                          const QGemmArgs& a, cudaStream_t st);
 cudaError_t launch_dequant(int wbits, const uint8_t* q0, const float* s0, const uint8_t* q1, const float* s1, int G,
                            int N, int K, int Fp, int interleave, int gsz, int per_channel, void* out,
                            cudaStream_t st);

@@ -108,6 +108,31 @@ def test_chunk_and_run_invariance():
     assert torch.equal(torch.cat([ya, yb]), y_full)
 
 
+@pytest.mark.parametrize("name", ["int4_shared", "int8_ragged", "int4_e64"])
+def test_weight_paths_bit_identical(name, monkeypatch):
+    """Fused in-GEMM dequantization, the separate dequant pass (CTA-pair GEMM) and the 1-CTA GEMM all
+    produce bit-identical layers: the choice between them is a pure performance policy."""
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
+    from paper_2508_19078_b200 import synthetic
+    cfg = SMALL[name]
+    shape = ModelShape.of(cfg)
+    qm = QuantizedModel(shape)
+    qm.quantize_from(synthetic.master_weights(cfg))
+    x = synthetic.tokens(cfg, 0, cfg.tokens)
+    outs = []
+    for env in ({"FLUX_GEMM_FUSED_DEQUANT": "1"}, {"FLUX_GEMM_DEQUANT_PASS": "1"}, {"FLUX_GEMM_1SM": "1"}):
+        for k in ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        prof = Profiler(shape, cfg.tokens)
+        prof.run(qm, x)
+        torch.cuda.synchronize()
+        outs.append((prof.y[(cfg.n_layers - 1) % 2].clone(), prof.ids.clone(), prof.hist.clone()))
+    for y, ids, hist in outs[1:]:
+        assert torch.equal(y, outs[0][0]) and torch.equal(ids, outs[0][1]) and torch.equal(hist, outs[0][2])
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("variant", ["balanced", "tuning", "zero_alpha", "singletons"])
 def test_merge_parity(dtype, variant):
