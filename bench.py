@@ -280,7 +280,8 @@ def main():
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(f"{args.config}:gemm_gate_up:{T}")
+            # dram read+write bytes per launch from the committed `ncu --set full` capture (profiles/)
+            traffic = json.load(open(tp)).get(f"{args.config}:{T}:K3/K5 gate/up GEMM (pair)")
         kernels = {n: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                    for n, v in kern.items() if v[1]}
         line = {

@@ -1,0 +1,109 @@
+"""Summarise ncu captures into profiles/ (tracked): per-kernel launch shares from a
+--metrics gpu__time_duration.sum launch list, and key counters of a --set full capture.
+
+usage: python tools/ncu_summary.py launches <launches.csv> <out.md>
+       python tools/ncu_summary.py full <report.ncu-rep> <out.md> [traffic.json key-prefix]
+"""
+import collections
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+NAMES = [("grouped_gemm_pair_kernel<0>", "K3/K5 gate/up GEMM (pair)"), ("grouped_gemm_pair_kernel<1>", "K4/K5 down GEMM (pair)"),
+         ("grouped_gemm_kernel<0>", "K3/K5 gate/up GEMM (1-CTA)"), ("grouped_gemm_kernel<1>", "K4/K5 down GEMM (1-CTA)"),
+         ("router_kernel", "K1 router"), ("schedule_kernel", "K2 schedule"), ("scatter_kernel", "K2 scatter"),
+         ("grouped_gemm_pair_kernel<(int)0>", "K3/K5 gate/up GEMM (pair)"),
+         ("grouped_gemm_pair_kernel<(int)1>", "K4/K5 down GEMM (pair)"),
+         ("grouped_gemm_pair_q_kernel<(int)0", "K3/K5 gate/up GEMM (fused dequant)"),
+         ("grouped_gemm_pair_q_kernel<(int)1", "K4/K5 down GEMM (fused dequant)"),
+         ("grouped_gemm_kernel<(int)0>", "K3/K5 gate/up GEMM (1-CTA)"), ("grouped_gemm_kernel<(int)1>", "K4/K5 down GEMM (1-CTA)"),
+         ("combine_kernel", "K6 combine"), ("quantize_kernel", "K0 quantize"), ("dequant_kernel", "K3/K4 dequant pass"),
+         ("merge_kernel", "K7 merge")]
+
+
+def label(name):
+    for key, lab in NAMES:
+        if key in name:
+            return lab
+    return name[:60]
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr = rows[i]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+    agg = collections.OrderedDict()
+    for r in rows[i + 1:]:
+        ms = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6)
+        agg.setdefault(label(r[ki]), []).append(ms)
+    total = sum(sum(v) for v in agg.values())
+    lines = [f"# ncu launch list — {path.split('/')[-1]}", "",
+             "`ncu --metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 1 --warmup 1`"
+             " (warm-up + timed + e2e step: 3 profiling rounds). Launches are serialised and cold-cache: compare"
+             " SHARES with bench.py's live per-kernel CUDA-event times, not absolutes.", "",
+             "| kernel | launches | mean ms | total ms | share |", "|---|---:|---:|---:|---:|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| {k} | {len(v)} | {sum(v) / len(v):.3f} | {sum(v):.1f} | {100 * sum(v) / total:.1f}% |")
+    lines.append(f"| **all** | {sum(len(v) for v in agg.values())} | | {total:.1f} | 100% |")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_op_read_hit_rate.pct",
+        "l1tex__m_xbar2l1tex_read_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active"]
+
+
+def full(path, out, traffic_prefix=None):
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units = rows[0], rows[1]
+    lines = [f"# ncu --set full — {path.split('/')[-1]}", ""]
+    traffic = {}
+    for r in rows[2:]:
+        d = {h: (u, v) for h, u, v in zip(hdr, units, r)}
+        name = d.get("Kernel Name", ("", "?"))[1]
+        lines += [f"## {label(name)}", f"`{name[:150]}`", "", "| metric | unit | value |", "|---|---|---:|"]
+        for k in KEYS:
+            # ncu prefixes some section metrics; match by suffix
+            hit = [h for h in d if h == k or h.endswith("." + k)]
+            if hit:
+                u, v = d[hit[0]]
+                lines.append(f"| {k} | {u} | {v} |")
+        rd = d.get("dram__bytes_read.sum")
+        wr = d.get("dram__bytes_write.sum")
+        if rd and wr:
+            mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tb = float(rd[1].replace(",", "")) * mult.get(rd[0], 1) + float(wr[1].replace(",", "")) * mult.get(wr[0], 1)
+            lines.append(f"| dram read+write per launch | byte | {tb:.4g} |")
+            traffic[label(name)] = tb
+        lines.append("")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    return traffic
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        tr = full(sys.argv[2], sys.argv[3])
+        if len(sys.argv) > 4:
+            p = "profiles/traffic.json"
+            try:
+                cur = json.load(open(p))
+            except Exception:
+                cur = {}
+            for k, v in tr.items():
+                cur[f"{sys.argv[4]}:{k}"] = v
+            json.dump(cur, open(p, "w"), indent=1)
