@@ -81,6 +81,10 @@ static bool dequant_pass(const flux_moe_cfg& c, int64_t T) {
   return T * c.top_k >= (int64_t)2048 * c.n_experts;
 }
 static int gemm_bm() { return env_on("FLUX_GEMM_1SM") ? 128 : 256; }
+// K6 placement with shared experts: a standalone gather kernel (default; HBM-bound at ~80% of the
+// copy roofline) or fused into the shared-MLP down GEMM's epilogue (FLUX_FUSED_COMBINE=1; bit-
+// identical, saves the y_sh round-trip, but its per-thread-row gathers are latency-bound today).
+static bool fused_combine() { return env_on("FLUX_FUSED_COMBINE"); }
 
 static bool tmap_u8(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_bytes, uint32_t box_cols) {
   return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rows, cols_bytes, cols_bytes, box_cols, 128,
@@ -99,7 +103,7 @@ struct Layout {
 };
 struct WsPlan {
   size_t tile_counts, tile_base, rank, offsets, token_index, inv_pos, counter, sched_gu, sched_dn, row0, rows;
-  size_t x_perm, act, act_sh, y_sh, wgu_r, wdn_r, wgu_s, wdn_s;
+  size_t x_perm, act, act_sh, sh_sched, y_sh, wgu_r, wdn_r, wgu_s, wdn_s;
   size_t total;
 };
 int pad128(int v) { return (v + 127) / 128 * 128; }
@@ -124,7 +128,8 @@ WsPlan plan(const flux_moe_cfg& c, int64_t T) {
   p.x_perm = L.take(2ull * Tk * c.hidden);  // reused as y_perm after the gate/up GEMM
   p.act = L.take(2ull * Tk * c.ffn);
   p.act_sh = L.take(2ull * T * c.shared_ffn);
-  p.y_sh = L.take(c.shared_ffn ? 2ull * T * c.hidden : 0);
+  p.sh_sched = L.take(4 * sizeof(int32_t));  // sched_sh[2], row0_sh[1], rows_sh[1]
+  p.y_sh = L.take(c.shared_ffn && !fused_combine() ? 2ull * T * c.hidden : 0);
   const size_t pass = dequant_pass(c, T) ? 1 : 0;  // bf16 B operands only for the separate-pass path
   p.wgu_r = L.take(pass * 2ull * c.n_experts * 2 * pad128(c.ffn) * c.hidden);
   p.wdn_r = L.take(pass * 2ull * c.n_experts * c.hidden * c.ffn);
@@ -217,7 +222,9 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   void* x_perm = W + P.x_perm;
   void* act = W + P.act;
   void* act_sh = W + P.act_sh;
-  void* y_sh = W + P.y_sh;
+  int32_t* sh_sched = (int32_t*)(W + P.sh_sched);
+  const bool fuse_combine = sh && fused_combine();
+  void* y_sh = W + P.y_sh;  // shared-MLP output (unused when the combine is fused into its down GEMM)
   void* wgu_r = W + P.wgu_r;
   void* wdn_r = W + P.wdn_r;
   void* wgu_s = W + P.wgu_s;
@@ -273,6 +280,9 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   sa.grp_row0 = (int32_t*)(W + P.row0);
   sa.grp_rows = (int32_t*)(W + P.rows);
   sa.gemm_bm = gemm_bm();
+  sa.sched_sh = sh ? sh_sched : nullptr;
+  sa.grp_row0_sh = sh_sched + 2;
+  sa.grp_rows_sh = sh_sched + 3;
   {
     KernelTimer kt(K_SCHEDULE, s);
     if ((e = launch_schedule(sa, s)) != cudaSuccess) { set_last_error("schedule", e); return FLUX_E_CUDA; }
@@ -327,6 +337,21 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   gd.out_s = y_sh;
   gd.ld_r = H;
   gd.ld_s = H;
+  if (fuse_combine) gd.n_groups = E;  // routed experts only; the shared MLP's down GEMM carries K6
+  const void* resid = residual ? residual : x;
+  // the shared MLP's down GEMM alone, epilogue = the layer output (K6 fused): one group, E = 0
+  GemmArgs gsc = gd;
+  gsc.n_groups = 1;
+  gsc.E = 0;
+  gsc.sched = sa.sched_sh;
+  gsc.grp_row0 = sa.grp_row0_sh;
+  gsc.grp_rows = sa.grp_rows_sh;
+  gsc.out_s = out->y;
+  gsc.resid = resid;
+  gsc.y_perm = y_perm;
+  gsc.topk_w = out->topk_w;
+  gsc.inv_pos = inv_pos;
+  gsc.k = k;
 
   CUtensorMap a_r, a_s, b_r, b_s;
   if (pass) {
@@ -346,10 +371,13 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
       set_last_error("down tensor maps", cudaErrorInvalidValue);
       return FLUX_E_CUDA;
     }
-    if (!sh) { a_s = a_r; b_s = b_r; }
     {
       KernelTimer kt(K_GEMM_DN, s);
-      if ((e = launch_gemm(EPI_STORE, a_r, a_s, b_r, b_s, gd, s)) != cudaSuccess) { set_last_error("gemm_down", e); return FLUX_E_CUDA; }
+      if ((e = launch_gemm(EPI_STORE, a_r, sh ? a_s : a_r, b_r, sh ? b_s : b_r, gd, s)) != cudaSuccess) { set_last_error("gemm_down", e); return FLUX_E_CUDA; }
+    }
+    if (fuse_combine) {
+      KernelTimer kt(K_GEMM_DN_SH_COMBINE, s);
+      if ((e = launch_gemm(EPI_COMBINE, a_s, a_s, b_s, b_s, gsc, s)) != cudaSuccess) { set_last_error("gemm_down_shared_combine", e); return FLUX_E_CUDA; }
     }
   } else {
     // fused dequant: B tiles are built on chip from the canonical quantized weights
@@ -388,7 +416,6 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
       set_last_error("down tensor maps", cudaErrorInvalidValue);
       return FLUX_E_CUDA;
     }
-    if (!sh) { a_s = a_r; q_s0 = q_r0; }
     q_r1 = q_r0;
     q_s1 = q_s0;
     qa.base = gd;
@@ -401,16 +428,24 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
     qa.gs_s0 = qa.gs_s1 = w->sh_down_s;
     {
       KernelTimer kt(K_GEMM_DN, s);
-      if ((e = launch_gemm_q(EPI_STORE, a_r, a_s, q_r0, q_r1, q_s0, q_s1, qa, s)) != cudaSuccess) { set_last_error("gemm_down", e); return FLUX_E_CUDA; }
+      if ((e = launch_gemm_q(EPI_STORE, a_r, sh ? a_s : a_r, q_r0, q_r1, sh ? q_s0 : q_r0, sh ? q_s1 : q_r1, qa,
+                             s)) != cudaSuccess) { set_last_error("gemm_down", e); return FLUX_E_CUDA; }
+    }
+    if (fuse_combine) {
+      qa.base = gsc;
+      KernelTimer kt(K_GEMM_DN_SH_COMBINE, s);
+      if ((e = launch_gemm_q(EPI_COMBINE, a_s, a_s, q_s0, q_s1, q_s0, q_s1, qa, s)) != cudaSuccess) { set_last_error("gemm_down_shared_combine", e); return FLUX_E_CUDA; }
     }
   }
 
-  // ---- (f) K6 combine
-  {
+  // ---- (f) K6 combine: fused into the shared-MLP down GEMM when there is one, else standalone
+  if (!fuse_combine) {
     KernelTimer kt(K_COMBINE, s);
-    if (launch_combine(T, H, k, residual ? residual : x, sh ? y_sh : nullptr, y_perm, out->topk_w, inv_pos, out->y,
-                       s) != cudaSuccess)
+    if ((e = launch_combine(T, H, k, resid, sh ? y_sh : nullptr, y_perm, out->topk_w, inv_pos, out->y, s)) !=
+        cudaSuccess) {
+      set_last_error("combine", e);
       return FLUX_E_CUDA;
+    }
   }
   return FLUX_OK;
 }

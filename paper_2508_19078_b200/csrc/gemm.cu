@@ -222,7 +222,9 @@ cudaError_t launch_gemm_1sm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorM
                             const CUtensorMap& b_s, const GemmArgs& g, cudaStream_t st) {
   const Params p = make_params(g);
   if (g.n_groups > kMaxGroups - 1) return cudaErrorInvalidValue;
-  auto kern = epi == EPI_SWIGLU ? grouped_gemm_kernel<EPI_SWIGLU> : grouped_gemm_kernel<EPI_STORE>;
+  auto kern = epi == EPI_SWIGLU  ? grouped_gemm_kernel<EPI_SWIGLU>
+              : epi == EPI_STORE ? grouped_gemm_kernel<EPI_STORE>
+                                 : grouped_gemm_kernel<EPI_COMBINE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (e != cudaSuccess) return e;
   kern<<<g.grid, kThreads, kSmemBytes, st>>>(a_r, a_s, b_r, b_s, p);

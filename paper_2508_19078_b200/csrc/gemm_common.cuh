@@ -23,6 +23,12 @@ struct Params {
   const float *cs0_r, *cs1_r, *cs0_s, *cs1_s;  // per-channel scales [group][N] or null
   void *out_r, *out_s;
   int64_t ld_r, ld_s;
+  // EPI_COMBINE (shared-MLP down GEMM only): y = bf16(resid + bf16(acc) + Σ_j w_j · y_perm[inv_pos_j])
+  const __nv_bfloat16* resid;
+  const __nv_bfloat16* y_perm;
+  const float* topk_w;
+  const int32_t* inv_pos;
+  int k;
 };
 
 struct TileInfo {
@@ -85,6 +91,72 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
         dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
+    }
+  } else if constexpr (EPI == EPI_COMBINE) {
+    // The layer output for token row `orow` (K6 fused here, reading R6): identical order and
+    // roundings to combine.cu — acc = r; acc += bf16(sh); acc = fma(w_j, o_j, acc) for j = 0..k-1.
+    int pos[8];
+    float wt[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      pos[jj] = 0;
+      wt[jj] = 0.f;
+      if (valid && jj < p.k) {
+        pos[jj] = __ldg(&p.inv_pos[orow * p.k + jj]);
+        wt[jj] = __ldg(&p.topk_w[orow * p.k + jj]);
+      }
+    }
+    const int H = N;
+    for (int j = 0; j < kBN; j += 16) {
+      const int c0 = ti.n * kBN + j;
+      float v[16];
+      tmem_ld16(taddr + j, v);
+      tmem_ld_wait();
+      if (c0 >= N || !valid) continue;
+      // issue every load of this 16-column chunk before using any of them
+      uint4 rr[2], oo[8][2];
+      const uint4* rp = reinterpret_cast<const uint4*>(p.resid + orow * H + c0);
+      rr[0] = __ldg(rp);
+      rr[1] = __ldg(rp + 1);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (jj < p.k) {
+          const uint4* op = reinterpret_cast<const uint4*>(p.y_perm + (int64_t)pos[jj] * H + c0);
+          oo[jj][0] = __ldg(op);
+          oo[jj][1] = __ldg(op + 1);
+        }
+      float acc[16];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&rr[h]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(b[i]);
+          acc[8 * h + 2 * i] = f.x;
+          acc[8 * h + 2 * i + 1] = f.y;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] += __bfloat162float(__float2bfloat16_rn(v[i]));  // o_sh = bf16(a·ŵ)
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (jj < p.k) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&oo[jj][h]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(b[i]);
+              acc[8 * h + 2 * i] = fmaf(wt[jj], f.x, acc[8 * h + 2 * i]);
+              acc[8 * h + 2 * i + 1] = fmaf(wt[jj], f.y, acc[8 * h + 2 * i + 1]);
+            }
+          }
+        }
+      uint4* dst = reinterpret_cast<uint4*>(out + c0);
+      dst[0] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                          pack_bf16x2(acc[6], acc[7]));
+      dst[1] = make_uint4(pack_bf16x2(acc[8], acc[9]), pack_bf16x2(acc[10], acc[11]),
+                          pack_bf16x2(acc[12], acc[13]), pack_bf16x2(acc[14], acc[15]));
     }
   } else {
     for (int j = 0; j < kBN; j += 16) {
@@ -176,6 +248,11 @@ inline Params make_params(const GemmArgs& g) {
   p.out_s = g.out_s;
   p.ld_r = g.ld_r;
   p.ld_s = g.ld_s;
+  p.resid = reinterpret_cast<const __nv_bfloat16*>(g.resid);
+  p.y_perm = reinterpret_cast<const __nv_bfloat16*>(g.y_perm);
+  p.topk_w = g.topk_w;
+  p.inv_pos = g.inv_pos;
+  p.k = g.k;
   return p;
 }
 

@@ -157,7 +157,9 @@ cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& 
   if (g.bm == 128) return launch_gemm_1sm(epi, a_r, a_s, b_r, b_s, g, st);
   if (g.bm != 256 || g.n_groups > kMaxGroups - 1) return cudaErrorInvalidValue;
   const Params p = make_params(g);
-  auto kern = epi == EPI_SWIGLU ? grouped_gemm_pair_kernel<EPI_SWIGLU> : grouped_gemm_pair_kernel<EPI_STORE>;
+  auto kern = epi == EPI_SWIGLU  ? grouped_gemm_pair_kernel<EPI_SWIGLU>
+              : epi == EPI_STORE ? grouped_gemm_pair_kernel<EPI_STORE>
+                                 : grouped_gemm_pair_kernel<EPI_COMBINE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (e != cudaSuccess) return e;
   kern<<<(g.grid / 2) * 2, kThreads, kSmemBytes, st>>>(a_r, a_s, b_r, b_s, p);

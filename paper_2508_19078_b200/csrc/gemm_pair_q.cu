@@ -311,6 +311,7 @@ cudaError_t launch_gemm_q(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap
   if (epi == E_ && g.wbits == W_ && grouped == G_) kern = grouped_gemm_pair_q_kernel<E_, W_, G_>;
   PICK(EPI_SWIGLU, 4, true) PICK(EPI_SWIGLU, 4, false) PICK(EPI_SWIGLU, 8, true) PICK(EPI_SWIGLU, 8, false)
   PICK(EPI_STORE, 4, true) PICK(EPI_STORE, 4, false) PICK(EPI_STORE, 8, true) PICK(EPI_STORE, 8, false)
+  PICK(EPI_COMBINE, 4, true) PICK(EPI_COMBINE, 4, false) PICK(EPI_COMBINE, 8, true) PICK(EPI_COMBINE, 8, false)
 #undef PICK
   if (!kern) return cudaErrorInvalidValue;
   const int smem = g.wbits == 4 ? Cfg<4>::kSmemBytes : Cfg<8>::kSmemBytes;

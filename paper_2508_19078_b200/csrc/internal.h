@@ -22,7 +22,7 @@ inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_O
 // ---------------------------------------------------------------- per-kernel timing (timing.cpp)
 enum KernelKind {
   K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_SCHEDULE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
-  FLUX_NUM_KERNELS
+  K_GEMM_DN_SH_COMBINE, FLUX_NUM_KERNELS
 };
 // RAII: counts one launch; when timing is enabled records CUDA events around it on `st`.
 class KernelTimer {
@@ -81,6 +81,9 @@ struct ScheduleArgs {
   int32_t* grp_row0;        // [n_groups] first A row of each group
   int32_t* grp_rows;        // [n_groups] rows of each group
   int gemm_bm;              // GEMM tile rows (128 or 256)
+  int32_t* sched_sh;        // [2] tile prefix of the shared-MLP-only down GEMM (fused combine)
+  int32_t* grp_row0_sh;     // [1] = 0
+  int32_t* grp_rows_sh;     // [1] = T
 };
 cudaError_t launch_schedule(const ScheduleArgs& a, cudaStream_t st);
 cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const int32_t* ids, const int32_t* rank,
@@ -92,7 +95,7 @@ cudaError_t launch_combine(int64_t T, int H, int k, const void* residual, const 
                            const float* w, const int32_t* inv_pos, void* y, cudaStream_t st);
 
 // K3/K4/K5 (gemm.cu)
-enum GemmEpi { EPI_SWIGLU = 0, EPI_STORE = 1 };
+enum GemmEpi { EPI_SWIGLU = 0, EPI_STORE = 1, EPI_COMBINE = 2 };
 struct GemmArgs {
   // groups 0..E-1: routed experts (A = tm_a_r rows grp_row0.., B = tm_b_r rows g*b_rows_r..);
   // group E (if n_groups > E): the shared MLP (A = tm_a_s, B = tm_b_s)
@@ -109,6 +112,12 @@ struct GemmArgs {
   int64_t ld_r, ld_s;
   int grid;
   int bm;                   // rows per tile: 128 (1-CTA kernel) or 256 (CTA-pair kernel)
+  // EPI_COMBINE only (shared-MLP down GEMM whose epilogue writes the layer output)
+  const void* resid;        // bf16 [T][H]
+  const void* y_perm;       // bf16 [T*k][H] routed expert outputs
+  const float* topk_w;      // [T][k]
+  const int32_t* inv_pos;   // [T][k]
+  int k;
 };
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);

@@ -100,6 +100,12 @@ __global__ void __launch_bounds__(256) schedule_kernel(ScheduleArgs a) {
   if (threadIdx.x == 0) {
     a.sched_gu[n_groups] = carry_gu;
     a.sched_dn[n_groups] = carry_dn;
+    if (a.sched_sh) {  // the shared MLP alone (down GEMM with the fused combine epilogue)
+      a.sched_sh[0] = 0;
+      a.sched_sh[1] = (int)((a.T + a.gemm_bm - 1) / a.gemm_bm) * a.n_tiles_dn_sh;
+      a.grp_row0_sh[0] = 0;
+      a.grp_rows_sh[0] = (int)a.T;
+    }
   }
   for (int g = threadIdx.x; g <= a.E; g += 256) {
     const int off = g < a.E ? a.grp_row0[g] : carry_rows;
