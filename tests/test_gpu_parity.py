@@ -178,6 +178,36 @@ def test_merge_parity(dtype, variant):
         assert torch.equal(out, dev_W)  # |E_c| = 1 -> identity, bit for bit
 
 
+def test_quantizer_ties_and_extremes_bit_exact():
+    """Half-integer quotients (ties to even), saturation, zero and tiny groups: the GPU quantizer's
+    reciprocal fast path must fall back to the IEEE division exactly where it matters."""
+    import json
+    import os
+    import paper_2508_19078_b200 as F
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "quantize_examples.json")))
+    rng = np.random.default_rng(11)
+    for wbits in (4, 8):
+        qmax = (1 << (wbits - 1)) - 1
+        rows = []
+        for c in gold["cases"]:
+            rows.append(np.array(c["w"] + [0.0] * 60, np.float32))
+        for _ in range(200):  # every element an exact multiple of s/2 -> many exact ties
+            s = np.float32(2.0) ** rng.integers(-20, 10)
+            k = rng.integers(-2 * qmax - 1, 2 * qmax + 2, size=64).astype(np.float32)
+            k[0] = 2 * qmax  # pins max|w| = qmax*s exactly
+            rows.append((k * s / 2).astype(np.float32))
+        rows.append(np.full(64, 1e-40, np.float32))  # denormal group
+        w = np.stack(rows)
+        q_ref, s_ref = oracle.quantize(w, wbits, 64)
+        tw = torch.from_numpy(w).cuda()
+        q = torch.empty(w.shape[0], 64 // (2 if wbits == 4 else 1), dtype=torch.uint8, device="cuda")
+        s = torch.empty(w.shape[0], 1, dtype=torch.float32, device="cuda")
+        F.quantize_weights(tw, wbits, 64, q, s)
+        qq = oracle.pack_int4(q_ref) if wbits == 4 else q_ref.view(np.uint8)
+        assert np.array_equal(q.cpu().numpy(), qq), wbits
+        assert np.array_equal(s.cpu().numpy(), s_ref), wbits
+
+
 def test_quantizer_direct_bit_exact():
     import paper_2508_19078_b200 as F
     rng = np.random.default_rng(3)

@@ -1,0 +1,82 @@
+"""Micro-benchmarks of single libflux entry points at BASELINE sizes (diagnostics, not bench lines).
+
+usage: python tools/micro.py [quantize] [merge] [layer]
+Each prints achieved algorithmic GB/s (HBM-bound kernels) against MEASURED_PEAKS.json.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2508_19078_b200 as F  # noqa: E402
+import synth  # noqa: E402
+
+
+def timed(fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p))["hbm_gbs"] if os.path.exists(p) else 6650.0
+
+
+def quantize():
+    cfg = synth.CONFIGS["deepseek_moe"]
+    R, K = 4 * cfg.n_experts * cfg.ffn, cfg.hidden  # 4 layers of routed gate weights
+    w = torch.randn(R, K, device="cuda").to(torch.bfloat16)
+    for wbits, g in ((4, 128), (8, 0)):
+        q = torch.empty(R, K // (2 if wbits == 4 else 1), dtype=torch.uint8, device="cuda")
+        s = torch.empty(R, K // (g or K), dtype=torch.float32, device="cuda")
+        ms = timed(lambda: F.quantize_weights(w, wbits, g, q, s))
+        by = w.numel() * 2 + q.numel() + s.numel() * 4
+        print(f"quantize INT{wbits} g={g}: {ms:.3f} ms  {by / ms / 1e6:.0f} GB/s  ({by / ms / 1e6 / peak():.2f} of peak)")
+
+
+def merge():
+    cfg = synth.CONFIGS["deepseek_moe"]
+    E, C = cfg.n_experts, 16
+    numel = cfg.ffn * cfg.hidden
+    W = torch.randn(E, numel, device="cuda").to(torch.bfloat16)
+    cl = torch.arange(E, dtype=torch.int32, device="cuda") % C
+    al = torch.rand(E, device="cuda")
+    out = torch.empty(C, numel, dtype=torch.bfloat16, device="cuda")
+    ms = timed(lambda: F.merge_experts(W, cl, al, C, out))
+    by = W.numel() * 2 + out.numel() * 2
+    print(f"merge 64->16 bf16 one family/layer: {ms:.3f} ms  {by / ms / 1e6:.0f} GB/s  ({by / ms / 1e6 / peak():.2f})")
+
+
+def layer():
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
+    from paper_2508_19078_b200 import synthetic
+    cfg = synth.CONFIGS["deepseek_moe"].with_(n_layers=1)
+    shape = ModelShape.of(cfg)
+    qm = QuantizedModel(shape)
+    qm.quantize_from(synthetic.master_weights(cfg))
+    prof = Profiler(shape, cfg.tokens, with_de=True)
+    x = synthetic.tokens(cfg, 0, cfg.tokens)
+    F.timing_read(reset=True)
+    F.timing_enable(True)
+    ms = timed(lambda: prof.run(qm, x), reps=5, warm=2)
+    F.timing_enable(False)
+    k = F.timing_read(reset=True)
+    print(f"one DeepSeek layer, 262144 tokens: {ms:.2f} ms;",
+          {n: round(v[0] / max(v[1], 1), 3) for n, v in k.items() if v[1]})
+
+
+if __name__ == "__main__":
+    for what in sys.argv[1:] or ["quantize", "merge", "layer"]:
+        globals()[what]()
