@@ -85,10 +85,23 @@ static int gemm_bm() { return env_on("FLUX_GEMM_1SM") ? 128 : 256; }
 // copy roofline) or fused into the shared-MLP down GEMM's epilogue (FLUX_FUSED_COMBINE=1; bit-
 // identical, saves the y_sh round-trip, but its per-thread-row gathers are latency-bound today).
 static bool fused_combine() { return env_on("FLUX_FUSED_COMBINE"); }
+// Routed A rows of the gate/up GEMM: materialised in expert order by K2 (default) or gathered from
+// x inside the CTA-pair GEMM with TMA tile::gather4 (FLUX_GATHER_A=1; bit-identical).  Measured on
+// B200: gather4 delivers ~5 B/clk/SM (~100 cycles per 512-byte request), and each A tile is fetched
+// by every n-tile (11 for the DeepSeek shape), so the gathered GEMM runs ~2.5x slower than writing
+// x_perm once (1.4 ms per layer) — kept as an opt-in for small or latency-bound batches.
+static bool gather_routed_a() { return env_on("FLUX_GATHER_A") && gemm_bm() == 256; }
 
 static bool tmap_u8(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_bytes, uint32_t box_cols) {
   return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rows, cols_bytes, cols_bytes, box_cols, 128,
                       CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+// A operand of the routed gate/up GEMM: a gather map over x (box {64 cols, 1 row}, rows picked by
+// token_index with tile::gather4) for the CTA-pair kernels, else the materialised x_perm.
+static bool tmap_a_routed(CUtensorMap* m, bool gather, const void* x, const void* x_perm, int64_t T, int64_t Tk,
+                          int H) {
+  if (gather) return tmap_bf16(m, x, T, H, 1);
+  return tmap_bf16(m, x_perm, Tk, H, 128);
 }
 
 // ---------------------------------------------------------------- workspace layout
@@ -103,7 +116,7 @@ struct Layout {
 };
 struct WsPlan {
   size_t tile_counts, tile_base, rank, offsets, token_index, inv_pos, counter, sched_gu, sched_dn, row0, rows;
-  size_t x_perm, act, act_sh, sh_sched, y_sh, wgu_r, wdn_r, wgu_s, wdn_s;
+  size_t x_perm, y_perm, act, act_sh, sh_sched, y_sh, wgu_r, wdn_r, wgu_s, wdn_s;
   size_t total;
 };
 int pad128(int v) { return (v + 127) / 128 * 128; }
@@ -125,7 +138,9 @@ WsPlan plan(const flux_moe_cfg& c, int64_t T) {
   p.sched_dn = L.take(sizeof(int32_t) * (n_groups + 1));
   p.row0 = L.take(sizeof(int32_t) * n_groups);
   p.rows = L.take(sizeof(int32_t) * n_groups);
-  p.x_perm = L.take(2ull * Tk * c.hidden);  // reused as y_perm after the gate/up GEMM
+  // x_perm (routed A rows materialised by K2) unless the GEMM gathers them; y_perm always.
+  p.x_perm = L.take(gather_routed_a() ? 0 : 2ull * Tk * c.hidden);
+  p.y_perm = L.take(2ull * Tk * c.hidden);
   p.act = L.take(2ull * Tk * c.ffn);
   p.act_sh = L.take(2ull * T * c.shared_ffn);
   p.sh_sched = L.take(4 * sizeof(int32_t));  // sched_sh[2], row0_sh[1], rows_sh[1]
@@ -219,7 +234,9 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   int32_t* offsets = (int32_t*)(W + P.offsets);
   int32_t* token_index = out->token_index ? out->token_index : (int32_t*)(W + P.token_index);
   int32_t* inv_pos = (int32_t*)(W + P.inv_pos);
-  void* x_perm = W + P.x_perm;
+  const bool gather_a = gather_routed_a();
+  void* x_perm = gather_a ? nullptr : W + P.x_perm;
+  void* y_perm = W + P.y_perm;
   void* act = W + P.act;
   void* act_sh = W + P.act_sh;
   int32_t* sh_sched = (int32_t*)(W + P.sh_sched);
@@ -296,7 +313,6 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
 
   // ---- (d) K3 + K5: gate/up grouped GEMM with SwiGLU epilogue (routed + shared in one launch)
   // ---- (e) K4 + K5: down grouped GEMM -> y_perm (aliases x_perm) and y_sh
-  void* y_perm = x_perm;
   GemmArgs ga{};
   ga.n_groups = n_groups;
   ga.E = E;
@@ -320,7 +336,9 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.ld_s = Fs;
   ga.grid = kNumSMs;
   ga.bm = sa.gemm_bm;
+  ga.gather_idx = gather_a ? token_index : nullptr;
   GemmArgs gd = ga;
+  gd.gather_idx = nullptr;  // the down GEMM reads act, materialised in permuted order by K3
   gd.sched = sa.sched_dn;
   gd.n_tiles_r = sa.n_tiles_dn;
   gd.n_tiles_s = sa.n_tiles_dn_sh;
@@ -356,7 +374,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   CUtensorMap a_r, a_s, b_r, b_s;
   if (pass) {
     const uint32_t bbox = sa.gemm_bm == 256 ? 128 : 256;  // B rows per TMA box: half the tile for CTA pairs
-    if (!tmap_bf16(&a_r, x_perm, Tk, H, 128) || !tmap_bf16(&b_r, wgu_r, (uint64_t)E * 2 * Fp, H, bbox) ||
+    if (!tmap_a_routed(&a_r, gather_a, x, x_perm, T, Tk, H) || !tmap_bf16(&b_r, wgu_r, (uint64_t)E * 2 * Fp, H, bbox) ||
         (sh && (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_bf16(&b_s, wgu_s, 2ull * Fsp, H, bbox)))) {
       set_last_error("gate/up tensor maps", cudaErrorInvalidValue);
       return FLUX_E_CUDA;
@@ -388,7 +406,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
     qa.wbits = c.wbits;
     qa.gsz = c.group_size;
     // gate/up
-    if (!tmap_bf16(&a_r, x_perm, Tk, H, 128) || !tmap_u8(&q_r0, w->gate_q, (uint64_t)E * F, Hq, qb) ||
+    if (!tmap_a_routed(&a_r, gather_a, x, x_perm, T, Tk, H) || !tmap_u8(&q_r0, w->gate_q, (uint64_t)E * F, Hq, qb) ||
         !tmap_u8(&q_r1, w->up_q, (uint64_t)E * F, Hq, qb) ||
         (sh && (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_u8(&q_s0, w->sh_gate_q, Fs, Hq, qb) ||
                 !tmap_u8(&q_s1, w->sh_up_q, Fs, Hq, qb)))) {

@@ -29,6 +29,8 @@ struct Params {
   const float* topk_w;
   const int32_t* inv_pos;
   int k;
+  // routed A rows gathered from x by token id (TMA tile::gather4) instead of a materialised x_perm
+  const int32_t* gather_idx;  // token_index [T*k] or null
 };
 
 struct TileInfo {
@@ -185,6 +187,35 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
 }
 
 // ---------------------------------------------------------------------------
+// A operand producer of the CTA-pair kernels, run by all 32 lanes of the producer warp.
+// Per tile: if rows come from a gather (routed groups with gather_idx), the warp stages the 128
+// token ids of this CTA's rows in shared memory (rows past the group end read token 0; they are
+// masked in the epilogue).  Per K slice, lane 0 issues one 128-row box, or 32 tile::gather4.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void stage_gather_rows(int32_t* s_idx, const Params& p, int row0, int rows_in_grp,
+                                                  int first_local_row) {
+  const int lane = (int)lane_id();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = lane * 4 + j, rl = first_local_row + r;
+    s_idx[r] = rl < rows_in_grp ? __ldg(&p.gather_idx[row0 + rl]) : 0;
+  }
+  __syncwarp();
+}
+// Called by all 32 lanes of the producer warp: lane 0 issues the plain 128-row box; for gathers
+// every lane issues one tile::gather4 (rows 4·lane .. 4·lane+3), i.e. one warp-wide instruction.
+__device__ __forceinline__ void load_a_pair(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int kb, int arow,
+                                            bool gather, const int32_t* s_idx) {
+  const int lane = (int)lane_id();
+  if (!gather) {
+    if (lane == 0) tma_load_2d_pair(dst, map, bar, kb * kBK, arow);
+    return;
+  }
+  const int4 r = *reinterpret_cast<const int4*>(s_idx + 4 * lane);
+  tma_gather4_pair(dst + lane * 512, map, bar, kb * kBK, r.x, r.y, r.z, r.w);
+}
+
+// ---------------------------------------------------------------------------
 // In-register weight dequantization (reading R1b): exact codes, one rounding.
 // ---------------------------------------------------------------------------
 // 8 INT4 codes (one 32-bit word, even k in the low nibble) -> 8 bf16 in k order.
@@ -253,6 +284,7 @@ inline Params make_params(const GemmArgs& g) {
   p.topk_w = g.topk_w;
   p.inv_pos = g.inv_pos;
   p.k = g.k;
+  p.gather_idx = g.gather_idx;
   return p;
 }
 

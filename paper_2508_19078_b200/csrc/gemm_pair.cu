@@ -25,7 +25,7 @@ constexpr int kABytes = kHalfM * kBK * 2;     // 16 KB: this CTA's A rows
 constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 256;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64 + 128 * 4 + 16;
 
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -42,6 +42,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   int32_t* s_sched = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 256);
   int32_t* s_row0 = s_sched + kMaxGroups;
   int32_t* s_rows = s_row0 + kMaxGroups;
+  int32_t* s_idx =  // [128] gathered token ids, 16-byte aligned
+      reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(s_rows + kMaxGroups) + 15) & ~uintptr_t(15));
 
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();
@@ -72,30 +74,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int cid = (int)cluster_id_x(), ncl = (int)ncluster_x();
 
   if (warp == 0) {
-    if (elect_one()) {
+    // whole warp: it stages gathered row ids; lane 0 issues the TMA
+    if (lane_id() == 0) {
       tma_prefetch(&tm_a_r);
       tma_prefetch(&tm_b_r);
       tma_prefetch(&tm_a_s);
       tma_prefetch(&tm_b_s);
-      uint32_t it = 0;
-      for (int tile = cid; tile < total; tile += ncl) {
-        const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
-        const bool routed = ti.g < p.E;
-        const int arow = s_row0[ti.g] + ti.m * kPairM + (int)rank * kHalfM;
-        const int brow = (routed ? ti.g * p.b_rows_r : 0) + ti.n * kBN + (int)rank * (kBN / 2);
-        const CUtensorMap* ta = routed ? &tm_a_r : &tm_a_s;
-        const CUtensorMap* tb = routed ? &tm_b_r : &tm_b_s;
-        const int nkb = routed ? nkb_r : nkb_s;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * kStageBytes;
-          if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
-          tma_load_2d_pair(st, ta, &full[s], kb * kBK, arow);
-          tma_load_2d_pair(st + kABytes, tb, &full[s], kb * kBK, brow);
-        }
+    }
+    uint32_t it = 0;
+    for (int tile = cid; tile < total; tile += ncl) {
+      const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+      const bool routed = ti.g < p.E;
+      const bool gather = routed && p.gather_idx != nullptr;
+      const int first = ti.m * kPairM + (int)rank * kHalfM;
+      const int arow = s_row0[ti.g] + first;
+      const int brow = (routed ? ti.g * p.b_rows_r : 0) + ti.n * kBN + (int)rank * (kBN / 2);
+      const CUtensorMap* ta = routed ? &tm_a_r : &tm_a_s;
+      const CUtensorMap* tb = routed ? &tm_b_r : &tm_b_s;
+      const int nkb = routed ? nkb_r : nkb_s;
+      if (gather) stage_gather_rows(s_idx, p, s_row0[ti.g], s_rows[ti.g], first);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = (it + kb) % kStages;
+        const uint32_t ph = ((it + kb) / kStages) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * kStageBytes;
+        if (leader && lane_id() == 0) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+        __syncwarp();  // the transaction count is armed before any of this warp's copies can land
+        load_a_pair(st, ta, &full[s], kb, arow, gather, s_idx);
+        if (lane_id() == 0) tma_load_2d_pair(st + kABytes, tb, &full[s], kb * kBK, brow);
       }
+      it += nkb;
+      __syncwarp();  // s_idx is rewritten for the next tile only after this one was issued
     }
   } else if (warp == 1) {
     if (leader) {

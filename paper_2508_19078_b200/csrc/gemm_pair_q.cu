@@ -38,7 +38,7 @@ struct Cfg {
   static constexpr int kStages = 5;
   static constexpr int kRawStages = WB == 4 ? 10 : 5;   // raw-code ring (consumed by the dequant warps)
   static constexpr int kSmemBytes =
-      kStages * kStageBytes + kRawStages * kRawBytes + 1024 + 512 + 3 * kMaxGroups * 4 + 64;
+      kStages * kStageBytes + kRawStages * kRawBytes + 1024 + 512 + 3 * kMaxGroups * 4 + 64 + 128 * 4 + 16;
 };
 constexpr int kScalePrefetch = 4;  // K slices of group scales kept in flight per dequant thread
 
@@ -76,6 +76,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   int32_t* s_sched = reinterpret_cast<int32_t*>(raw_ring + kRawStages * kRawTx + 512);
   int32_t* s_row0 = s_sched + kMaxGroups;
   int32_t* s_rows = s_row0 + kMaxGroups;
+  int32_t* s_idx =  // [128] gathered token ids, 16-byte aligned
+      reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(s_rows + kMaxGroups) + 15) & ~uintptr_t(15));
 
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();
@@ -118,24 +120,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ A producer (ring freed by the MMA)
-    if (elect_one()) {
+    if (lane_id() == 0) {
       tma_prefetch(&tm_a_r);
       tma_prefetch(&tm_a_s);
-      uint32_t it = 0;
-      for (int tile = cid; tile < total; tile += ncl) {
-        const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
-        const bool routed = ti.g < p.E;
-        const int arow = s_row0[ti.g] + ti.m * kPairM + (int)rank * kHalfM;
-        const CUtensorMap* ta = routed ? &tm_a_r : &tm_a_s;
-        const int nkb = routed ? nkb_r : nkb_s;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[s], 2 * kABytes);
-          tma_load_2d_pair(smem + s * kStageBytes, ta, &full[s], kb * kBK, arow);
-        }
+    }
+    uint32_t it = 0;
+    for (int tile = cid; tile < total; tile += ncl) {
+      const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+      const bool routed = ti.g < p.E;
+      const bool gather = routed && p.gather_idx != nullptr;
+      const int first = ti.m * kPairM + (int)rank * kHalfM;
+      const int arow = s_row0[ti.g] + first;
+      const CUtensorMap* ta = routed ? &tm_a_r : &tm_a_s;
+      const int nkb = routed ? nkb_r : nkb_s;
+      if (gather) stage_gather_rows(s_idx, p, s_row0[ti.g], s_rows[ti.g], first);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = (it + kb) % kStages;
+        const uint32_t ph = ((it + kb) / kStages) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        if (leader && lane_id() == 0) mbar_arrive_expect_tx(&full[s], 2 * kABytes);
+        __syncwarp();
+        load_a_pair(smem + s * kStageBytes, ta, &full[s], kb, arow, gather, s_idx);
       }
+      it += nkb;
+      __syncwarp();
     }
   } else if (warp == 3) {
     // ------------------------------------------------------------ raw-code producer (ring freed by dequant)

@@ -118,6 +118,9 @@ struct GemmArgs {
   const float* topk_w;      // [T][k]
   const int32_t* inv_pos;   // [T][k]
   int k;
+  // routed A rows gathered from x (tm_a_r = gather map over x, box {64,1}) by token_index; null =
+  // rows read contiguously from a materialised x_perm / act
+  const int32_t* gather_idx;
 };
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);

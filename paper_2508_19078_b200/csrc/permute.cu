@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
     inv_pos[t * k + lane] = p;
     token_index[p] = (int32_t)t;
   }
+  if (!x_perm) return;  // the GEMM gathers A rows from x itself (TMA tile::gather4)
   const int nvec = H / 8;  // 16-byte vectors per row
   const uint4* src = x + t * nvec;
   for (int c = lane; c < nvec; c += 32) {
