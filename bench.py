@@ -145,8 +145,8 @@ def main():
     ap.add_argument("--config", default="deepseek_moe")
     ap.add_argument("--tokens", type=int, default=0, help="tokens per GPU (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-tokens", type=int, default=16)
-    ap.add_argument("--ref-layers", type=int, default=1)
+    ap.add_argument("--ref-tokens", type=int, default=32)  # oracle sample: ~10 s of host CPU work
+    ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--clusters", type=int, default=0)
     args = ap.parse_args()
 
@@ -166,7 +166,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2508_19078_b200 as F
     from paper_2508_19078_b200 import synthetic
-    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel, budgets, merge_model
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel, budgets, merge_model, shard
 
     T = args.tokens or cfg.tokens
     T_total = T * world
@@ -179,7 +179,8 @@ def main():
     masters = synthetic.master_weights(cfg)
     qm = QuantizedModel(shape)
     prof = Profiler(shape, T, with_de=True)
-    x = synthetic.tokens(cfg, rank * T, T)
+    t0, _ = shard(rank, world, T)  # this rank's contiguous slice of the global token stream
+    x = synthetic.tokens(cfg, t0, T)
     cluster_of = torch.from_numpy(synth.cluster_assignment(cfg, C)).cuda()
     alpha = torch.empty(L, E, dtype=torch.float32, device="cuda")
     alpha_host = torch.empty(L, E, dtype=torch.float32).pin_memory()

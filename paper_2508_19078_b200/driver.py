@@ -146,6 +146,15 @@ class Profiler:
         return cur
 
 
+def shard(rank: int, world: int, tokens_per_rank: int) -> tuple[int, int]:
+    """Data-parallel split of the global token stream: rank r profiles the contiguous
+    tokens [r·T, (r+1)·T); tokens are independent and the statistics additive, so the all-reduced
+    histogram equals one GPU profiling the union."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return rank * tokens_per_rank, tokens_per_rank
+
+
 def frequencies(hist_host: np.ndarray, T_total: int) -> np.ndarray:
     """Activation frequency f = activated tokens / total tokens, fp64 on the host."""
     return hist_host.astype(np.float64) / float(T_total)
