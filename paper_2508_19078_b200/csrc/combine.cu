@@ -38,28 +38,46 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
       wt[j] = __ldg(&w[t * k + j]);
     }
   }
-  for (int c = lane; c < nvec; c += 32) {
-    float acc[8], f[8];
-    unpack8(__ldg(&residual[t * nvec + c]), acc);
-    if (y_sh) {
-      unpack8(__ldg(&y_sh[t * nvec + c]), f);
+  // two 16-byte chunks per lane per iteration: all (k + 2) x 2 loads are issued before any is used
+  for (int c0 = lane; c0 < nvec; c0 += 64) {
+    uint4 rv[2], sv[2], ov[8][2];
+    bool has[2];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] += f[i];
+    for (int u = 0; u < 2; ++u) {
+      const int c = c0 + 32 * u;
+      has[u] = c < nvec;
+      if (!has[u]) continue;
+      rv[u] = __ldg(&residual[t * nvec + c]);
+      if (y_sh) sv[u] = __ldg(&y_sh[t * nvec + c]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) ov[j][u] = __ldcs(&y_perm[(int64_t)pos[j] * nvec + c]);  // read once: streaming
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j < k) {
-        unpack8(__ldg(&y_perm[(int64_t)pos[j] * nvec + c]), f);
+    for (int u = 0; u < 2; ++u) {
+      if (!has[u]) continue;
+      float acc[8], f[8];
+      unpack8(rv[u], acc);
+      if (y_sh) {
+        unpack8(sv[u], f);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt[j], f[i], acc[i]);
+        for (int i = 0; i < 8; ++i) acc[i] += f[i];
       }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < k) {
+          unpack8(ov[j][u], f);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt[j], f[i], acc[i]);
+        }
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      y[t * nvec + c0 + 32 * u] = o;
     }
-    uint4 o;
-    o.x = pack_bf16x2(acc[0], acc[1]);
-    o.y = pack_bf16x2(acc[2], acc[3]);
-    o.z = pack_bf16x2(acc[4], acc[5]);
-    o.w = pack_bf16x2(acc[6], acc[7]);
-    y[t * nvec + c] = o;
   }
 }
 }  // namespace

@@ -187,17 +187,32 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
     const int64_t srow = (int64_t)g * N + src_row;
     const float* srow_s = s + (per_channel ? 0 : srow * (K / gsz));
     const int vec_per_grp = per_channel ? vec_per_row : gsz / 8;
-    for (int v = lane; v < vec_per_row; v += 32) {
-      const float sc = per_channel ? 0.f : __bfloat162float(__float2bfloat16_rn(__ldg(&srow_s[v / vec_per_grp])));
-      if (WBITS == 4) {
-        const uint32_t raw = __ldg(reinterpret_cast<const uint32_t*>(q + srow * (K / 2)) + v);
-        dst[v] = per_channel ? deq_int4x8<false>(raw, __floats2bfloat162_rn(0.f, 0.f))
-                             : deq_int4x8<true>(raw, __floats2bfloat162_rn(sc, sc));
-      } else {
-        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(q + srow * K) + v);
-        const uint2 a = per_channel ? deq_int8x4<false>(raw.x, 0.f) : deq_int8x4<true>(raw.x, sc);
-        const uint2 b = per_channel ? deq_int8x4<false>(raw.y, 0.f) : deq_int8x4<true>(raw.y, sc);
-        dst[v] = make_uint4(a.x, a.y, b.x, b.y);
+    // four output vectors per lane per iteration: all raw loads in flight before converting
+    for (int v0 = lane; v0 < vec_per_row; v0 += 128) {
+      uint32_t r4[4];
+      uint2 r8[4];
+      float sc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int v = v0 + 32 * u;
+        if (v >= vec_per_row) continue;
+        sc[u] = per_channel ? 0.f : __ldg(&srow_s[v / vec_per_grp]);
+        if (WBITS == 4) r4[u] = __ldg(reinterpret_cast<const uint32_t*>(q + srow * (K / 2)) + v);
+        else r8[u] = __ldg(reinterpret_cast<const uint2*>(q + srow * K) + v);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int v = v0 + 32 * u;
+        if (v >= vec_per_row) continue;
+        const float s = __bfloat162float(__float2bfloat16_rn(sc[u]));
+        if (WBITS == 4) {
+          dst[v] = per_channel ? deq_int4x8<false>(r4[u], __floats2bfloat162_rn(0.f, 0.f))
+                               : deq_int4x8<true>(r4[u], __floats2bfloat162_rn(s, s));
+        } else {
+          const uint2 a = per_channel ? deq_int8x4<false>(r8[u].x, 0.f) : deq_int8x4<true>(r8[u].x, s);
+          const uint2 b = per_channel ? deq_int8x4<false>(r8[u].y, 0.f) : deq_int8x4<true>(r8[u].y, s);
+          dst[v] = make_uint4(a.x, a.y, b.x, b.y);
+        }
       }
     }
   }

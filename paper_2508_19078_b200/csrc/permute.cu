@@ -143,11 +143,19 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
   if (!x_perm) return;  // the GEMM gathers A rows from x itself (TMA tile::gather4)
   const int nvec = H / 8;  // 16-byte vectors per row
   const uint4* src = x + t * nvec;
-  for (int c = lane; c < nvec; c += 32) {
-    const uint4 v = __ldg(&src[c]);
+  // four 16-byte vectors per lane in flight before the k copies are written
+  for (int c0 = lane; c0 < nvec; c0 += 128) {
+    uint4 v[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < k) x_perm[(int64_t)pos[j] * nvec + c] = v;
+    for (int u = 0; u < 4; ++u)
+      if (c0 + 32 * u < nvec) v[u] = __ldg(&src[c0 + 32 * u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (c0 + 32 * u >= nvec) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) x_perm[(int64_t)pos[j] * nvec + c0 + 32 * u] = v[u];
+    }
   }
 }
 }  // namespace

@@ -23,7 +23,7 @@
 namespace flux {
 
 namespace {
-constexpr int kStages = 4;
+constexpr int kStages = 4;  // (3 stages / 3 CTAs per SM measured slower: 0.38 vs 0.32 ms per layer)
 constexpr int kBM = 128, kBK = 64;
 constexpr int kThreads = 192;  // warp 0: TMA, warp 1: MMA + TMEM, warps 2..5: epilogue
 
