@@ -132,6 +132,38 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
                                int32_t* remap, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * NEXT-1: similarity-based expert clustering, §5.2.
+ * ------------------------------------------------------------------------- */
+/* Bytes of device workspace flux_expert_features needs (16-byte aligned). */
+size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam);
+/* C1, reading R12: PCA features of the experts of each layer.  Expert e is
+ * the concatenation of its parameter families (e.g. gate|up, down); family f of layer l
+ * is fam[l*n_fam + f], a bf16 device array [E][fam_numel[f]] (expert-major, contiguous;
+ * fam: HOST array of device pointers).  Per layer: raw Gram G = Σ_f X_f X_fᵀ (tensor
+ * cores, fp32 accumulation, deterministic split-K reduction), centred H G H, fp64 Jacobi
+ * eigendecomposition, scores features[l][e][j] = V[e][j]·sqrt(max(λ_j,0)) for the top-d
+ * eigenvalues (descending).  Each score column is defined up to sign.
+ * Outputs (device, fp32): features [L][E][d]; gram [L][E][E] raw Gram (NULL = skip);
+ * eigvals [L][d] (NULL = skip).  2 <= E <= 64, 1 <= d <= min(E, 32), fam_numel % 8 == 0,
+ * pointers 16-byte aligned.  Asynchronous on `stream`. */
+flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_fam, const void* const* fam,
+                                 const int64_t* fam_numel, int32_t d, float* features, float* gram, float* eigvals,
+                                 void* ws, size_t ws_bytes, void* stream);
+/* C2, reading R13: fused, layer-masked cosine K-Means over all layers (one
+ * CTA per layer; masking cross-layer distances decouples the layers exactly).  Init: the
+ * n_clusters[l] non-tuning experts with the highest count (ties: lower id); assignment
+ * argmin of 1 - cos (ties: lower centroid); update: member mean (empty: unchanged);
+ * stop when no assignment changes or after max_iter iterations.  fp64 arithmetic.
+ * features: device fp32 [L][E][d]; counts: device int64 [L][E] (the profiled
+ * histograms, frequency = count / T); n_clusters: HOST int32 [L], 1 <= B(l) <= number of
+ * non-tuning experts; tuning: HOST uint8 [L][E] (non-zero = tuning expert, NULL = none).
+ * cluster_of: device int32 [L][E] (-1 for tuning experts, ready for flux_merge_experts);
+ * iterations: device int32 [L] (NULL = skip).  L <= 128, E <= 64, d <= 32. */
+flux_status flux_cluster_experts(int32_t n_layers, int32_t n_experts, int32_t d, const float* features,
+                                 const int64_t* counts, const int32_t* n_clusters, const uint8_t* tuning,
+                                 int32_t max_iter, int32_t* cluster_of, int32_t* iterations, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Statistics all-reduce over the GPUs of one box (NCCL over NVLink/NVSwitch).
  * The counts are additive integers, so the reduced histogram equals the
  * single-GPU histogram of the union of the shards bit for bit.

@@ -70,12 +70,16 @@ def _lib():
         L.flux_merge_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
         L.flux_quantize_weights.argtypes = [I32, I32, ctypes.c_int, P, I64, I64, P, P, P]
         L.flux_layer_budget.argtypes = [I32, I32, P, I64, I64, P, P, P]
+        L.flux_expert_features_workspace.argtypes = [I32, I32]
+        L.flux_expert_features_workspace.restype = SZ
+        L.flux_expert_features.argtypes = [I32, I32, I32, P, P, I32, P, P, P, P, SZ, P]
+        L.flux_cluster_experts.argtypes = [I32, I32, I32, P, P, P, P, I32, P, P, P]
         L.flux_comm_unique_id.argtypes = [P]
         L.flux_comm_init.argtypes = [ctypes.POINTER(P), P, I32, I32]
         L.flux_reduce_stats.argtypes = [P, P, SZ, P]
         L.flux_comm_destroy.argtypes = [P]
         for f in ("flux_profile_layer", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
-                  "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
+                  "flux_expert_features", "flux_cluster_experts", "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
             getattr(L, f).restype = ctypes.c_int
         L.flux_timing_enable.argtypes = [ctypes.c_int]
         L.flux_timing_enable.restype = None
@@ -176,6 +180,47 @@ def layer_budget(hist, T: int, B_non: int, n_non=None):
                                   C.ctypes.data, ctypes.byref(over))
     _check(st, "flux_layer_budget")
     return C, over.value
+
+
+def expert_features_workspace(n_layers: int, n_fam: int) -> int:
+    return int(_lib().flux_expert_features_workspace(n_layers, n_fam))
+
+
+def expert_features(families, d: int, features, gram=None, eigvals=None, ws=None, stream=None):
+    """§5.2 C1 (flux_expert_features).  families: per layer, a list of bf16 CUDA tensors [E][...]
+    (contiguous; same family shapes in every layer) -> features fp32 [L][E][d] (+ raw Gram [L][E][E],
+    eigenvalues [L][d])."""
+    import numpy as np
+    L, nf = len(families), len(families[0])
+    E = families[0][0].shape[0]
+    numel = np.array([t.numel() // E for t in families[0]], np.int64)
+    ptrs = (ctypes.c_void_p * (L * nf))(*[t.data_ptr() for fam in families for t in fam])
+    for fam in families:
+        for t, n in zip(fam, numel):
+            if t.dtype != torch.bfloat16 or not t.is_contiguous() or t.numel() != E * n:
+                raise ValueError("expert_features: families must be contiguous bf16 [E][numel] of equal shapes")
+    if ws is None:
+        ws = torch.empty(expert_features_workspace(L, nf), dtype=torch.uint8, device=features.device)
+    st = _lib().flux_expert_features(L, E, nf, ptrs, numel.ctypes.data, d, _ptr(features), _ptr(gram),
+                                     _ptr(eigvals), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "flux_expert_features")
+
+
+def cluster_experts(features, counts, n_clusters, tuning=None, max_iter: int = 50, cluster_of=None,
+                    iterations=None, stream=None):
+    """§5.2 C2 (flux_cluster_experts).  features fp32 CUDA [L][E][d]; counts int64 CUDA [L][E];
+    n_clusters host ints [L]; tuning host bool [L][E] or None -> cluster_of int32 CUDA [L][E]."""
+    import numpy as np
+    L, E, d = features.shape
+    B = np.ascontiguousarray(n_clusters, dtype=np.int32)
+    tu = None if tuning is None else np.ascontiguousarray(tuning, dtype=np.uint8)
+    if cluster_of is None:
+        cluster_of = torch.empty((L, E), dtype=torch.int32, device=features.device)
+    st = _lib().flux_cluster_experts(L, E, d, _ptr(features), _ptr(counts), B.ctypes.data,
+                                     None if tu is None else tu.ctypes.data, max_iter, _ptr(cluster_of),
+                                     _ptr(iterations), _stream(stream))
+    _check(st, "flux_cluster_experts")
+    return cluster_of
 
 
 class Comm:

@@ -498,4 +498,82 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
                                   remap, (cudaStream_t)stream));
 }
 
+/* ---------------------------------------------------------------- NEXT-1: expert clustering (§5.2) */
+size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam) {
+  if (n_layers < 1 || n_fam < 1) return 0;
+  return features_workspace(n_layers, n_fam);
+}
+
+flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_fam, const void* const* fam,
+                                 const int64_t* fam_numel, int32_t d, float* features, float* gram,
+                                 float* eigvals, void* ws, size_t ws_bytes, void* stream) {
+  const int L = n_layers, E = n_experts;
+  if (L < 1 || n_fam < 1 || E < 2 || E > kClusterMaxE || d < 1 || d > E || d > kClusterMaxD) return FLUX_E_INVALID;
+  if (!fam || !fam_numel || !features || !ws) return FLUX_E_INVALID;
+  if (ws_bytes < features_workspace(L, n_fam) || !aligned16(ws)) return FLUX_E_INVALID;
+  for (int f = 0; f < n_fam; ++f)
+    if (fam_numel[f] < 1 || fam_numel[f] % 8) return FLUX_E_UNSUPPORTED;
+  for (int i = 0; i < L * n_fam; ++i)
+    if (!fam[i] || !aligned16(fam[i])) return FLUX_E_INVALID;
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  float* partial = reinterpret_cast<float*>(ws);
+  float* G = partial + (size_t)n_fam * kNumSMs * kClusterMaxE * kClusterMaxE;
+  for (int l = 0; l < L; ++l) {
+    int slots = 0;
+    for (int f = 0; f < n_fam; ++f) {
+      int n = 0;
+      KernelTimer kt(K_GRAM, s);
+      cudaError_t e = launch_gram(E, fam[l * n_fam + f], fam_numel[f],
+                                  partial + (size_t)slots * kClusterMaxE * kClusterMaxE, &n, s);
+      if (e != cudaSuccess) {
+        set_last_error("gram", e);
+        return FLUX_E_CUDA;
+      }
+      slots += n;
+    }
+    KernelTimer kt(K_GRAM_REDUCE, s);
+    cudaError_t e = launch_gram_reduce(E, partial, slots, G + (size_t)l * kClusterMaxE * kClusterMaxE,
+                                       gram ? gram + (size_t)l * E * E : nullptr, s);
+    if (e != cudaSuccess) {
+      set_last_error("gram_reduce", e);
+      return FLUX_E_CUDA;
+    }
+  }
+  KernelTimer kt(K_EIG, s);
+  cudaError_t e = launch_eig(L, E, d, G, features, eigvals, s);
+  if (e != cudaSuccess) set_last_error("eig", e);
+  return cuda_status(e);
+}
+
+flux_status flux_cluster_experts(int32_t n_layers, int32_t n_experts, int32_t d, const float* features,
+                                 const int64_t* counts, const int32_t* n_clusters, const uint8_t* tuning,
+                                 int32_t max_iter, int32_t* cluster_of, int32_t* iterations, void* stream) {
+  const int L = n_layers, E = n_experts;
+  if (L < 1 || L > kClusterMaxL || E < 1 || E > kClusterMaxE || d < 1 || d > kClusterMaxD || max_iter < 1)
+    return FLUX_E_INVALID;
+  if (!features || !counts || !n_clusters || !cluster_of) return FLUX_E_INVALID;
+  KMeansArgs ka;
+  for (int l = 0; l < L; ++l) {
+    uint64_t m = 0;
+    int n_non = E;
+    if (tuning)
+      for (int e = 0; e < E; ++e)
+        if (tuning[l * E + e]) {
+          m |= 1ull << e;
+          --n_non;
+        }
+    if (n_clusters[l] < 1 || n_clusters[l] > n_non) return FLUX_E_INVALID;
+    ka.n_clusters[l] = n_clusters[l];
+    ka.tuning[l] = m;
+  }
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  KernelTimer kt(K_KMEANS, (cudaStream_t)stream);
+  cudaError_t e = launch_kmeans(L, E, d, features, counts, ka, max_iter, cluster_of, iterations, (cudaStream_t)stream);
+  if (e != cudaSuccess) set_last_error("kmeans", e);
+  return cuda_status(e);
+}
+
 }  // extern "C"

@@ -22,7 +22,7 @@ inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_O
 // ---------------------------------------------------------------- per-kernel timing (timing.cpp)
 enum KernelKind {
   K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_SCHEDULE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
-  K_GEMM_DN_SH_COMBINE, FLUX_NUM_KERNELS
+  K_GEMM_DN_SH_COMBINE, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, FLUX_NUM_KERNELS
 };
 // RAII: counts one launch; when timing is enabled records CUDA events around it on `st`.
 class KernelTimer {
@@ -48,6 +48,19 @@ cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, i
 // K7 (merge.cu)
 cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
                          const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st);
+
+// NEXT-1 expert clustering (cluster.cu), §5.2
+constexpr int kClusterMaxE = 64, kClusterMaxD = 32, kClusterMaxL = 128;
+struct KMeansArgs {
+  int32_t n_clusters[kClusterMaxL];  // B(l)
+  uint64_t tuning[kClusterMaxL];     // bit e set: expert e of layer l is a tuning expert (not clustered)
+};
+size_t features_workspace(int L, int n_fam);
+cudaError_t launch_gram(int E, const void* X, int64_t P, float* partial, int* n_slots, cudaStream_t st);
+cudaError_t launch_gram_reduce(int E, const float* partial, int n_slots, float* G, float* G_user, cudaStream_t st);
+cudaError_t launch_eig(int L, int E, int d, const float* G, float* features, float* eigvals, cudaStream_t st);
+cudaError_t launch_kmeans(int L, int E, int d, const float* features, const int64_t* counts, const KMeansArgs& ka,
+                          int max_iter, int32_t* cluster_of, int32_t* iters, cudaStream_t st);
 
 // K1 (router.cu)
 struct RouterArgs {

@@ -5,6 +5,7 @@ One profiling round (paper §4.1-4.2, §5.3; Fig. 7):
   a1-a6  profile local tokens through all layers   flux_profile_layer per layer
   a7  reduce the expert histograms over the box   flux_reduce_stats
   a8-pre per-layer merge budget, eq.(1)   flux_layer_budget (optional)
+  NEXT-1 expert clustering, §5.2   flux_expert_features, flux_cluster_experts
   a8  merge the non-tuning experts, eq.(2)   flux_merge_experts
 This module owns buffers and sequencing only; all arithmetic is in libflux.
 Layer chaining (R7): x_{l+1} = y_l (the path carries no attention/norm weights).
@@ -16,8 +17,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import (FLUX_OK, Comm, LayerOut, QLayer, layer_budget, make_cfg, merge_experts, profile_layer,
-               profile_layer_workspace, quantize_weights)
+from . import (FLUX_OK, Comm, LayerOut, QLayer, cluster_experts, expert_features, layer_budget, make_cfg,
+               merge_experts, profile_layer, profile_layer_workspace, quantize_weights)
 
 
 @dataclass
@@ -187,10 +188,38 @@ def merge_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tensor,
     return out
 
 
+def feature_dim(n_experts: int) -> int:
+    """Reading R12: number of PCA components kept per layer, d = min(16, E - 1) (the paper does not fix it;
+    E - 1 is the rank of E centred vectors)."""
+    return max(1, min(16, n_experts - 1))
+
+
+def expert_features_model(m: MasterWeights, d: int | None = None, with_gram: bool = False, stream=None):
+    """NEXT-1 C1 (§5.2): PCA features [L][E][d] of every layer's experts (gate|up|down)."""
+    s = m.shape
+    L, E = s.n_layers, s.n_experts
+    d = d or feature_dim(E)
+    dev = m.gate.device
+    feats = torch.empty(L, E, d, dtype=torch.float32, device=dev)
+    gram = torch.empty(L, E, E, dtype=torch.float32, device=dev) if with_gram else None
+    eig = torch.empty(L, d, dtype=torch.float32, device=dev)
+    fams = [[m.gate[l], m.up[l], m.down[l]] for l in range(L)]
+    expert_features(fams, d, feats, gram, eig, stream=stream)
+    return feats, gram, eig
+
+
+def cluster_model(features: torch.Tensor, hist_dev: torch.Tensor, n_clusters, tuning=None, max_iter: int = 50,
+                  stream=None) -> torch.Tensor:
+    """NEXT-1 C2 (§5.2): fused layer-masked K-Means -> cluster_of int32 [L][E] on the device."""
+    L = features.shape[0]
+    B = np.full(L, n_clusters, np.int32) if np.isscalar(n_clusters) else np.asarray(n_clusters, np.int32)
+    return cluster_experts(features, hist_dev, B, tuning, max_iter, stream=stream)
+
+
 def budgets(hist_host: np.ndarray, T_total: int, B_non: int, n_non=None):
     """a8-pre: eq.(1) layer budgets from the reduced histogram (host, libflux)."""
     return layer_budget(hist_host, T_total, B_non, n_non)
 
 
 __all__ = ["ModelShape", "MasterWeights", "QuantizedModel", "Profiler", "MergedModel", "merge_model", "frequencies",
-           "budgets", "Comm", "FLUX_OK"]
+           "budgets", "feature_dim", "expert_features_model", "cluster_model", "Comm", "FLUX_OK"]

@@ -58,6 +58,16 @@ def test_host_validation_without_gpu(F):
     assert L.flux_merge_experts(0, 4, 12, None, None, None, 2, None, None, None) == F.FLUX_E_UNSUPPORTED
     assert L.flux_merge_experts(0, 4, 16, None, None, None, 5, None, None, None) == F.FLUX_E_INVALID
     assert L.flux_reduce_stats(None, None, 0, None) == F.FLUX_E_INVALID
+    # clustering: E > 64, d > E, odd family size, B(l) above the non-tuning count
+    assert L.flux_expert_features_workspace(28, 2) > 0 and L.flux_expert_features_workspace(0, 2) == 0
+    numel = (ctypes.c_int64 * 1)(12)
+    ptr = (ctypes.c_void_p * 1)(None)
+    assert L.flux_expert_features(1, 65, 1, ptr, numel, 4, None, None, None, None, 0, None) == F.FLUX_E_INVALID
+    assert L.flux_expert_features(1, 8, 1, ptr, numel, 9, None, None, None, None, 0, None) == F.FLUX_E_INVALID
+    B = (ctypes.c_int32 * 1)(4)
+    tun = (ctypes.c_uint8 * 4)(1, 0, 0, 0)
+    assert L.flux_cluster_experts(1, 4, 2, 16, 16, B, tun, 10, 16, None, None) == F.FLUX_E_INVALID
+    assert L.flux_cluster_experts(1, 4, 40, 16, 16, B, None, 10, 16, None, None) == F.FLUX_E_INVALID
 
 
 def test_budget_host_matches_oracle(F):
