@@ -7,6 +7,9 @@ One step = one participant round of the hot path (all rows):
                                              flux_profile_layer x L
   a7 all-reduce the int64 histograms         flux_reduce_stats (NCCL)
   a8-pre eq.(1) layer budgets (host)         flux_layer_budget
+  §5.2 expert clustering (NEXT-1): PCA features of every layer's experts
+        (side stream, overlapping a1-a6) + fused K-Means into 16 clusters
+                                             flux_expert_features, flux_cluster_experts
   a8 eq.(2) merge 64 -> 16 experts per layer, α = f (bf16)   flux_merge_experts
 Data parallel over tokens, weak scaling: every rank profiles its own shard of
 `tokens` tokens (the N=8 run is BASELINE.json's 2M-token DP config).
@@ -45,7 +48,7 @@ def load_peaks():
 def workload_config(cfg, tokens_per_gpu, n_gpus):
     return {
         "workload": f"{cfg.name}: INT{cfg.wbits}{'-g' + str(cfg.group_size) if cfg.group_size else ' per-channel'} "
-                    f"quantize + profile {cfg.n_layers} layers + NCCL hist all-reduce + eq.(2) merge "
+                    f"quantize + profile {cfg.n_layers} layers + NCCL hist all-reduce + PCA/K-Means clustering + eq.(2) merge "
                     f"{cfg.n_experts}->{max(1, cfg.n_experts // 4)} bf16",
         "layers": cfg.n_layers, "hidden": cfg.hidden, "experts": cfg.n_experts, "shared_ffn": cfg.shared_ffn,
         "top_k": cfg.top_k, "ffn": cfg.ffn, "wbits": cfg.wbits, "group_size": cfg.group_size,
@@ -148,6 +151,8 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=32)  # oracle sample: ~10 s of host CPU work
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--clusters", type=int, default=0)
+    ap.add_argument("--clustering", default="pca", choices=["pca", "seeded"],
+                    help="pca: §5.2 PCA + K-Means on the GPU inside the step; seeded: a fixed balanced partition")
     args = ap.parse_args()
 
     import synth
@@ -166,7 +171,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2508_19078_b200 as F
     from paper_2508_19078_b200 import synthetic
-    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel, budgets, merge_model, shard
+    from paper_2508_19078_b200.driver import (ModelShape, Profiler, QuantizedModel, budgets, cluster_model,
+                                              expert_features_model, feature_dim, merge_model, shard)
 
     T = args.tokens or cfg.tokens
     T_total = T * world
@@ -182,6 +188,9 @@ def main():
     t0, _ = shard(rank, world, T)  # this rank's contiguous slice of the global token stream
     x = synthetic.tokens(cfg, t0, T)
     cluster_of = torch.from_numpy(synth.cluster_assignment(cfg, C)).cuda()
+    side = torch.cuda.Stream()
+    ev_start, ev_feat = torch.cuda.Event(), torch.cuda.Event()
+    d_feat = feature_dim(E)
     alpha = torch.empty(L, E, dtype=torch.float32, device="cuda")
     alpha_host = torch.empty(L, E, dtype=torch.float32).pin_memory()
     hist_host = torch.empty(L, E, dtype=torch.int64).pin_memory()
@@ -195,10 +204,20 @@ def main():
     budget_out = {}
 
     def step(x_in):
-        nonlocal merged
+        nonlocal merged, cluster_of
+        if args.clustering == "pca":                                # §5.2 C1 on a side stream (reads masters only)
+            ev_start.record(stream)
+            side.wait_event(ev_start)
+            with torch.cuda.stream(side):
+                feats, _, _ = expert_features_model(masters, d_feat, stream=side)
+                ev_feat.record(side)
+            feats.record_stream(stream)
         qm.quantize_from(masters)                                   # a0
         prof.run(qm, x_in)                                          # a1-a6 (hist zeroed first)
         comm.reduce_stats(prof.hist)                                # a7
+        if args.clustering == "pca":                                # §5.2 C2: K-Means from the reduced counts
+            stream.wait_event(ev_feat)
+            cluster_of = cluster_model(feats, prof.hist, C)
         hist_host.copy_(prof.hist, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         h = hist_host.numpy()

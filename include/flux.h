@@ -134,17 +134,20 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
 /* ---------------------------------------------------------------------------
  * NEXT-1: similarity-based expert clustering, §5.2.
  * ------------------------------------------------------------------------- */
-/* Bytes of device workspace flux_expert_features needs (16-byte aligned). */
-size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam);
+/* Bytes of device workspace flux_expert_features needs (16-byte aligned); fam_numel: HOST
+ * int64 [n_fam] (per-expert element count of each family).  0 on invalid arguments. */
+size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam, const int64_t* fam_numel);
 /* C1, reading R12: PCA features of the experts of each layer.  Expert e is
  * the concatenation of its parameter families (e.g. gate|up, down); family f of layer l
  * is fam[l*n_fam + f], a bf16 device array [E][fam_numel[f]] (expert-major, contiguous;
  * fam: HOST array of device pointers).  Per layer: raw Gram G = Σ_f X_f X_fᵀ (tensor
- * cores, fp32 accumulation, deterministic split-K reduction), centred H G H, fp64 Jacobi
+ * cores, fp32 accumulation over 2048-column sub-chunks, 4096-column chunks claimed
+ * dynamically by the CTAs, chunk partials summed in fp64 in chunk order: deterministic),
+ * centred H G H, fp64 Jacobi
  * eigendecomposition, scores features[l][e][j] = V[e][j]·sqrt(max(λ_j,0)) for the top-d
  * eigenvalues (descending).  Each score column is defined up to sign.
  * Outputs (device, fp32): features [L][E][d]; gram [L][E][E] raw Gram (NULL = skip);
- * eigvals [L][d] (NULL = skip).  2 <= E <= 64, 1 <= d <= min(E, 32), fam_numel % 8 == 0,
+ * eigvals [L][d] (NULL = skip).  2 <= E <= 64, 1 <= d <= min(E, 32), 1 <= n_fam <= 4, fam_numel % 8 == 0,
  * pointers 16-byte aligned.  Asynchronous on `stream`. */
 flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_fam, const void* const* fam,
                                  const int64_t* fam_numel, int32_t d, float* features, float* gram, float* eigvals,

@@ -499,50 +499,54 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
 }
 
 /* ---------------------------------------------------------------- NEXT-1: expert clustering (§5.2) */
-size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam) {
-  if (n_layers < 1 || n_fam < 1) return 0;
-  return features_workspace(n_layers, n_fam);
+size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam, const int64_t* fam_numel) {
+  if (n_layers < 1 || n_fam < 1 || n_fam > kClusterMaxFam || !fam_numel) return 0;
+  for (int f = 0; f < n_fam; ++f)
+    if (fam_numel[f] < 1) return 0;
+  return features_workspace(n_layers, n_fam, fam_numel);
 }
 
 flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_fam, const void* const* fam,
                                  const int64_t* fam_numel, int32_t d, float* features, float* gram,
                                  float* eigvals, void* ws, size_t ws_bytes, void* stream) {
   const int L = n_layers, E = n_experts;
-  if (L < 1 || n_fam < 1 || E < 2 || E > kClusterMaxE || d < 1 || d > E || d > kClusterMaxD) return FLUX_E_INVALID;
+  if (L < 1 || n_fam < 1 || n_fam > kClusterMaxFam || E < 2 || E > kClusterMaxE || d < 1 || d > E ||
+      d > kClusterMaxD)
+    return FLUX_E_INVALID;
   if (!fam || !fam_numel || !features || !ws) return FLUX_E_INVALID;
-  if (ws_bytes < features_workspace(L, n_fam) || !aligned16(ws)) return FLUX_E_INVALID;
   for (int f = 0; f < n_fam; ++f)
     if (fam_numel[f] < 1 || fam_numel[f] % 8) return FLUX_E_UNSUPPORTED;
+  if (ws_bytes < features_workspace(L, n_fam, fam_numel) || !aligned16(ws)) return FLUX_E_INVALID;
   for (int i = 0; i < L * n_fam; ++i)
     if (!fam[i] || !aligned16(fam[i])) return FLUX_E_INVALID;
   flux_status st = check_device();
   if (st != FLUX_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
   float* partial = reinterpret_cast<float*>(ws);
-  float* G = partial + (size_t)n_fam * kNumSMs * kClusterMaxE * kClusterMaxE;
+  float* G = features_gram_slot(ws, n_fam, fam_numel, 0);
+  int* counter = features_counter(ws, L, n_fam, fam_numel);
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+  if (e != cudaSuccess) return FLUX_E_CUDA;
   for (int l = 0; l < L; ++l) {
     int slots = 0;
-    for (int f = 0; f < n_fam; ++f) {
-      int n = 0;
+    {
       KernelTimer kt(K_GRAM, s);
-      cudaError_t e = launch_gram(E, fam[l * n_fam + f], fam_numel[f],
-                                  partial + (size_t)slots * kClusterMaxE * kClusterMaxE, &n, s);
+      e = launch_gram(E, n_fam, fam + (size_t)l * n_fam, fam_numel, partial, counter, &slots, s);
       if (e != cudaSuccess) {
         set_last_error("gram", e);
         return FLUX_E_CUDA;
       }
-      slots += n;
     }
     KernelTimer kt(K_GRAM_REDUCE, s);
-    cudaError_t e = launch_gram_reduce(E, partial, slots, G + (size_t)l * kClusterMaxE * kClusterMaxE,
-                                       gram ? gram + (size_t)l * E * E : nullptr, s);
+    e = launch_gram_reduce(E, partial, slots, G + (size_t)l * kClusterMaxE * kClusterMaxE,
+                           gram ? gram + (size_t)l * E * E : nullptr, counter, s);
     if (e != cudaSuccess) {
       set_last_error("gram_reduce", e);
       return FLUX_E_CUDA;
     }
   }
   KernelTimer kt(K_EIG, s);
-  cudaError_t e = launch_eig(L, E, d, G, features, eigvals, s);
+  e = launch_eig(L, E, d, G, features, eigvals, s);
   if (e != cudaSuccess) set_last_error("eig", e);
   return cuda_status(e);
 }

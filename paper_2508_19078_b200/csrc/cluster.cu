@@ -15,6 +15,9 @@
 //     in one launch: init from the most frequent non-tuning experts, cosine
 //     assignment (ties -> lower centroid), mean update (fixed member order), stop
 //     when no assignment changes.  fp64.
+#include <stdlib.h>
+#include <string.h>
+
 #include <algorithm>
 
 #include "internal.h"
@@ -23,32 +26,80 @@
 namespace flux {
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kStages = 4, kMaxE = 64;
+constexpr int kBM = 128, kBK = 64, kMaxE = 64;
+constexpr int kMaxFam = 4;
+constexpr int kGramInflight = 128 * 1024;  // bytes of expert data in flight per SM (HBM latency x bandwidth / SM)
+constexpr int kSlices = 4;                 // 64-column slices per stage: each row streams 512 contiguous bytes
+constexpr int kSubStages = 8;              // TMEM accumulation sub-chunk (32 slices = 128 MMAs), then drained
+constexpr int kChunkSlices = 64;           // work unit claimed dynamically; one partial slot each
+constexpr int kChunkStages = kChunkSlices / kSlices;
+constexpr int kRing = 8;                   // claimed-chunk ring (producer -> MMA, epilogue)
 
-template <int NPAD>
+struct GramMaps {
+  CUtensorMap map[kMaxFam];  // family f of this layer: bf16 [E][P_f], box {64 cols, NPAD rows}
+  int64_t kb_end[kMaxFam];   // cumulative 64-column slice counts
+  int n_fam;
+};
+
+template <int NPAD, int INFL>
+struct GramCfg {
+  static constexpr int kSlice = NPAD * kBK * 2;  // NPAD expert rows x 64 columns (128 B rows)
+  static constexpr int kTile = kSlices * kSlice;
+  static constexpr int kStages = INFL / kTile < 16 ? INFL / kTile : 16;
+  // The MMA reads M=128 rows from a slice; rows >= NPAD only feed accumulator rows that are never
+  // stored, but they must be readable shared memory: pad the ring by the overhang.
+  static constexpr int kPad = (kBM - NPAD) * 128;
+  static constexpr int kBarriers = 2 * kStages + 4 + 2 * kRing;
+  static constexpr int kBytes = kStages * kTile + kPad + 1024 + kBarriers * 8 + kRing * 4 + 64;
+};
+
+// Split-K Gram of one layer.  The concatenated 64-column slices of every family form chunks of
+// kChunkSlices; CTAs claim chunks from a global counter (SMs stream HBM at different rates, so a
+// static split leaves the fast ones idle) and store each chunk's fp32 X_k X_kᵀ [E][E] to its own
+// slot partial[chunk] — the slot depends only on the chunk, so the reduction below is deterministic.
+// A and B are the same shared-memory tile.  Precision: the tensor-core fp32 accumulator loses
+// ~2^-24 (relative) per accumulating MMA, a bias that grows with the accumulation length; TMEM
+// therefore accumulates sub-chunks of 128 MMAs (two buffers: the MMAs of sub-chunk c+1 overlap the
+// drain of c) and the epilogue sums the sub-chunks of a chunk in registers.
+// The counter is reset by gram_reduce_kernel, which runs after this kernel on the same stream.
+template <int NPAD, int INFL>
 __global__ void __launch_bounds__(192, 1)
-    gram_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n_kb, int E, float* __restrict__ partial) {
-  constexpr int kTile = kBM * kBK * 2;  // 16 KB
+    gram_kernel(const __grid_constant__ GramMaps gm, int E, float* __restrict__ partial, int* __restrict__ counter) {
+  using C = GramCfg<NPAD, INFL>;
+  constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kTile);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kTile + C::kPad);
   uint64_t* empty = full + kStages;
-  uint64_t* acc_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-  constexpr uint32_t kCols = NPAD <= 32 ? 32 : (NPAD <= 64 ? 64 : 128);
+  uint64_t* acc_full = empty + kStages;    // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2]
+  uint64_t* chunk_full = acc_empty + 2;    // [kRing]
+  uint64_t* chunk_empty = chunk_full + kRing;
+  int* ring = reinterpret_cast<int*>(chunk_empty + kRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
+  constexpr uint32_t kCols = NPAD <= 16 ? 32 : (NPAD <= 32 ? 64 : 128);  // two accumulators
   const int warp = warp_id();
-  // this CTA's contiguous range of 64-column slices
-  const int64_t per = n_kb / gridDim.x, rem = n_kb % gridDim.x;
-  const int64_t bx = blockIdx.x;
-  const int64_t kb0 = bx * per + (bx < rem ? bx : rem);
-  const int nk = (int)(per + (blockIdx.x < rem ? 1 : 0));
+  const int64_t n_kb = gm.kb_end[gm.n_fam - 1];
+  const int n_chunks = (int)((n_kb + kChunkSlices - 1) / kChunkSlices);
+  auto chunk_stages = [&](int id) {
+    const int64_t left = n_kb - (int64_t)id * kChunkSlices;
+    const int sl = left < kChunkSlices ? (int)left : kChunkSlices;
+    return (sl + kSlices - 1) / kSlices;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrive per epilogue warp
+    }
+    for (int r = 0; r < kRing; ++r) {
+      mbar_init(&chunk_full[r], 1);
+      mbar_init(&chunk_empty[r], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kCols>(tmem_slot);
@@ -59,51 +110,110 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      tma_prefetch(&tmap);
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (i / kStages) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], kTile);
-        tma_load_2d(smem + s * kTile, &tmap, &full[s], (int32_t)((kb0 + i) * kBK), 0);
+      for (int i = 0; i < gm.n_fam; ++i) tma_prefetch(&gm.map[i]);
+      const uint64_t pol = policy_evict_first();
+      int gs = 0;  // stages issued by this CTA
+      for (int j = 0;; ++j) {
+        const int r = j % kRing;
+        mbar_wait(&chunk_empty[r], ((j / kRing) & 1) ^ 1);
+        int id = atomicAdd(counter, 1);
+        if (id >= n_chunks) id = -1;
+        ring[r] = id;
+        mbar_arrive(&chunk_full[r]);
+        if (id < 0) break;
+        const int64_t kb0 = (int64_t)id * kChunkSlices;
+        const int64_t kb1 = kb0 + kChunkSlices < n_kb ? kb0 + kChunkSlices : n_kb;
+        int f = 0;
+        while (kb0 >= gm.kb_end[f]) ++f;
+        for (int64_t kb = kb0; kb < kb1; kb += kSlices, ++gs) {
+          const int s = gs % kStages;
+          const uint32_t ph = (gs / kStages) & 1;
+          const int n_sl = kb1 - kb < kSlices ? (int)(kb1 - kb) : kSlices;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], n_sl * C::kSlice);
+          for (int t = 0; t < n_sl; ++t) {
+            while (kb + t >= gm.kb_end[f]) ++f;
+            const int64_t local = kb + t - (f ? gm.kb_end[f - 1] : 0);
+            tma_load_2d_hint(smem + s * C::kTile + t * C::kSlice, &gm.map[f], &full[s], (int32_t)(local * kBK), 0,
+                             pol);
+          }
+        }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = umma_idesc_bf16(kBM, NPAD);
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % kStages;
-      const uint32_t ph = (i / kStages) & 1;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint64_t desc = umma_desc_sw128(smem_u32(smem + s * kTile));
+    int gs = 0, gc = 0;  // stages consumed, sub-chunks accumulated
+    for (int j = 0;; ++j) {
+      const int r = j % kRing;
+      mbar_wait(&chunk_full[r], (j / kRing) & 1);
+      const int id = ring[r];
+      if (id < 0) break;
+      const int n_st = chunk_stages(id);
+      const int64_t kb_base = (int64_t)id * kChunkSlices;
+      for (int st = 0; st < n_st; ++st, ++gs) {
+        const int s = gs % kStages;
+        const uint32_t ph = (gs / kStages) & 1;
+        const int b = gc & 1;
+        const bool first = st % kSubStages == 0;
+        const bool last = (st + 1) % kSubStages == 0 || st == n_st - 1;
+        if (first) mbar_wait(&acc_empty[b], ((gc >> 1) & 1) ^ 1);
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const int64_t left = n_kb - kb_base - (int64_t)st * kSlices;
+          const int n_sl = left < kSlices ? (int)left : kSlices;
+          const uint32_t d = tmem + b * NPAD;
+          for (int t = 0; t < n_sl; ++t) {
+            const uint64_t desc = umma_desc_sw128(smem_u32(smem + s * C::kTile + t * C::kSlice));
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) umma_bf16(tmem, desc + 2 * k, desc + 2 * k, idesc, (i | k) != 0);
-        umma_commit(&empty[s]);
-        if (i == nk - 1) umma_commit(acc_full);
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16(d, desc + 2 * k, desc + 2 * k, idesc, !(first && t == 0 && k == 0));
+          }
+          umma_commit(&empty[s]);
+          if (last) umma_commit(&acc_full[b]);
+        }
+        __syncwarp();
+        if (last) ++gc;
       }
-      __syncwarp();
     }
   } else {
     const int q = warp & 3;
     const int row = q * 32 + lane_id();
-    float* out = partial + (int64_t)blockIdx.x * kMaxE * kMaxE;
-    if (nk == 0) {
-      if (row < E)
-        for (int c = 0; c < E; ++c) out[row * kMaxE + c] = 0.f;
-    } else {
-      mbar_wait(acc_full, 0);
-      tc_fence_after();
+    int gc = 0;
+    for (int j = 0;; ++j) {
+      const int r = j % kRing;
+      mbar_wait(&chunk_full[r], (j / kRing) & 1);
+      const int id = ring[r];
+      if (id < 0) break;
+      const int n_sub = (chunk_stages(id) + kSubStages - 1) / kSubStages;
+      float acc[NPAD];
 #pragma unroll
-      for (int c = 0; c < NPAD; c += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c, v);
-        tmem_ld_wait();
-        if (row < E)
+      for (int i = 0; i < NPAD; ++i) acc[i] = 0.f;
+      for (int sub = 0; sub < n_sub; ++sub, ++gc) {
+        const int b = gc & 1;
+        mbar_wait(&acc_full[b], (gc >> 1) & 1);
+        tc_fence_after();
+        if (q * 32 < E) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c + i < E) out[row * kMaxE + c + i] = v[i];
+          for (int col = 0; col < NPAD; col += 16) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * NPAD + col, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[col + i] += v[i];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&acc_empty[b]);
       }
+      float* out = partial + (int64_t)id * kMaxE * kMaxE;
+      if (row < E)
+#pragma unroll
+        for (int i = 0; i < NPAD; ++i)
+          if (i < E) out[row * kMaxE + i] = acc[i];
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&chunk_empty[r]);
     }
   }
   tc_fence_before();
@@ -111,14 +221,26 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<kCols>(tmem);
 }
 
-__global__ void gram_reduce_kernel(const float* __restrict__ partial, int n_partial, int E, float* __restrict__ G,
-                                   float* __restrict__ G_user) {
-  const int i = blockIdx.x, j = threadIdx.x;
-  if (j >= E) return;
-  double acc = 0.0;  // fixed order over partials: deterministic
-  for (int p = 0; p < n_partial; ++p) acc += partial[(int64_t)p * kMaxE * kMaxE + i * kMaxE + j];
-  G[i * kMaxE + j] = (float)acc;
-  if (G_user) G_user[i * E + j] = (float)acc;
+// G[i][j] = Σ_p partial[p][i][j]: 16 groups of partials per (i, j), each summed in ascending p,
+// then the 16 group sums in ascending order (fixed order: deterministic).  One CTA per row i.
+__global__ void __launch_bounds__(1024) gram_reduce_kernel(const float* __restrict__ partial, int n_partial, int E,
+                                                           float* __restrict__ G, float* __restrict__ G_user,
+                                                           int* __restrict__ counter) {
+  __shared__ double part[16][kMaxE];
+  const int i = blockIdx.x, j = threadIdx.x & (kMaxE - 1), g = threadIdx.x / kMaxE;
+  if (i == 0 && threadIdx.x == 0) *counter = 0;  // the Gram kernel that claimed from it has completed
+  double acc = 0.0;
+  if (j < E)
+    for (int p = g; p < n_partial; p += 16) acc += partial[(int64_t)p * kMaxE * kMaxE + i * kMaxE + j];
+  part[g][j] = acc;
+  __syncthreads();
+  if (g == 0 && j < E) {
+    double t = 0.0;
+#pragma unroll
+    for (int h = 0; h < 16; ++h) t += part[h][j];
+    G[i * kMaxE + j] = (float)t;
+    if (G_user) G_user[i * E + j] = (float)t;
+  }
 }
 
 // One CTA (256 threads).  A = H G H in fp64 shared memory; parallel cyclic Jacobi.
@@ -331,38 +453,62 @@ __global__ void __launch_bounds__(kMaxE) kmeans_kernel(int E, int d, const float
 }
 }  // namespace
 
-size_t features_workspace(int L, int n_fam) {
-  return ((size_t)n_fam * kNumSMs + (size_t)L) * kMaxE * kMaxE * sizeof(float);
+static int64_t gram_chunks(int n_fam, const int64_t* P) {
+  int64_t kb = 0;
+  for (int f = 0; f < n_fam; ++f) kb += (P[f] + kBK - 1) / kBK;
+  return (kb + kChunkSlices - 1) / kChunkSlices;
 }
 
-// Split-K Gram of one (layer, family) matrix X [E][P] into `partial` slots; returns the slot count.
-cudaError_t launch_gram(int E, const void* X, int64_t P, float* partial, int* n_slots, cudaStream_t st) {
-  CUtensorMap m;
-  if (!make_tmap_2d(&m, X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)E, (uint64_t)P, (uint64_t)P * 2, 64, kBM,
-                    CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  const int64_t n_kb = (P + kBK - 1) / kBK;
-  const int grid = (int)std::min<int64_t>(kNumSMs, std::max<int64_t>(n_kb, 1));
-  const int smem = kStages * kBM * kBK * 2 + 1024 + 256;
-  const int npad = E <= 16 ? 16 : E <= 32 ? 32 : 64;
-  cudaError_t e;
-  if (npad == 16) {
-    e = cudaFuncSetAttribute(gram_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) gram_kernel<16><<<grid, 192, smem, st>>>(m, n_kb, E, partial);
-  } else if (npad == 32) {
-    e = cudaFuncSetAttribute(gram_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) gram_kernel<32><<<grid, 192, smem, st>>>(m, n_kb, E, partial);
-  } else {
-    e = cudaFuncSetAttribute(gram_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) gram_kernel<64><<<grid, 192, smem, st>>>(m, n_kb, E, partial);
-  }
+// [partial slots: n_chunks][kMaxE][kMaxE] fp32 | G [L][kMaxE][kMaxE] fp32 | counter
+size_t features_workspace(int L, int n_fam, const int64_t* P) {
+  return ((size_t)gram_chunks(n_fam, P) + (size_t)L) * kMaxE * kMaxE * sizeof(float) + 256;
+}
+float* features_gram_slot(void* ws, int n_fam, const int64_t* P, int l) {
+  return reinterpret_cast<float*>(ws) + ((size_t)gram_chunks(n_fam, P) + (size_t)l) * kMaxE * kMaxE;
+}
+int* features_counter(void* ws, int L, int n_fam, const int64_t* P) {
+  return reinterpret_cast<int*>(features_gram_slot(ws, n_fam, P, L));
+}
+
+template <int NPAD>
+static cudaError_t launch_gram_n(const GramMaps& gm, int E, float* partial, int* counter, int grid, cudaStream_t st) {
+  const int smem = GramCfg<NPAD, kGramInflight>::kBytes;
+  cudaError_t e =
+      cudaFuncSetAttribute(gram_kernel<NPAD, kGramInflight>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  *n_slots = grid;
+  gram_kernel<NPAD, kGramInflight><<<grid, 192, smem, st>>>(gm, E, partial, counter);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram_reduce(int E, const float* partial, int n_slots, float* G, float* G_user, cudaStream_t st) {
-  gram_reduce_kernel<<<E, kMaxE, 0, st>>>(partial, n_slots, E, G, G_user);
+// Gram partials of one layer (families X_f [E][P_f]); *n_slots = number of partial slots written.
+cudaError_t launch_gram(int E, int n_fam, const void* const* X, const int64_t* P, float* partial, int* counter,
+                        int* n_slots, cudaStream_t st) {
+  if (n_fam < 1 || n_fam > kMaxFam) return cudaErrorInvalidValue;
+  const int npad = E <= 16 ? 16 : E <= 32 ? 32 : 64;
+  GramMaps gm;
+  memset(&gm, 0, sizeof(gm));
+  gm.n_fam = n_fam;
+  int64_t acc = 0;
+  for (int f = 0; f < n_fam; ++f) {
+    if (!make_tmap_2d(&gm.map[f], X[f], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)E, (uint64_t)P[f],
+                      (uint64_t)P[f] * 2, 64, (uint32_t)npad, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    acc += (P[f] + kBK - 1) / kBK;
+    gm.kb_end[f] = acc;
+  }
+  const int64_t chunks = gram_chunks(n_fam, P);
+  const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
+  *n_slots = (int)chunks;
+  switch (npad) {
+    case 16: return launch_gram_n<16>(gm, E, partial, counter, grid, st);
+    case 32: return launch_gram_n<32>(gm, E, partial, counter, grid, st);
+    default: return launch_gram_n<64>(gm, E, partial, counter, grid, st);
+  }
+}
+
+cudaError_t launch_gram_reduce(int E, const float* partial, int n_slots, float* G, float* G_user, int* counter,
+                               cudaStream_t st) {
+  gram_reduce_kernel<<<E, 1024, 0, st>>>(partial, n_slots, E, G, G_user, counter);
   return cudaGetLastError();
 }
 

@@ -55,9 +55,14 @@ struct KMeansArgs {
   int32_t n_clusters[kClusterMaxL];  // B(l)
   uint64_t tuning[kClusterMaxL];     // bit e set: expert e of layer l is a tuning expert (not clustered)
 };
-size_t features_workspace(int L, int n_fam);
-cudaError_t launch_gram(int E, const void* X, int64_t P, float* partial, int* n_slots, cudaStream_t st);
-cudaError_t launch_gram_reduce(int E, const float* partial, int n_slots, float* G, float* G_user, cudaStream_t st);
+size_t features_workspace(int L, int n_fam, const int64_t* P);
+float* features_gram_slot(void* ws, int n_fam, const int64_t* P, int l);
+int* features_counter(void* ws, int L, int n_fam, const int64_t* P);
+constexpr int kClusterMaxFam = 4;
+cudaError_t launch_gram(int E, int n_fam, const void* const* X, const int64_t* P, float* partial, int* counter,
+                        int* n_slots, cudaStream_t st);
+cudaError_t launch_gram_reduce(int E, const float* partial, int n_slots, float* G, float* G_user, int* counter,
+                               cudaStream_t st);
 cudaError_t launch_eig(int L, int E, int d, const float* G, float* features, float* eigvals, cudaStream_t st);
 cudaError_t launch_kmeans(int L, int E, int d, const float* features, const int64_t* counts, const KMeansArgs& ka,
                           int max_iter, int32_t* cluster_of, int32_t* iters, cudaStream_t st);

@@ -59,8 +59,8 @@ def test_host_validation_without_gpu(F):
     assert L.flux_merge_experts(0, 4, 16, None, None, None, 5, None, None, None) == F.FLUX_E_INVALID
     assert L.flux_reduce_stats(None, None, 0, None) == F.FLUX_E_INVALID
     # clustering: E > 64, d > E, odd family size, B(l) above the non-tuning count
-    assert L.flux_expert_features_workspace(28, 2) > 0 and L.flux_expert_features_workspace(0, 2) == 0
     numel = (ctypes.c_int64 * 1)(12)
+    assert L.flux_expert_features_workspace(28, 1, numel) > 0 and L.flux_expert_features_workspace(0, 1, numel) == 0
     ptr = (ctypes.c_void_p * 1)(None)
     assert L.flux_expert_features(1, 65, 1, ptr, numel, 4, None, None, None, None, 0, None) == F.FLUX_E_INVALID
     assert L.flux_expert_features(1, 8, 1, ptr, numel, 9, None, None, None, None, 0, None) == F.FLUX_E_INVALID

@@ -1,6 +1,6 @@
 """Micro-benchmarks of single libflux entry points at BASELINE sizes (diagnostics, not bench lines).
 
-usage: python tools/micro.py [quantize] [merge] [layer]
+usage: python tools/micro.py [quantize] [merge] [features] [layer]
 Each prints achieved algorithmic GB/s (HBM-bound kernels) against MEASURED_PEAKS.json.
 """
 import json
@@ -57,6 +57,25 @@ def merge():
     ms = timed(lambda: F.merge_experts(W, cl, al, C, out))
     by = W.numel() * 2 + out.numel() * 2
     print(f"merge 64->16 bf16 one family/layer: {ms:.3f} ms  {by / ms / 1e6:.0f} GB/s  ({by / ms / 1e6 / peak():.2f})")
+
+
+def features():
+    """§5.2 C1 over all 28 DeepSeek layers (gate|up|down of 64 experts) + C2 K-Means into 16 clusters."""
+    from paper_2508_19078_b200 import synthetic
+    from paper_2508_19078_b200.driver import cluster_model, expert_features_model
+    cfg = synth.CONFIGS["deepseek_moe"]
+    m = synthetic.master_weights(cfg)
+    hist = torch.randint(0, 1000, (cfg.n_layers, cfg.n_experts), dtype=torch.int64, device="cuda")
+    F.timing_read(reset=True)
+    F.timing_enable(True)
+    ms = timed(lambda: expert_features_model(m, 16), reps=5, warm=2)
+    feats, _, _ = expert_features_model(m, 16)
+    ms_k = timed(lambda: cluster_model(feats, hist, 16), reps=5, warm=2)
+    F.timing_enable(False)
+    k = F.timing_read(reset=True)
+    by = m.gate.numel() * 2 * 3
+    print(f"features 28 layers: {ms:.2f} ms  {by / ms / 1e6:.0f} GB/s ({by / ms / 1e6 / peak():.2f} of HBM); "
+          f"kmeans {ms_k:.3f} ms;", {n: round(v[0] / max(v[1], 1), 4) for n, v in k.items() if v[1]})
 
 
 def layer():
