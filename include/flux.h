@@ -136,7 +136,7 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
  * ------------------------------------------------------------------------- */
 /* Bytes of device workspace flux_expert_features needs (16-byte aligned); fam_numel: HOST
  * int64 [n_fam] (per-expert element count of each family).  0 on invalid arguments. */
-size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam, const int64_t* fam_numel);
+size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_experts, int32_t n_fam, const int64_t* fam_numel);
 /* C1, reading R12: PCA features of the experts of each layer.  Expert e is
  * the concatenation of its parameter families (e.g. gate|up, down); family f of layer l
  * is fam[l*n_fam + f], a bf16 device array [E][fam_numel[f]] (expert-major, contiguous;
@@ -147,7 +147,7 @@ size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam, const int
  * eigendecomposition, scores features[l][e][j] = V[e][j]·sqrt(max(λ_j,0)) for the top-d
  * eigenvalues (descending).  Each score column is defined up to sign.
  * Outputs (device, fp32): features [L][E][d]; gram [L][E][E] raw Gram (NULL = skip);
- * eigvals [L][d] (NULL = skip).  2 <= E <= 64, 1 <= d <= min(E, 32), 1 <= n_fam <= 4, fam_numel % 8 == 0,
+ * eigvals [L][d] (NULL = skip).  2 <= E <= 128, 1 <= d <= min(E, 32), 1 <= n_fam <= 4, fam_numel % 8 == 0,
  * pointers 16-byte aligned.  Asynchronous on `stream`. */
 flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_fam, const void* const* fam,
                                  const int64_t* fam_numel, int32_t d, float* features, float* gram, float* eigvals,
@@ -161,7 +161,7 @@ flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_
  * histograms, frequency = count / T); n_clusters: HOST int32 [L], 1 <= B(l) <= number of
  * non-tuning experts; tuning: HOST uint8 [L][E] (non-zero = tuning expert, NULL = none).
  * cluster_of: device int32 [L][E] (-1 for tuning experts, ready for flux_merge_experts);
- * iterations: device int32 [L] (NULL = skip).  L <= 128, E <= 64, d <= 32. */
+ * iterations: device int32 [L] (NULL = skip).  L <= 128, E <= 128, d <= 32. */
 flux_status flux_cluster_experts(int32_t n_layers, int32_t n_experts, int32_t d, const float* features,
                                  const int64_t* counts, const int32_t* n_clusters, const uint8_t* tuning,
                                  int32_t max_iter, int32_t* cluster_of, int32_t* iterations, void* stream);

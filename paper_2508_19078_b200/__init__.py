@@ -70,7 +70,7 @@ def _lib():
         L.flux_merge_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
         L.flux_quantize_weights.argtypes = [I32, I32, ctypes.c_int, P, I64, I64, P, P, P]
         L.flux_layer_budget.argtypes = [I32, I32, P, I64, I64, P, P, P]
-        L.flux_expert_features_workspace.argtypes = [I32, I32, P]
+        L.flux_expert_features_workspace.argtypes = [I32, I32, I32, P]
         L.flux_expert_features_workspace.restype = SZ
         L.flux_expert_features.argtypes = [I32, I32, I32, P, P, I32, P, P, P, P, SZ, P]
         L.flux_cluster_experts.argtypes = [I32, I32, I32, P, P, P, P, I32, P, P, P]
@@ -182,10 +182,10 @@ def layer_budget(hist, T: int, B_non: int, n_non=None):
     return C, over.value
 
 
-def expert_features_workspace(n_layers: int, fam_numel) -> int:
+def expert_features_workspace(n_layers: int, n_experts: int, fam_numel) -> int:
     import numpy as np
     n = np.ascontiguousarray(fam_numel, dtype=np.int64)
-    return int(_lib().flux_expert_features_workspace(n_layers, len(n), n.ctypes.data))
+    return int(_lib().flux_expert_features_workspace(n_layers, n_experts, len(n), n.ctypes.data))
 
 
 def expert_features(families, d: int, features, gram=None, eigvals=None, ws=None, stream=None):
@@ -202,7 +202,7 @@ def expert_features(families, d: int, features, gram=None, eigvals=None, ws=None
             if t.dtype != torch.bfloat16 or not t.is_contiguous() or t.numel() != E * n:
                 raise ValueError("expert_features: families must be contiguous bf16 [E][numel] of equal shapes")
     if ws is None:
-        ws = torch.empty(expert_features_workspace(L, numel), dtype=torch.uint8, device=features.device)
+        ws = torch.empty(expert_features_workspace(L, E, numel), dtype=torch.uint8, device=features.device)
     st = _lib().flux_expert_features(L, E, nf, ptrs, numel.ctypes.data, d, _ptr(features), _ptr(gram),
                                      _ptr(eigvals), _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "flux_expert_features")

@@ -499,11 +499,12 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
 }
 
 /* ---------------------------------------------------------------- NEXT-1: expert clustering (§5.2) */
-size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_fam, const int64_t* fam_numel) {
-  if (n_layers < 1 || n_fam < 1 || n_fam > kClusterMaxFam || !fam_numel) return 0;
+size_t flux_expert_features_workspace(int32_t n_layers, int32_t n_experts, int32_t n_fam, const int64_t* fam_numel) {
+  if (n_layers < 1 || n_experts < 2 || n_experts > kClusterMaxE || n_fam < 1 || n_fam > kClusterMaxFam || !fam_numel)
+    return 0;
   for (int f = 0; f < n_fam; ++f)
     if (fam_numel[f] < 1) return 0;
-  return features_workspace(n_layers, n_fam, fam_numel);
+  return features_workspace(n_layers, n_experts, n_fam, fam_numel);
 }
 
 flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_fam, const void* const* fam,
@@ -516,15 +517,15 @@ flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_
   if (!fam || !fam_numel || !features || !ws) return FLUX_E_INVALID;
   for (int f = 0; f < n_fam; ++f)
     if (fam_numel[f] < 1 || fam_numel[f] % 8) return FLUX_E_UNSUPPORTED;
-  if (ws_bytes < features_workspace(L, n_fam, fam_numel) || !aligned16(ws)) return FLUX_E_INVALID;
+  if (ws_bytes < features_workspace(L, E, n_fam, fam_numel) || !aligned16(ws)) return FLUX_E_INVALID;
   for (int i = 0; i < L * n_fam; ++i)
     if (!fam[i] || !aligned16(fam[i])) return FLUX_E_INVALID;
   flux_status st = check_device();
   if (st != FLUX_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
   float* partial = reinterpret_cast<float*>(ws);
-  float* G = features_gram_slot(ws, n_fam, fam_numel, 0);
-  int* counter = features_counter(ws, L, n_fam, fam_numel);
+  float* G = features_gram_slot(ws, E, n_fam, fam_numel, 0);
+  int* counter = features_counter(ws, L, E, n_fam, fam_numel);
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
   if (e != cudaSuccess) return FLUX_E_CUDA;
   for (int l = 0; l < L; ++l) {
@@ -538,7 +539,7 @@ flux_status flux_expert_features(int32_t n_layers, int32_t n_experts, int32_t n_
       }
     }
     KernelTimer kt(K_GRAM_REDUCE, s);
-    e = launch_gram_reduce(E, partial, slots, G + (size_t)l * kClusterMaxE * kClusterMaxE,
+    e = launch_gram_reduce(E, partial, slots, G + (size_t)l * E * E,
                            gram ? gram + (size_t)l * E * E : nullptr, counter, s);
     if (e != cudaSuccess) {
       set_last_error("gram_reduce", e);
@@ -560,17 +561,18 @@ flux_status flux_cluster_experts(int32_t n_layers, int32_t n_experts, int32_t d,
   if (!features || !counts || !n_clusters || !cluster_of) return FLUX_E_INVALID;
   KMeansArgs ka;
   for (int l = 0; l < L; ++l) {
-    uint64_t m = 0;
+    uint64_t m[2] = {0, 0};
     int n_non = E;
     if (tuning)
       for (int e = 0; e < E; ++e)
         if (tuning[l * E + e]) {
-          m |= 1ull << e;
+          m[e >> 6] |= 1ull << (e & 63);
           --n_non;
         }
     if (n_clusters[l] < 1 || n_clusters[l] > n_non) return FLUX_E_INVALID;
     ka.n_clusters[l] = n_clusters[l];
-    ka.tuning[l] = m;
+    ka.tuning[l][0] = m[0];
+    ka.tuning[l][1] = m[1];
   }
   flux_status st = check_device();
   if (st != FLUX_OK) return st;

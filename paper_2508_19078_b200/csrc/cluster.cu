@@ -26,7 +26,7 @@
 namespace flux {
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kMaxE = 64;
+constexpr int kBM = 128, kBK = 64, kMaxE = 128;
 constexpr int kMaxFam = 4;
 constexpr int kGramInflight = 128 * 1024;  // bytes of expert data in flight per SM (HBM latency x bandwidth / SM)
 constexpr int kSlices = 4;                 // 64-column slices per stage: each row streams 512 contiguous bytes
@@ -45,7 +45,7 @@ template <int NPAD, int INFL>
 struct GramCfg {
   static constexpr int kSlice = NPAD * kBK * 2;  // NPAD expert rows x 64 columns (128 B rows)
   static constexpr int kTile = kSlices * kSlice;
-  static constexpr int kStages = INFL / kTile < 16 ? INFL / kTile : 16;
+  static constexpr int kStages = INFL / kTile < 3 ? 3 : (INFL / kTile < 16 ? INFL / kTile : 16);
   // The MMA reads M=128 rows from a slice; rows >= NPAD only feed accumulator rows that are never
   // stored, but they must be readable shared memory: pad the ring by the overhang.
   static constexpr int kPad = (kBM - NPAD) * 128;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* chunk_empty = chunk_full + kRing;
   int* ring = reinterpret_cast<int*>(chunk_empty + kRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
-  constexpr uint32_t kCols = NPAD <= 16 ? 32 : (NPAD <= 32 ? 64 : 128);  // two accumulators
+  constexpr uint32_t kCols = NPAD <= 16 ? 32 : (NPAD <= 32 ? 64 : (NPAD <= 64 ? 128 : 256));  // two accumulators
   const int warp = warp_id();
   const int64_t n_kb = gm.kb_end[gm.n_fam - 1];
   const int n_chunks = (int)((n_kb + kChunkSlices - 1) / kChunkSlices);
@@ -207,11 +207,11 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&acc_empty[b]);
       }
-      float* out = partial + (int64_t)id * kMaxE * kMaxE;
+      float* out = partial + (int64_t)id * E * E;
       if (row < E)
 #pragma unroll
         for (int i = 0; i < NPAD; ++i)
-          if (i < E) out[row * kMaxE + i] = acc[i];
+          if (i < E) out[row * E + i] = acc[i];
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&chunk_empty[r]);
     }
@@ -221,155 +221,159 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<kCols>(tmem);
 }
 
-// G[i][j] = Σ_p partial[p][i][j]: 16 groups of partials per (i, j), each summed in ascending p,
-// then the 16 group sums in ascending order (fixed order: deterministic).  One CTA per row i.
+// G[i][j] = Σ_p partial[p][i][j]: NG = 1024/EP groups of partials per (i, j), each summed in
+// ascending p, then the group sums in ascending order (fixed order: deterministic).  One CTA per row.
+template <int EP>
 __global__ void __launch_bounds__(1024) gram_reduce_kernel(const float* __restrict__ partial, int n_partial, int E,
                                                            float* __restrict__ G, float* __restrict__ G_user,
                                                            int* __restrict__ counter) {
-  __shared__ double part[16][kMaxE];
-  const int i = blockIdx.x, j = threadIdx.x & (kMaxE - 1), g = threadIdx.x / kMaxE;
+  constexpr int NG = 1024 / EP;
+  __shared__ double part[NG][EP];
+  const int i = blockIdx.x, j = threadIdx.x % EP, g = threadIdx.x / EP;
   if (i == 0 && threadIdx.x == 0) *counter = 0;  // the Gram kernel that claimed from it has completed
   double acc = 0.0;
   if (j < E)
-    for (int p = g; p < n_partial; p += 16) acc += partial[(int64_t)p * kMaxE * kMaxE + i * kMaxE + j];
+    for (int p = g; p < n_partial; p += NG) acc += partial[(int64_t)p * E * E + i * E + j];
   part[g][j] = acc;
   __syncthreads();
   if (g == 0 && j < E) {
     double t = 0.0;
 #pragma unroll
-    for (int h = 0; h < 16; ++h) t += part[h][j];
-    G[i * kMaxE + j] = (float)t;
+    for (int h = 0; h < NG; ++h) t += part[h][j];
+    G[i * E + j] = (float)t;
     if (G_user) G_user[i * E + j] = (float)t;
   }
 }
 
-// One CTA (256 threads).  A = H G H in fp64 shared memory; parallel cyclic Jacobi.
-__global__ void __launch_bounds__(256) eig_kernel(const float* __restrict__ G, int E, int d,
-                                                  float* __restrict__ features, float* __restrict__ eigvals) {
-  extern __shared__ double eig_smem[];  // A, V: [kMaxE][kMaxE + 1] fp64 each (66.5 KB, dynamic)
-  double(*A)[kMaxE + 1] = reinterpret_cast<double(*)[kMaxE + 1]>(eig_smem);
-  double(*V)[kMaxE + 1] = reinterpret_cast<double(*)[kMaxE + 1]>(eig_smem + kMaxE * (kMaxE + 1));
-  G += (size_t)blockIdx.x * kMaxE * kMaxE;
+// One CTA per layer.  A = H G H in fp64 shared memory; parallel cyclic Jacobi (round-robin
+// pairing: n/2 disjoint rotations per round applied to rows, then to columns and to V).
+// V is fp64 for E <= 64 and fp32 for E <= 128 (A fp64 + V fp64 would not fit in 227 KB).
+constexpr int kEigThreads = 512;
+template <typename VT>
+__global__ void __launch_bounds__(kEigThreads) eig_kernel(const float* __restrict__ G, int E, int d,
+                                                          float* __restrict__ features, float* __restrict__ eigvals) {
+  const int n = E + (E & 1);  // even count for the round-robin pairing (dummy index n-1 if E is odd)
+  const int ld = n + 1;
+  extern __shared__ double eig_smem[];  // A [n][ld] fp64, then V [n][ld] VT
+  double* A = eig_smem;
+  VT* V = reinterpret_cast<VT*>(eig_smem + n * ld);
+  G += (size_t)blockIdx.x * E * E;
   features += (size_t)blockIdx.x * E * d;
   if (eigvals) eigvals += (size_t)blockIdx.x * d;
   __shared__ double rc[kMaxE / 2], rs[kMaxE / 2];
   __shared__ int rp[kMaxE / 2], rq[kMaxE / 2];
-  __shared__ double red[256];
+  __shared__ double red[kEigThreads];
   __shared__ int order[kMaxE];
-  const int tid = threadIdx.x;
-  const int n = E + (E & 1);  // even count for the round-robin pairing (dummy index n-1 if E is odd)
-  // centring: A = G - r/E 1ᵀ - 1 r/Eᵀ + s/E², r_i = Σ_j G_ij, s = Σ r_i
   __shared__ double rsum[kMaxE];
   __shared__ double tot;
-  for (int i = tid; i < E; i += 256) {
+  const int tid = threadIdx.x;
+  // centring: A = G - r/E 1ᵀ - 1 r/Eᵀ + s/E², r_i = Σ_j G_ij, s = Σ r_i
+  for (int i = tid; i < E; i += kEigThreads) {
     double r = 0.0;
-    for (int j = 0; j < E; ++j) r += (double)G[i * kMaxE + j];
+    for (int j = 0; j < E; ++j) r += (double)G[i * E + j];
     rsum[i] = r;
   }
   __syncthreads();
   if (tid == 0) {
-    double s = 0.0;
-    for (int i = 0; i < E; ++i) s += rsum[i];
-    tot = s;
+    double t = 0.0;
+    for (int i = 0; i < E; ++i) t += rsum[i];
+    tot = t;
   }
   __syncthreads();
-  for (int idx = tid; idx < n * n; idx += 256) {
+  for (int idx = tid; idx < n * n; idx += kEigThreads) {
     const int i = idx / n, j = idx % n;
     double a = 0.0;
-    if (i < E && j < E) a = (double)G[i * kMaxE + j] - rsum[i] / E - rsum[j] / E + tot / ((double)E * E);
-    A[i][j] = a;
-    V[i][j] = i == j ? 1.0 : 0.0;
+    if (i < E && j < E) a = (double)G[i * E + j] - rsum[i] / E - rsum[j] / E + tot / ((double)E * E);
+    A[i * ld + j] = a;
+    V[i * ld + j] = i == j ? VT(1) : VT(0);
   }
   __syncthreads();
+  auto block_sum = [&](double v) {
+    red[tid] = v;
+    __syncthreads();
+    for (int st = kEigThreads / 2; st > 0; st >>= 1) {
+      if (tid < st) red[tid] += red[tid + st];
+      __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+  };
   for (int sweep = 0; sweep < 40; ++sweep) {
-    // convergence: off-diagonal vs total Frobenius norm
     double off = 0.0, all = 0.0;
-    for (int idx = tid; idx < n * n; idx += 256) {
+    for (int idx = tid; idx < n * n; idx += kEigThreads) {
       const int i = idx / n, j = idx % n;
-      const double a2 = A[i][j] * A[i][j];
+      const double a2 = A[i * ld + j] * A[i * ld + j];
       all += a2;
       if (i != j) off += a2;
     }
-    red[tid] = off;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-      if (tid < s) red[tid] += red[tid + s];
-      __syncthreads();
-    }
-    const double off_t = red[0];
-    __syncthreads();
-    red[tid] = all;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-      if (tid < s) red[tid] += red[tid + s];
-      __syncthreads();
-    }
-    const double all_t = red[0];
-    __syncthreads();
+    const double off_t = block_sum(off), all_t = block_sum(all);
     if (off_t <= 1e-24 * all_t || all_t == 0.0) break;  // off-diagonal norm <= 1e-12 of the total
     for (int round = 0; round < n - 1; ++round) {
-      // circle method: position 0 fixed, others rotate
-      if (tid < n / 2) {
+      if (tid < n / 2) {  // circle method: position 0 fixed, the others rotate
         auto player = [&](int pos) { return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (n - 1)); };
         int p = player(tid), q = player(n - 1 - tid);
-        if (p > q) { const int t = p; p = q; q = t; }
-        const double apq = A[p][q];
-        double c = 1.0, s = 0.0;
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        const double apq = A[p * ld + q];
+        double c = 1.0, sn = 0.0;
         if (fabs(apq) > 1e-300) {
-          const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
+          const double theta = (A[q * ld + q] - A[p * ld + p]) / (2.0 * apq);
           const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
           c = 1.0 / sqrt(t * t + 1.0);
-          s = t * c;
+          sn = t * c;
         }
         rp[tid] = p;
         rq[tid] = q;
         rc[tid] = c;
-        rs[tid] = s;
+        rs[tid] = sn;
       }
       __syncthreads();
-      // A <- Jᵀ A (rows p, q of every pair)
-      for (int idx = tid; idx < (n / 2) * n; idx += 256) {
+      for (int idx = tid; idx < (n / 2) * n; idx += kEigThreads) {  // A <- Jᵀ A
         const int r = idx / n, k = idx % n;
         const int p = rp[r], q = rq[r];
-        const double c = rc[r], s = rs[r];
-        const double ap = A[p][k], aq = A[q][k];
-        A[p][k] = c * ap - s * aq;
-        A[q][k] = s * ap + c * aq;
+        const double c = rc[r], sn = rs[r];
+        const double ap = A[p * ld + k], aq = A[q * ld + k];
+        A[p * ld + k] = c * ap - sn * aq;
+        A[q * ld + k] = sn * ap + c * aq;
       }
       __syncthreads();
-      // A <- A J (columns p, q), V <- V J
-      for (int idx = tid; idx < (n / 2) * n; idx += 256) {
+      for (int idx = tid; idx < (n / 2) * n; idx += kEigThreads) {  // A <- A J, V <- V J
         const int r = idx / n, k = idx % n;
         const int p = rp[r], q = rq[r];
-        const double c = rc[r], s = rs[r];
-        const double ap = A[k][p], aq = A[k][q];
-        A[k][p] = c * ap - s * aq;
-        A[k][q] = s * ap + c * aq;
-        const double vp = V[k][p], vq = V[k][q];
-        V[k][p] = c * vp - s * vq;
-        V[k][q] = s * vp + c * vq;
+        const double c = rc[r], sn = rs[r];
+        const double ap = A[k * ld + p], aq = A[k * ld + q];
+        A[k * ld + p] = c * ap - sn * aq;
+        A[k * ld + q] = sn * ap + c * aq;
+        const double vp = V[k * ld + p], vq = V[k * ld + q];
+        V[k * ld + p] = VT(c * vp - sn * vq);
+        V[k * ld + q] = VT(sn * vp + c * vq);
       }
       __syncthreads();
     }
   }
-  // eigenvalues descending (stable: lower index first on ties)
-  if (tid == 0) {
+  if (tid == 0) {  // eigenvalues descending (stable: lower index first on ties)
     for (int i = 0; i < E; ++i) order[i] = i;
     for (int i = 0; i < E; ++i)
       for (int j = i + 1; j < E; ++j)
-        if (A[order[j]][order[j]] > A[order[i]][order[i]]) {
-          const int t = order[i]; order[i] = order[j]; order[j] = t;
+        if (A[order[j] * ld + order[j]] > A[order[i] * ld + order[i]]) {
+          const int t = order[i];
+          order[i] = order[j];
+          order[j] = t;
         }
   }
   __syncthreads();
-  for (int idx = tid; idx < E * d; idx += 256) {
+  for (int idx = tid; idx < E * d; idx += kEigThreads) {
     const int e = idx / d, j = idx % d;
     const int col = order[j];
-    const double lam = A[col][col] > 0.0 ? A[col][col] : 0.0;
-    features[e * d + j] = (float)(V[e][col] * sqrt(lam));
+    const double lam = A[col * ld + col] > 0.0 ? A[col * ld + col] : 0.0;
+    features[e * d + j] = (float)((double)V[e * ld + col] * sqrt(lam));
   }
   if (eigvals)
-    for (int j = tid; j < d; j += 256) eigvals[j] = (float)A[order[j]][order[j]];
+    for (int j = tid; j < d; j += kEigThreads) eigvals[j] = (float)A[order[j] * ld + order[j]];
 }
 
 // One CTA per layer; thread e = expert e.  Frequencies enter as the profiled counts (f = count / T
@@ -379,23 +383,24 @@ __global__ void __launch_bounds__(kMaxE) kmeans_kernel(int E, int d, const float
                                                        const __grid_constant__ KMeansArgs ka, int max_iter,
                                                        int32_t* __restrict__ cluster_of, int32_t* __restrict__ iters) {
   constexpr int kMaxD = 32;
-  __shared__ double F[kMaxE][kMaxD];
-  __shared__ double mu[kMaxE][kMaxD];
+  extern __shared__ double km_smem[];  // F [E][d], mu [E][d]
+  double* F = km_smem;
+  double* mu = km_smem + E * d;
   __shared__ int init_rank[kMaxE];
   __shared__ int assign[kMaxE];
   const int l = blockIdx.x, e = threadIdx.x;
   const int B = ka.n_clusters[l];
-  const uint64_t tmask = ka.tuning[l];
+  auto is_tuning = [&](int x) { return (ka.tuning[l][x >> 6] >> (x & 63)) & 1; };
   const bool valid = e < E;
-  const bool tun = valid && ((tmask >> e) & 1);
+  const bool tun = valid && is_tuning(e);
   if (valid)
-    for (int j = 0; j < d; ++j) F[e][j] = (double)features[((int64_t)l * E + e) * d + j];
-  // rank among non-tuning experts by (-freq, id)
+    for (int j = 0; j < d; ++j) F[e * d + j] = (double)features[((int64_t)l * E + e) * d + j];
+  // rank among non-tuning experts by (-count, id)
   if (valid && !tun) {
     const int64_t fe = counts[l * E + e];
     int r = 0;
     for (int o = 0; o < E; ++o) {
-      if ((tmask >> o) & 1) continue;
+      if (is_tuning(o)) continue;
       const int64_t fo = counts[l * E + o];
       r += (fo > fe) || (fo == fe && o < e);
     }
@@ -405,7 +410,7 @@ __global__ void __launch_bounds__(kMaxE) kmeans_kernel(int E, int d, const float
   }
   __syncthreads();
   if (valid && !tun && init_rank[e] < B)
-    for (int j = 0; j < d; ++j) mu[init_rank[e]][j] = F[e][j];
+    for (int j = 0; j < d; ++j) mu[init_rank[e] * d + j] = F[e * d + j];
   if (valid) assign[e] = -1;
   __syncthreads();
   int it = 0;
@@ -413,14 +418,14 @@ __global__ void __launch_bounds__(kMaxE) kmeans_kernel(int E, int d, const float
     int mine = -1;
     if (valid && !tun) {
       double nf = 0.0;
-      for (int j = 0; j < d; ++j) nf += F[e][j] * F[e][j];
+      for (int j = 0; j < d; ++j) nf += F[e * d + j] * F[e * d + j];
       nf = sqrt(nf);
       double best = INFINITY;
       for (int c = 0; c < B; ++c) {
         double dot = 0.0, nm = 0.0;
         for (int j = 0; j < d; ++j) {
-          dot += F[e][j] * mu[c][j];
-          nm += mu[c][j] * mu[c][j];
+          dot += F[e * d + j] * mu[c * d + j];
+          nm += mu[c * d + j] * mu[c * d + j];
         }
         nm = sqrt(nm);
         const double dist = (nf == 0.0 || nm == 0.0) ? 1.0 : 1.0 - dot / (nf * nm);
@@ -440,10 +445,10 @@ __global__ void __launch_bounds__(kMaxE) kmeans_kernel(int E, int d, const float
       for (int o = 0; o < E; ++o)
         if (assign[o] == e) {
           ++cnt;
-          for (int j = 0; j < d; ++j) acc[j] += F[o][j];
+          for (int j = 0; j < d; ++j) acc[j] += F[o * d + j];
         }
       if (cnt)
-        for (int j = 0; j < d; ++j) mu[e][j] = acc[j] / cnt;
+        for (int j = 0; j < d; ++j) mu[e * d + j] = acc[j] / cnt;
     }
     __syncthreads();
     if (!changed) break;
@@ -459,15 +464,16 @@ static int64_t gram_chunks(int n_fam, const int64_t* P) {
   return (kb + kChunkSlices - 1) / kChunkSlices;
 }
 
-// [partial slots: n_chunks][kMaxE][kMaxE] fp32 | G [L][kMaxE][kMaxE] fp32 | counter
-size_t features_workspace(int L, int n_fam, const int64_t* P) {
-  return ((size_t)gram_chunks(n_fam, P) + (size_t)L) * kMaxE * kMaxE * sizeof(float) + 256;
+// [partial slots: n_chunks][E][E] fp32 | G [L][E][E] fp32 | counter
+size_t features_workspace(int L, int E, int n_fam, const int64_t* P) {
+  return ((size_t)gram_chunks(n_fam, P) + (size_t)L) * E * E * sizeof(float) + 256;
 }
-float* features_gram_slot(void* ws, int n_fam, const int64_t* P, int l) {
-  return reinterpret_cast<float*>(ws) + ((size_t)gram_chunks(n_fam, P) + (size_t)l) * kMaxE * kMaxE;
+float* features_gram_slot(void* ws, int E, int n_fam, const int64_t* P, int l) {
+  return reinterpret_cast<float*>(ws) + ((size_t)gram_chunks(n_fam, P) + (size_t)l) * E * E;
 }
-int* features_counter(void* ws, int L, int n_fam, const int64_t* P) {
-  return reinterpret_cast<int*>(features_gram_slot(ws, n_fam, P, L));
+int* features_counter(void* ws, int L, int E, int n_fam, const int64_t* P) {
+  const uintptr_t p = reinterpret_cast<uintptr_t>(features_gram_slot(ws, E, n_fam, P, L));
+  return reinterpret_cast<int*>((p + 15) & ~uintptr_t(15));
 }
 
 template <int NPAD>
@@ -484,7 +490,7 @@ static cudaError_t launch_gram_n(const GramMaps& gm, int E, float* partial, int*
 cudaError_t launch_gram(int E, int n_fam, const void* const* X, const int64_t* P, float* partial, int* counter,
                         int* n_slots, cudaStream_t st) {
   if (n_fam < 1 || n_fam > kMaxFam) return cudaErrorInvalidValue;
-  const int npad = E <= 16 ? 16 : E <= 32 ? 32 : 64;
+  const int npad = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
   GramMaps gm;
   memset(&gm, 0, sizeof(gm));
   gm.n_fam = n_fam;
@@ -502,27 +508,42 @@ cudaError_t launch_gram(int E, int n_fam, const void* const* X, const int64_t* P
   switch (npad) {
     case 16: return launch_gram_n<16>(gm, E, partial, counter, grid, st);
     case 32: return launch_gram_n<32>(gm, E, partial, counter, grid, st);
-    default: return launch_gram_n<64>(gm, E, partial, counter, grid, st);
+    case 64: return launch_gram_n<64>(gm, E, partial, counter, grid, st);
+    default: return launch_gram_n<128>(gm, E, partial, counter, grid, st);
   }
 }
 
 cudaError_t launch_gram_reduce(int E, const float* partial, int n_slots, float* G, float* G_user, int* counter,
                                cudaStream_t st) {
-  gram_reduce_kernel<<<E, 1024, 0, st>>>(partial, n_slots, E, G, G_user, counter);
+  if (E <= 64)
+    gram_reduce_kernel<64><<<E, 1024, 0, st>>>(partial, n_slots, E, G, G_user, counter);
+  else
+    gram_reduce_kernel<128><<<E, 1024, 0, st>>>(partial, n_slots, E, G, G_user, counter);
   return cudaGetLastError();
 }
 
 cudaError_t launch_eig(int L, int E, int d, const float* G, float* features, float* eigvals, cudaStream_t st) {
-  const int smem = 2 * kMaxE * (kMaxE + 1) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int n = E + (E & 1);
+  cudaError_t e;
+  if (E <= 64) {
+    const int smem = n * (n + 1) * (8 + 8);
+    e = cudaFuncSetAttribute(eig_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) eig_kernel<double><<<L, kEigThreads, smem, st>>>(G, E, d, features, eigvals);
+  } else {
+    const int smem = n * (n + 1) * (8 + 4) + 8;
+    e = cudaFuncSetAttribute(eig_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) eig_kernel<float><<<L, kEigThreads, smem, st>>>(G, E, d, features, eigvals);
+  }
   if (e != cudaSuccess) return e;
-  eig_kernel<<<L, 256, smem, st>>>(G, E, d, features, eigvals);
   return cudaGetLastError();
 }
 
 cudaError_t launch_kmeans(int L, int E, int d, const float* features, const int64_t* counts, const KMeansArgs& ka,
                           int max_iter, int32_t* cluster_of, int32_t* iters, cudaStream_t st) {
-  kmeans_kernel<<<L, kMaxE, 0, st>>>(E, d, features, counts, ka, max_iter, cluster_of, iters);
+  const int smem = 2 * E * d * (int)sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(kmeans_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  kmeans_kernel<<<L, kMaxE, smem, st>>>(E, d, features, counts, ka, max_iter, cluster_of, iters);
   return cudaGetLastError();
 }
 

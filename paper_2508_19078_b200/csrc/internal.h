@@ -50,14 +50,14 @@ cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, c
                          const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st);
 
 // NEXT-1 expert clustering (cluster.cu), §5.2
-constexpr int kClusterMaxE = 64, kClusterMaxD = 32, kClusterMaxL = 128;
+constexpr int kClusterMaxE = 128, kClusterMaxD = 32, kClusterMaxL = 128;
 struct KMeansArgs {
   int32_t n_clusters[kClusterMaxL];  // B(l)
-  uint64_t tuning[kClusterMaxL];     // bit e set: expert e of layer l is a tuning expert (not clustered)
+  uint64_t tuning[kClusterMaxL][2];  // bit e set: expert e of layer l is a tuning expert (not clustered)
 };
-size_t features_workspace(int L, int n_fam, const int64_t* P);
-float* features_gram_slot(void* ws, int n_fam, const int64_t* P, int l);
-int* features_counter(void* ws, int L, int n_fam, const int64_t* P);
+size_t features_workspace(int L, int E, int n_fam, const int64_t* P);
+float* features_gram_slot(void* ws, int E, int n_fam, const int64_t* P, int l);
+int* features_counter(void* ws, int L, int E, int n_fam, const int64_t* P);
 constexpr int kClusterMaxFam = 4;
 cudaError_t launch_gram(int E, int n_fam, const void* const* X, const int64_t* P, float* partial, int* counter,
                         int* n_slots, cudaStream_t st);

@@ -60,9 +60,10 @@ def test_host_validation_without_gpu(F):
     assert L.flux_reduce_stats(None, None, 0, None) == F.FLUX_E_INVALID
     # clustering: E > 64, d > E, odd family size, B(l) above the non-tuning count
     numel = (ctypes.c_int64 * 1)(12)
-    assert L.flux_expert_features_workspace(28, 1, numel) > 0 and L.flux_expert_features_workspace(0, 1, numel) == 0
+    assert L.flux_expert_features_workspace(28, 64, 1, numel) > 0
+    assert L.flux_expert_features_workspace(0, 64, 1, numel) == 0 and L.flux_expert_features_workspace(1, 129, 1, numel) == 0
     ptr = (ctypes.c_void_p * 1)(None)
-    assert L.flux_expert_features(1, 65, 1, ptr, numel, 4, None, None, None, None, 0, None) == F.FLUX_E_INVALID
+    assert L.flux_expert_features(1, 129, 1, ptr, numel, 4, None, None, None, None, 0, None) == F.FLUX_E_INVALID
     assert L.flux_expert_features(1, 8, 1, ptr, numel, 9, None, None, None, None, 0, None) == F.FLUX_E_INVALID
     B = (ctypes.c_int32 * 1)(4)
     tun = (ctypes.c_uint8 * 4)(1, 0, 0, 0)

@@ -42,7 +42,8 @@ def _score_gram(F):
 
 
 @pytest.mark.parametrize("E,sizes,d", [(16, [4096, 1000, 8], 8), (64, [20000, 7704], 16), (7, [640], 6),
-                                       (64, [64 * 148 * 3 + 72], 16)])
+                                       (64, [64 * 148 * 3 + 72], 16), (128, [12000, 3000, 800, 64], 24),
+                                       (100, [9000], 32), (33, [4096 * 40 + 8], 12)])
 def test_gram_features_vs_oracle(E, sizes, d):
     import paper_2508_19078_b200 as F
     rng = np.random.default_rng(100 + E + len(sizes))
@@ -87,11 +88,11 @@ def test_features_deterministic():
     assert np.array_equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(10))
 def test_kmeans_vs_oracle(seed):
     import paper_2508_19078_b200 as F
     rng = np.random.default_rng(seed)
-    L, E = int(rng.integers(1, 9)), int(rng.choice([5, 16, 37, 64]))
+    L, E = int(rng.integers(1, 9)), int(rng.choice([5, 16, 37, 64, 100, 128]))
     d = int(rng.integers(1, min(E, 32) + 1))
     feats = rng.standard_normal((L, E, d)).astype(np.float32)
     counts = rng.integers(0, 50, size=(L, E)).astype(np.int64)  # small range: frequency ties occur

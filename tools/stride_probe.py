@@ -11,7 +11,7 @@ for numel in (1408 * 2048, 1408 * 2048 + 64, 1408 * 2048 + 8 * 37, 1 << 21, (1 <
     ms = timed(lambda: F.merge_experts(W, cl, al, C, out), reps=20)
     by = W.numel() * 2 + out.numel() * 2
     feats = torch.empty(1, E, 16, device="cuda")
-    ws = torch.empty(F.expert_features_workspace(1, [numel]), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(F.expert_features_workspace(1, E, [numel]), dtype=torch.uint8, device="cuda")
     ms2 = timed(lambda: F.expert_features([[W]], 16, feats, ws=ws), reps=20)
     by2 = W.numel() * 2
     print(f"numel={numel} stride%64K={numel*2 % 65536}: merge {by/ms/1e6:.0f} GB/s; features(1 fam) {by2/ms2/1e6:.0f} GB/s ({ms2*1000:.0f} us)")
