@@ -61,6 +61,7 @@ def lib():
         L.orc_permute.argtypes = [_I64, _I, _I, _P, _P, _P, _P, _P]
         L.orc_moe_tokens.argtypes = [_I64, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.orc_moe_tokens.restype = _I
+        L.orc_compact_tokens.argtypes = [_I64, _I, _I, _I, _I, _I, _I, _I] + [_P] * 14
         L.orc_layer_budget.argtypes = [_I, _I, _P, _I64, _I64, _P, _P, _P, _P]
         L.orc_layer_budget.restype = _I64
         L.orc_merge.argtypes = [_I, _I64, _P, _P, _P, _I, _P, _P]
@@ -119,7 +120,7 @@ def router(x, wr, k: int, norm: int):
 
 
 def permute(ids, E: int):
-    """O3: ids [T][k] -> (hist [E] int64, offsets [E+1], token_index [T*k], inv_pos [T][k])."""
+    """O3: ids [T][k] (-1 = empty pick) -> (hist [E] int64, offsets [E+1], token_index [offsets[E]], inv_pos [T][k])."""
     ids = _c(ids, np.int32)
     T, k = ids.shape
     hist = np.zeros(E, np.int64)
@@ -127,7 +128,7 @@ def permute(ids, E: int):
     ti = np.empty(T * k, np.int64)
     inv = np.empty((T, k), np.int64)
     lib().orc_permute(T, E, k, ids.ctypes.data, hist.ctypes.data, off.ctypes.data, ti.ctypes.data, inv.ctypes.data)
-    return hist, off, ti, inv
+    return hist, off, ti[:off[E]], inv
 
 
 class _Expert(ctypes.Structure):
@@ -165,6 +166,37 @@ def moe_tokens(x, wr, experts, shared, *, k: int, group_size: int, norm: int):
                               ids.ctypes.data, w.ctypes.data, z.ctypes.data, m.ctypes.data)
     if rc:
         raise RuntimeError(f"orc_moe_tokens failed ({rc})")
+    return y, ids, w, z, m
+
+
+def compact_tokens(x, wr, remap, gate, up, down, shared=None, *, k: int, norm: int):
+    """O11 (NEXT-2): gate re-routing through remap + compact-model forward with full-precision weights.
+    gate/up [S][F][H], down [S][H][F]; shared = (gate [Fs][H], up [Fs][H], down [H][Fs]) or None.
+    Returns (y, ids (slot or -1), w, z, margin)."""
+    x = _c(x, np.float64)
+    wr = _c(wr, np.float64)
+    n, H = x.shape
+    Er = wr.shape[0]
+    g, u, d = _c(gate, np.float64), _c(up, np.float64), _c(down, np.float64)
+    S, F = g.shape[0], g.shape[1]
+    if shared is not None:
+        sg, su, sd = (_c(a, np.float64) for a in shared)
+        Fs = sg.shape[0]
+    else:
+        sg = su = sd = None
+        Fs = 0
+    rm = _c(remap, np.int32)
+    y = np.empty((n, H))
+    ids = np.empty((n, k), np.int32)
+    w = np.empty((n, k))
+    z = np.empty((n, Er))
+    m = np.empty(n)
+    p = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+    rc = lib().orc_compact_tokens(n, H, Er, k, S, F, Fs, norm, x.ctypes.data, wr.ctypes.data, rm.ctypes.data,
+                                  g.ctypes.data, u.ctypes.data, d.ctypes.data, p(sg), p(su), p(sd), y.ctypes.data,
+                                  ids.ctypes.data, w.ctypes.data, z.ctypes.data, m.ctypes.data)
+    if rc:
+        raise ValueError(f"orc_compact_tokens failed ({rc})")
     return y, ids, w, z, m
 
 

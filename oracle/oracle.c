@@ -161,12 +161,14 @@ int orc_router(int64_t T, int H, int E, int k, int norm, const double* x, const 
  *   offsets        = exclusive prefix sum of this call's counts, offsets[E] = T·k
  *   token_index[offsets[e] + r] = the r-th smallest t with e in S_t
  *   inv_pos[t][j]  = that position for e = S_tj
+ * An empty pick (id -1, O11's folded re-routing) is not counted: inv_pos = -1.
  * -------------------------------------------------------------------------- */
 void orc_permute(int64_t T, int E, int k, const int32_t* ids, int64_t* hist, int64_t* offsets, int64_t* token_index,
                  int64_t* inv_pos) {
   int64_t* cnt = (int64_t*)calloc((size_t)E, sizeof(int64_t));
   for (int64_t t = 0; t < T; ++t)
-    for (int j = 0; j < k; ++j) cnt[ids[t * k + j]]++;
+    for (int j = 0; j < k; ++j)
+      if (ids[t * k + j] >= 0) cnt[ids[t * k + j]]++;
   offsets[0] = 0;
   for (int e = 0; e < E; ++e) {
     offsets[e + 1] = offsets[e] + cnt[e];
@@ -176,6 +178,10 @@ void orc_permute(int64_t T, int E, int k, const int32_t* ids, int64_t* hist, int
   for (int64_t t = 0; t < T; ++t)
     for (int j = 0; j < k; ++j) {
       int e = ids[t * k + j];
+      if (e < 0) {
+        inv_pos[t * k + j] = -1;
+        continue;
+      }
       int64_t pos = offsets[e] + fill[e]++;
       token_index[pos] = t;
       inv_pos[t * k + j] = pos;
@@ -309,6 +315,77 @@ int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int nor
   free(o);
   free(sh);
   return ok ? 0 : 2;
+}
+
+/* ----------------------------------------------------------------------------
+ * O11 (NEXT-2). Gate re-routing after merging (§7: "remaps the
+ * original experts assigned by the gate network to new destinations if they have
+ * been merged") + the forward of the compact model, reading R14:
+ *   (z, S, w, margin) = router(x_t) over the ORIGINAL E_r experts (O2; the gate is
+ *                       unchanged, so w is normalised over the original picks)
+ *   slot_j  = remap[S_j]  (tuning experts first, then clusters: O10's remap)
+ *   a pick whose slot already appeared earlier in S_t (a higher logit) is folded
+ *   into that earlier pick: w_i += w_j; pick j becomes empty (id -1, w 0)
+ *   o_{t,j} = SwiGLU_{slot_j}(x_t) (O4) with the given full-precision weights
+ *   y_t     = bf16( x_t + sh_t + Σ_{j non-empty} w_tj · o_{t,j} )   (O6)
+ * Weights: gate/up [S][F][H], down [S][H][F] (real, bf16-valued); sh_* NULL if F_s == 0.
+ * ids/w out: the re-routed picks ([n][k], slot or -1).
+ * -------------------------------------------------------------------------- */
+int orc_compact_tokens(int64_t n, int H, int Er, int k, int S, int F, int Fs, int norm, const double* x,
+                       const double* wr, const int32_t* remap, const double* gate, const double* up,
+                       const double* down, const double* sh_gate, const double* sh_up, const double* sh_down,
+                       double* y, int32_t* ids, double* w, double* z, double* margin) {
+  if (S < 1) return 1;
+  for (int e = 0; e < Er; ++e)
+    if (remap[e] < 0 || remap[e] >= S) return 1;
+  if (orc_router(n, H, Er, k, norm, x, wr, z, ids, w, margin)) return 1;
+  for (int64_t t = 0; t < n; ++t) {  /* gate re-routing with folding of repeated slots */
+    int32_t* it = ids + t * k;
+    double* wt = w + t * k;
+    for (int j = 0; j < k; ++j) it[j] = remap[it[j]];
+    for (int j = 1; j < k; ++j)
+      for (int i = 0; i < j; ++i)
+        if (it[i] >= 0 && it[i] == it[j]) {
+          wt[i] += wt[j];
+          wt[j] = 0.0;
+          it[j] = -1;
+          break;
+        }
+  }
+  double* o = (double*)calloc((size_t)n * k * H, sizeof(double)); /* o[t][j][h] */
+  double* sh = (double*)calloc((size_t)n * H, sizeof(double));
+  if (!o || !sh) { free(o); free(sh); return 2; }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int s = 0; s < S; ++s) {
+    deq_expert d = {(double*)gate + (int64_t)s * F * H, (double*)up + (int64_t)s * F * H,
+                    (double*)down + (int64_t)s * H * F};
+    double* a = (double*)malloc(sizeof(double) * (size_t)F);
+    for (int64_t t = 0; t < n; ++t)
+      for (int j = 0; j < k; ++j)
+        if (ids[t * k + j] == s) swiglu_expert(H, F, &d, x + t * H, a, o + (t * k + j) * (int64_t)H);
+    free(a);
+  }
+  if (Fs > 0 && sh_gate) {
+    deq_expert d = {(double*)sh_gate, (double*)sh_up, (double*)sh_down};
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t t = 0; t < n; ++t) {
+      double* a = (double*)malloc(sizeof(double) * (size_t)Fs);
+      swiglu_expert(H, Fs, &d, x + t * H, a, sh + t * H);
+      free(a);
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < n; ++t)
+    for (int h = 0; h < H; ++h) {
+      double acc = x[t * H + h];
+      acc += sh[t * H + h];
+      for (int j = 0; j < k; ++j)
+        if (ids[t * k + j] >= 0) acc += w[t * k + j] * o[(t * k + j) * (int64_t)H + h];
+      y[t * H + h] = orc_bf16_round(acc);
+    }
+  free(o);
+  free(sh);
+  return 0;
 }
 
 /* ----------------------------------------------------------------------------
