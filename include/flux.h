@@ -60,18 +60,27 @@ typedef struct {
   int32_t n_experts;  /* E, routed experts                                    */
   int32_t top_k;      /* k, experts per token                                 */
   int32_t shared_ffn; /* F_s of the always-on shared experts (0 = none), R5   */
-  int32_t wbits;      /* 8 or 4 (bit level chosen per participant) */
-  int32_t group_size; /* 0 = per output channel, else g along the contraction */
+  int32_t wbits;      /* 8 or 4 (bit level chosen per participant); 16 = bf16
+                         weights, not quantized (the compact model after merging, NEXT-2) */
+  int32_t group_size; /* 0 = per output channel, else g along the contraction (0 for wbits 16) */
   int32_t norm_topk;  /* 0: w = softmax prob; 1: renormalised over top-k (R2) */
+  int32_t n_router;   /* 0: the router scores the n_experts experts.  > 0 (NEXT-2, gate
+                         re-routing after merging, §7, reading R14): the router
+                         keeps the ORIGINAL n_router experts and flux_qlayer.remap sends each
+                         pick to one of the n_experts slots of the compact model; requires
+                         n_experts <= n_router <= 128 and top_k <= n_router */
 } flux_moe_cfg;
 
 /* Quantized weights of one layer, canonical layout (device pointers):
- *   router_w  bf16 [E][H]               (not quantized, R1)
+ *   router_w  bf16 [E_r][H]             (not quantized, R1; E_r = n_router or n_experts)
  *   gate_q    [E][F][H']   up_q [E][F][H']   H' = H (int8) or H/2 bytes (int4)
  *   gate_s    fp32 [E][F][H/g]          (g = H when group_size == 0)
  *   down_q    [E][H][F']                F' = F or F/2
  *   down_s    fp32 [E][H][F/g]
  *   sh_*      same for the shared MLP with F_s instead of F (NULL if F_s == 0)
+ *   wbits 16: *_q are bf16 [E][F][H] / [E][H][F] weights and the scales are ignored (may be NULL)
+ *   remap     int32 [n_router], slot in [0, n_experts) of every original expert (flux_merge_experts'
+ *             remap); required iff cfg.n_router > 0, else ignored
  * All pointers 16-byte aligned. */
 typedef struct {
   const void* router_w;
@@ -79,12 +88,16 @@ typedef struct {
   const float *gate_s, *up_s, *down_s;
   const void *sh_gate_q, *sh_up_q, *sh_down_q;
   const float *sh_gate_s, *sh_up_s, *sh_down_s;
+  const int32_t* remap;
 } flux_qlayer;
 
 /* Per-layer outputs (device pointers, caller-owned; optional ones may be NULL):
  *   y              bf16 [T][H]   y_t = bf16(r_t + sh_t + Σ_j w_tj · o_{t,S_tj})   (R6) — required
- *   topk_ids       int32 [T][k]  S_t, descending logit, lower index on ties (R2)  — required
- *   topk_w         fp32 [T][k]   gate weights w_tj (R2)                           — required
+ *   topk_ids       int32 [T][k]  S_t, descending logit, lower index on ties (R2)  — required.
+ *                                With re-routing (n_router > 0): the slot of every pick; a pick
+ *                                whose slot repeats an earlier pick's is folded into it (its
+ *                                weight added there) and reads -1
+ *   topk_w         fp32 [T][k]   gate weights w_tj (R2), 0 for a folded pick      — required
  *   hist           int64 [E]     ACCUMULATED (+=) activation counts, P:296-298    — required;
  *                                the caller zeroes it once per profiling round
  *   expert_offsets int32 [E+1]   D_e segment bounds into token_index  — optional
@@ -130,6 +143,26 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
 flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t numel, const void* experts,
                                const int32_t* cluster_of, const float* alpha, int32_t n_clusters, void* merged,
                                int32_t* remap, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * NEXT-2: the compact model after merging (§5.3 + §7 "Customized MoE construction",
+ * "Gate re-routing") and its quality measure.
+ * ------------------------------------------------------------------------- */
+/* eq.(2) as flux_merge_experts, but the output holds every slot of the compact model in
+ * remap order: compact[remap[e]] for all e — each tuning expert copied bit for bit (a
+ * singleton with weight α/α = 1), then the C merged clusters.  compact: [n_tun + C][numel].
+ * Feed the slots to flux_profile_layer with wbits = 16, n_experts = n_tun + C,
+ * n_router = E and flux_qlayer.remap = remap (the gate keeps scoring the original experts). */
+flux_status flux_compact_experts(flux_dtype dtype, int32_t n_experts, int64_t numel, const void* experts,
+                                 const int32_t* cluster_of, const float* alpha, int32_t n_clusters, void* compact,
+                                 int32_t* remap, void* stream);
+/* The paper's merge output error: the average over T tokens of the
+ * cosine distance 1 - a_t·b_t/(|a_t||b_t|) between two bf16 [T][H] outputs (the merged and the
+ * original model's final token outputs); fp64 accumulation, fixed order (deterministic).
+ * result: device double [1]; ws: device, >= flux_output_error_workspace() bytes. */
+size_t flux_output_error_workspace(void);
+flux_status flux_output_error(int64_t T, int32_t hidden, const void* a, const void* b, double* result, void* ws,
+                              size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * NEXT-1: similarity-based expert clustering, §5.2.

@@ -37,13 +37,14 @@ class FluxError(RuntimeError):
 
 class MoECfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
-                ("hidden", "ffn", "n_experts", "top_k", "shared_ffn", "wbits", "group_size", "norm_topk")]
+                ("hidden", "ffn", "n_experts", "top_k", "shared_ffn", "wbits", "group_size", "norm_topk",
+                 "n_router")]
 
 
 class QLayer(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
                 ("router_w", "gate_q", "up_q", "down_q", "gate_s", "up_s", "down_s",
-                 "sh_gate_q", "sh_up_q", "sh_down_q", "sh_gate_s", "sh_up_s", "sh_down_s")]
+                 "sh_gate_q", "sh_up_q", "sh_down_q", "sh_gate_s", "sh_up_s", "sh_down_s", "remap")]
 
 
 class LayerOut(ctypes.Structure):
@@ -69,6 +70,10 @@ def _lib():
                                          ctypes.POINTER(LayerOut), P, SZ, P]
         L.flux_merge_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
         L.flux_quantize_weights.argtypes = [I32, I32, ctypes.c_int, P, I64, I64, P, P, P]
+        L.flux_compact_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
+        L.flux_output_error_workspace.argtypes = []
+        L.flux_output_error_workspace.restype = SZ
+        L.flux_output_error.argtypes = [I64, I32, P, P, P, P, SZ, P]
         L.flux_layer_budget.argtypes = [I32, I32, P, I64, I64, P, P, P]
         L.flux_expert_features_workspace.argtypes = [I32, I32, I32, P]
         L.flux_expert_features_workspace.restype = SZ
@@ -79,7 +84,8 @@ def _lib():
         L.flux_reduce_stats.argtypes = [P, P, SZ, P]
         L.flux_comm_destroy.argtypes = [P]
         for f in ("flux_profile_layer", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
-                  "flux_expert_features", "flux_cluster_experts", "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
+                  "flux_expert_features", "flux_cluster_experts", "flux_compact_experts", "flux_output_error",
+                  "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
             getattr(L, f).restype = ctypes.c_int
         L.flux_timing_enable.argtypes = [ctypes.c_int]
         L.flux_timing_enable.restype = None
@@ -133,8 +139,8 @@ def _stream(stream=None):
 
 
 # ------------------------------------------------------------------------------------------ API
-def make_cfg(hidden, ffn, n_experts, top_k, shared_ffn, wbits, group_size, norm_topk) -> MoECfg:
-    return MoECfg(hidden, ffn, n_experts, top_k, shared_ffn, wbits, group_size, norm_topk)
+def make_cfg(hidden, ffn, n_experts, top_k, shared_ffn, wbits, group_size, norm_topk, n_router=0) -> MoECfg:
+    return MoECfg(hidden, ffn, n_experts, top_k, shared_ffn, wbits, group_size, norm_topk, n_router)
 
 
 def profile_layer_workspace(cfg: MoECfg, T: int) -> int:
@@ -157,6 +163,28 @@ def merge_experts(experts, cluster_of, alpha, n_clusters: int, merged, remap=Non
     st = _lib().flux_merge_experts(dt, E, numel, _ptr(experts), _ptr(cluster_of), _ptr(alpha), n_clusters,
                                    _ptr(merged), _ptr(remap), _stream(stream))
     _check(st, "flux_merge_experts")
+
+
+def compact_experts(experts, cluster_of, alpha, n_clusters: int, compact, remap=None, stream=None):
+    """NEXT-2: slots of the compact model (tuning experts, then eq.(2) clusters) -> compact [S][numel]."""
+    dt = FLUX_FP32 if experts.dtype == torch.float32 else FLUX_BF16
+    E = experts.shape[0]
+    numel = experts.numel() // E
+    st = _lib().flux_compact_experts(dt, E, numel, _ptr(experts), _ptr(cluster_of), _ptr(alpha), n_clusters,
+                                     _ptr(compact), _ptr(remap), _stream(stream))
+    _check(st, "flux_compact_experts")
+
+
+def output_error(a, b, result=None, ws=None, stream=None):
+    """Mean cosine distance between two bf16 [T][H] CUDA outputs -> device double [1]."""
+    T, H = a.shape
+    if result is None:
+        result = torch.empty(1, dtype=torch.float64, device=a.device)
+    if ws is None:
+        ws = torch.empty(int(_lib().flux_output_error_workspace()), dtype=torch.uint8, device=a.device)
+    st = _lib().flux_output_error(T, H, _ptr(a), _ptr(b), _ptr(result), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "flux_output_error")
+    return result
 
 
 def quantize_weights(w, wbits: int, group_size: int, q, s, stream=None):

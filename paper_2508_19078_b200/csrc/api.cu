@@ -76,6 +76,7 @@ static bool env_on(const char* name) {
 // Policy: pass when the average routed rows per expert reach 8 tile rows (2048); overrides:
 // FLUX_GEMM_DEQUANT_PASS=1 / FLUX_GEMM_FUSED_DEQUANT=1 (FLUX_GEMM_1SM=1 implies the pass).
 static bool dequant_pass(const flux_moe_cfg& c, int64_t T) {
+  if (c.wbits == 16) return true;  // bf16 weights: the pass is a layout copy; the fused kernel is for codes
   if (env_on("FLUX_GEMM_DEQUANT_PASS") || env_on("FLUX_GEMM_1SM")) return true;
   if (env_on("FLUX_GEMM_FUSED_DEQUANT")) return false;
   return T * c.top_k >= (int64_t)2048 * c.n_experts;
@@ -158,9 +159,13 @@ flux_status validate_cfg(const flux_moe_cfg* c) {
   if (!c) return FLUX_E_INVALID;
   if (c->hidden <= 0 || c->ffn <= 0 || c->n_experts <= 0 || c->top_k <= 0 || c->shared_ffn < 0)
     return FLUX_E_INVALID;
-  if (c->wbits != 4 && c->wbits != 8) return FLUX_E_UNSUPPORTED;
+  if (c->wbits != 4 && c->wbits != 8 && c->wbits != 16) return FLUX_E_UNSUPPORTED;
+  if (c->wbits == 16 && c->group_size != 0) return FLUX_E_UNSUPPORTED;
+  if (c->n_router < 0) return FLUX_E_INVALID;
+  if (c->n_router > 0 && (c->n_router > 128 || c->n_experts > c->n_router || c->top_k > c->n_router))
+    return FLUX_E_UNSUPPORTED;
   if (c->hidden % 64 || c->ffn % 16 || c->shared_ffn % 16) return FLUX_E_UNSUPPORTED;
-  if (c->n_experts > 128 || c->top_k > 8 || c->top_k > c->n_experts) return FLUX_E_UNSUPPORTED;
+  if (c->n_experts > 128 || c->top_k > 8 || (c->n_router == 0 && c->top_k > c->n_experts)) return FLUX_E_UNSUPPORTED;
   if (c->norm_topk != 0 && c->norm_topk != 1) return FLUX_E_INVALID;
   if (c->group_size < 0) return FLUX_E_INVALID;
   if (c->group_size > 0) {
@@ -205,11 +210,14 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   if (T * cfg->top_k >= (int64_t)1 << 31) return FLUX_E_UNSUPPORTED;
   const flux_moe_cfg& c = *cfg;
   const bool sh = c.shared_ffn > 0;
+  const bool quantized = c.wbits != 16;
   if (!x || !out->y || !out->topk_ids || !out->topk_w || !out->hist || !w->router_w || !w->gate_q || !w->up_q ||
-      !w->down_q || !w->gate_s || !w->up_s || !w->down_s)
+      !w->down_q || (quantized && (!w->gate_s || !w->up_s || !w->down_s)))
     return FLUX_E_INVALID;
-  if (sh && (!w->sh_gate_q || !w->sh_up_q || !w->sh_down_q || !w->sh_gate_s || !w->sh_up_s || !w->sh_down_s))
+  if (sh && (!w->sh_gate_q || !w->sh_up_q || !w->sh_down_q ||
+             (quantized && (!w->sh_gate_s || !w->sh_up_s || !w->sh_down_s))))
     return FLUX_E_INVALID;
+  if (c.n_router > 0 && !w->remap) return FLUX_E_INVALID;
   const void* ptrs16[] = {x, residual, out->y, w->router_w, w->gate_q, w->up_q, w->down_q,
                           w->sh_gate_q, w->sh_up_q, w->sh_down_q, ws};
   for (const void* p : ptrs16)
@@ -221,7 +229,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   uint8_t* W = (uint8_t*)ws;
   const int H = c.hidden, F = c.ffn, Fs = c.shared_ffn, E = c.n_experts, k = c.top_k;
   const int Fp = pad128(F), Fsp = pad128(Fs);
-  const bool per_channel = c.group_size == 0;
+  const bool per_channel = c.group_size == 0 && quantized;  // per-channel scales applied in the epilogue
+  const int E_r = c.n_router > 0 ? c.n_router : E;           // experts the router scores
   const int g_h = per_channel ? H : c.group_size, g_f = per_channel ? F : c.group_size,
             g_fs = per_channel ? Fs : c.group_size;
   const int64_t n_rt = (T + 127) / 128;
@@ -267,10 +276,11 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   if (e != cudaSuccess) { set_last_error("dequant", e); return FLUX_E_CUDA; }
 
   // ---- (b) K1 router + top-k + histogram
-  const int npad = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
+  const int npad = E_r <= 16 ? 16 : E_r <= 32 ? 32 : E_r <= 64 ? 64 : 128;
   CUtensorMap tm_x, tm_wr;
-  if (!tmap_bf16(&tm_x, x, T, H, 128) || !tmap_bf16(&tm_wr, w->router_w, E, H, npad)) { set_last_error("router tensor map", cudaErrorInvalidValue); return FLUX_E_CUDA; }
-  RouterArgs ra{T, H, E, k, c.norm_topk, out->topk_ids, out->topk_w, out->router_logits, out->hist, tile_counts, rank};
+  if (!tmap_bf16(&tm_x, x, T, H, 128) || !tmap_bf16(&tm_wr, w->router_w, E_r, H, npad)) { set_last_error("router tensor map", cudaErrorInvalidValue); return FLUX_E_CUDA; }
+  RouterArgs ra{T, H, E_r, k, c.norm_topk, out->topk_ids, out->topk_w, out->router_logits, out->hist, tile_counts, rank,
+                E, c.n_router > 0 ? w->remap : nullptr};
   {
     KernelTimer kt(K_ROUTER, s);
     if ((e = launch_router(tm_x, tm_wr, npad, ra, s)) != cudaSuccess) { set_last_error("router", e); return FLUX_E_CUDA; }
@@ -496,6 +506,38 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
   KernelTimer kt(K_MERGE, (cudaStream_t)stream);
   return cuda_status(launch_merge(dtype == FLUX_FP32, n_experts, numel, experts, cluster_of, alpha, n_clusters, merged,
                                   remap, (cudaStream_t)stream));
+}
+
+/* ---------------------------------------------------------------- NEXT-2: compact model + output error */
+flux_status flux_compact_experts(flux_dtype dtype, int32_t n_experts, int64_t numel, const void* experts,
+                                 const int32_t* cluster_of, const float* alpha, int32_t n_clusters, void* compact,
+                                 int32_t* remap, void* stream) {
+  if (dtype != FLUX_BF16 && dtype != FLUX_FP32) return FLUX_E_INVALID;
+  if (n_experts < 1 || n_experts > 1024 || n_clusters < 0 || n_clusters > n_experts || numel < 0)
+    return FLUX_E_INVALID;
+  if (numel % 8) return FLUX_E_UNSUPPORTED;
+  if (!experts || !cluster_of || !alpha || !compact || !aligned16(experts) || !aligned16(compact))
+    return FLUX_E_INVALID;
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  KernelTimer kt(K_MERGE, (cudaStream_t)stream);
+  return cuda_status(launch_merge(dtype == FLUX_FP32, n_experts, numel, experts, cluster_of, alpha, n_clusters,
+                                  compact, remap, (cudaStream_t)stream, 1));
+}
+
+size_t flux_output_error_workspace(void) { return cosine_workspace(); }
+
+flux_status flux_output_error(int64_t T, int32_t hidden, const void* a, const void* b, double* result, void* ws,
+                              size_t ws_bytes, void* stream) {
+  if (T < 0 || hidden <= 0 || hidden % 8) return FLUX_E_INVALID;
+  if (!a || !b || !result || !ws || !aligned16(a) || !aligned16(b) || !aligned16(ws)) return FLUX_E_INVALID;
+  if (ws_bytes < cosine_workspace()) return FLUX_E_WORKSPACE;
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  KernelTimer kt(K_COSINE, (cudaStream_t)stream);
+  cudaError_t e = launch_cosine_distance(T, hidden, a, b, (double*)ws, result, (cudaStream_t)stream);
+  if (e != cudaSuccess) set_last_error("cosine_distance", e);
+  return cuda_status(e);
 }
 
 /* ---------------------------------------------------------------- NEXT-1: expert clustering (§5.2) */

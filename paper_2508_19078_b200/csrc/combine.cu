@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
       if (y_sh) sv[u] = __ldg(&y_sh[t * nvec + c]);
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < k) ov[j][u] = __ldcs(&y_perm[(int64_t)pos[j] * nvec + c]);  // read once: streaming
+        if (j < k && pos[j] >= 0) ov[j][u] = __ldcs(&y_perm[(int64_t)pos[j] * nvec + c]);  // read once: streaming
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (j < k) {
+        if (j < k && pos[j] >= 0) {  // pos -1: a pick folded by gate re-routing
           unpack8(ov[j][u], f);
 #pragma unroll
           for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt[j], f[i], acc[i]);

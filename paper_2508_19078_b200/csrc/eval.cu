@@ -1,0 +1,81 @@
+// eval.cu — the paper's merge-quality measure (NEXT-2): "the average cosine distance between the
+// final token embeddings from the MoE model with merged experts and those from the original full
+// model":  err = (1/T) Σ_t (1 - a_t·b_t / (|a_t| |b_t|)).
+//
+// HBM-bound (reads both [T][H] bf16 outputs once).  One warp per token (16-byte vectors, fp64
+// accumulation); each CTA sums its tokens' distances in token order, and the last CTA to finish
+// (atomic ticket) sums the CTA partials in CTA order: deterministic.
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace flux {
+namespace {
+
+constexpr int kCosBlocks = kNumSMs * 4, kCosThreads = 256;
+
+__global__ void __launch_bounds__(kCosThreads) cosine_distance_kernel(int64_t T, int H, const uint4* __restrict__ a,
+                                                                      const uint4* __restrict__ b,
+                                                                      double* __restrict__ partial,
+                                                                      unsigned* __restrict__ ticket,
+                                                                      double* __restrict__ out) {
+  __shared__ double warp_sum[kCosThreads / 32];
+  __shared__ bool is_last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nvec = H / 8;
+  double my = 0.0;  // this warp's tokens, in token order
+  for (int64_t t = (int64_t)blockIdx.x * (kCosThreads / 32) + wid; t < T; t += (int64_t)gridDim.x * (kCosThreads / 32)) {
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    for (int v = lane; v < nvec; v += 32) {
+      const uint4 x = __ldcs(&a[t * nvec + v]), y = __ldcs(&b[t * nvec + v]);
+      const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
+      const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 fx = __bfloat1622float2(hx[i]), fy = __bfloat1622float2(hy[i]);
+        dot += (double)fx.x * fy.x + (double)fx.y * fy.y;
+        na += (double)fx.x * fx.x + (double)fx.y * fx.y;
+        nb += (double)fy.x * fy.x + (double)fy.y * fy.y;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      na += __shfl_xor_sync(0xffffffffu, na, o);
+      nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    }
+    my += (na == 0.0 || nb == 0.0) ? 1.0 : 1.0 - dot / (sqrt(na) * sqrt(nb));
+  }
+  if (lane == 0) warp_sum[wid] = my;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kCosThreads / 32; ++w) s += warp_sum[w];
+    partial[blockIdx.x] = s;
+    __threadfence();
+    is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) s += __ldcg(&partial[i]);
+    *out = T ? s / (double)T : 0.0;
+    *ticket = 0;  // ready for the next call
+  }
+}
+}  // namespace
+
+size_t cosine_workspace() { return (kCosBlocks + 2) * sizeof(double); }
+
+cudaError_t launch_cosine_distance(int64_t T, int H, const void* a, const void* b, double* ws, double* out,
+                                   cudaStream_t st) {
+  unsigned* ticket = reinterpret_cast<unsigned*>(ws + kCosBlocks);
+  cudaError_t e = cudaMemsetAsync(ticket, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  const int64_t want = (T + kCosThreads / 32 - 1) / (kCosThreads / 32);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, kCosBlocks));
+  cosine_distance_kernel<<<grid, kCosThreads, 0, st>>>(T, H, (const uint4*)a, (const uint4*)b, ws, ticket, out);
+  return cudaGetLastError();
+}
+
+}  // namespace flux

@@ -185,6 +185,19 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
       continue;
     }
     const int64_t srow = (int64_t)g * N + src_row;
+    if constexpr (WBITS == 16) {  // bf16 weights (compact model, NEXT-2): layout copy only
+      const uint4* src = reinterpret_cast<const uint4*>(q) + srow * vec_per_row;
+      for (int v0 = lane; v0 < vec_per_row; v0 += 128) {
+        uint4 r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (v0 + 32 * u < vec_per_row) r[u] = __ldg(&src[v0 + 32 * u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (v0 + 32 * u < vec_per_row) dst[v0 + 32 * u] = r[u];
+      }
+      continue;
+    }
     const float* srow_s = s + (per_channel ? 0 : srow * (K / gsz));
     const int vec_per_grp = per_channel ? vec_per_row : gsz / 8;
     // four output vectors per lane per iteration: all raw loads in flight before converting
@@ -226,7 +239,9 @@ cudaError_t launch_dequant(int wbits, const uint8_t* q0, const float* s0, const 
   const int64_t n_rows = (int64_t)G * rows_out;
   if (n_rows == 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>((n_rows + 7) / 8, (int64_t)kNumSMs * 16);
-  if (wbits == 8)
+  if (wbits == 16)
+    dequant_kernel<16><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
+  else if (wbits == 8)
     dequant_kernel<8><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
   else
     dequant_kernel<4><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);

@@ -122,7 +122,7 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
       rr[1] = __ldg(rp + 1);
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj)
-        if (jj < p.k) {
+        if (jj < p.k && pos[jj] >= 0) {  // pos -1: a pick folded by gate re-routing (NEXT-2)
           const uint4* op = reinterpret_cast<const uint4*>(p.y_perm + (int64_t)pos[jj] * H + c0);
           oo[jj][0] = __ldg(op);
           oo[jj][1] = __ldg(op + 1);
@@ -142,7 +142,7 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
       for (int i = 0; i < 16; ++i) acc[i] += __bfloat162float(__float2bfloat16_rn(v[i]));  // o_sh = bf16(a·ŵ)
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj)
-        if (jj < p.k) {
+        if (jj < p.k && pos[jj] >= 0) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&oo[jj][h]);

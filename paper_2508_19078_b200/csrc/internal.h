@@ -22,7 +22,7 @@ inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_O
 // ---------------------------------------------------------------- per-kernel timing (timing.cpp)
 enum KernelKind {
   K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_SCHEDULE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
-  K_GEMM_DN_SH_COMBINE, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, FLUX_NUM_KERNELS
+  K_GEMM_DN_SH_COMBINE, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, K_COSINE, FLUX_NUM_KERNELS
 };
 // RAII: counts one launch; when timing is enabled records CUDA events around it on `st`.
 class KernelTimer {
@@ -47,7 +47,11 @@ cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, i
                             cudaStream_t st);
 // K7 (merge.cu)
 cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
-                         const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st);
+                         const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st, int compact = 0);
+// output error of a merged model: mean over tokens of 1 - cos(a_t, b_t)
+size_t cosine_workspace();
+cudaError_t launch_cosine_distance(int64_t T, int H, const void* a, const void* b, double* ws, double* out,
+                                   cudaStream_t st);
 
 // NEXT-1 expert clustering (cluster.cu), §5.2
 constexpr int kClusterMaxE = 128, kClusterMaxD = 32, kClusterMaxL = 128;
@@ -77,6 +81,8 @@ struct RouterArgs {
   int64_t* hist;        // [E] (+=)
   int32_t* tile_counts; // [n_tiles][E]
   int32_t* rank;        // [T][k] rank of t inside its 128-token tile among tokens choosing the same expert
+  int E_slots;           // experts of the weights (hist, tile counts); == E unless re-routing
+  const int32_t* remap;  // [E] pick -> slot (NEXT-2 gate re-routing) or null
 };
 cudaError_t launch_router(const CUtensorMap& tmap_x, const CUtensorMap& tmap_wr, int npad, const RouterArgs& a,
                           cudaStream_t st);

@@ -55,17 +55,37 @@ __device__ __forceinline__ void store_vec(void* base, int64_t elem, const float 
   }
 }
 
+// compact = 0: outputs are the C clusters.  compact = 1 (NEXT-2): outputs are the slots of the
+// compact model in remap order — every tuning expert as its own slot (ascending id; a singleton
+// with weight α/α = 1, so its copy is bit-exact), then the C clusters.
 template <bool F32>
 __global__ void __launch_bounds__(256) merge_kernel(int E, int64_t numel, const void* __restrict__ experts,
                                                     const int32_t* __restrict__ cluster_of,
                                                     const float* __restrict__ alpha, int C, void* __restrict__ merged,
-                                                    int32_t* __restrict__ remap) {
+                                                    int32_t* __restrict__ remap, int compact) {
   __shared__ int s_cl[kMaxE];
   __shared__ float s_w[kMaxE];       // weight of member slot
   __shared__ int s_mem[kMaxE];       // member expert ids grouped by cluster
   __shared__ int s_start[kMaxE + 1]; // cluster -> first member slot
+  __shared__ int s_ntun;
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_cl[e] = cluster_of[e];
   __syncthreads();
+  if (compact) {  // relabel: tuning expert -> its rank among tuning experts, cluster c -> n_tun + c
+    if (threadIdx.x == 0) {
+      int n = 0;
+      for (int e = 0; e < E; ++e) n += s_cl[e] < 0;
+      s_ntun = n;
+    }
+    __syncthreads();
+    const int n_tun = s_ntun;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int r = 0;
+      for (int e = 0; e < E; ++e) s_cl[e] = s_cl[e] < 0 ? r++ : n_tun + s_cl[e];
+    }
+    C += n_tun;
+    __syncthreads();
+  }
   // per cluster: count, Σα (ascending e), then the member slots
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     int cnt = 0;
@@ -93,11 +113,15 @@ __global__ void __launch_bounds__(256) merge_kernel(int E, int64_t numel, const 
   }
   __syncthreads();
   if (remap && blockIdx.x == 0 && threadIdx.x == 0) {
-    int slot = 0;
-    for (int e = 0; e < E; ++e)
-      if (s_cl[e] == -1) remap[e] = slot++;
-    for (int e = 0; e < E; ++e)
-      if (s_cl[e] >= 0) remap[e] = slot + s_cl[e];
+    if (compact) {
+      for (int e = 0; e < E; ++e) remap[e] = s_cl[e];
+    } else {
+      int slot = 0;
+      for (int e = 0; e < E; ++e)
+        if (s_cl[e] == -1) remap[e] = slot++;
+      for (int e = 0; e < E; ++e)
+        if (s_cl[e] >= 0) remap[e] = slot + s_cl[e];
+    }
   }
   const int64_t nvec = numel / 8;
   const int64_t items = (int64_t)C * nvec;
@@ -119,13 +143,13 @@ __global__ void __launch_bounds__(256) merge_kernel(int E, int64_t numel, const 
 }  // namespace
 
 cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
-                         const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st) {
-  const int64_t items = (int64_t)C * (numel / 8);
+                         const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st, int compact) {
+  const int64_t items = (int64_t)(compact ? E : C) * (numel / 8);  // upper bound for the compact case
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)kNumSMs * 8));
   if (fp32)
-    merge_kernel<true><<<grid, 256, 0, st>>>(E, numel, experts, cluster_of, alpha, C, merged, remap);
+    merge_kernel<true><<<grid, 256, 0, st>>>(E, numel, experts, cluster_of, alpha, C, merged, remap, compact);
   else
-    merge_kernel<false><<<grid, 256, 0, st>>>(E, numel, experts, cluster_of, alpha, C, merged, remap);
+    merge_kernel<false><<<grid, 256, 0, st>>>(E, numel, experts, cluster_of, alpha, C, merged, remap, compact);
   return cudaGetLastError();
 }
 

@@ -126,10 +126,11 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
   int pos[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    pos[j] = 0;
+    pos[j] = -1;
     if (j < k) {
       const int e = __ldg(&ids[t * k + j]);
-      pos[j] = __ldg(&offsets[e]) + __ldg(&tile_base[(int64_t)tile * E + e]) + __ldg(&rank[t * k + j]);
+      if (e >= 0)  // -1: a pick folded by gate re-routing (NEXT-2) owns no row
+        pos[j] = __ldg(&offsets[e]) + __ldg(&tile_base[(int64_t)tile * E + e]) + __ldg(&rank[t * k + j]);
     }
   }
   if (lane < k) {
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
     for (int j = 0; j < 8; ++j)
       if (j == lane) p = pos[j];
     inv_pos[t * k + lane] = p;
-    token_index[p] = (int32_t)t;
+    if (p >= 0) token_index[p] = (int32_t)t;
   }
   if (!x_perm) return;  // the GEMM gathers A rows from x itself (TMA tile::gather4)
   const int nvec = H / 8;  // 16-byte vectors per row
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
       if (c0 + 32 * u >= nvec) continue;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < k) x_perm[(int64_t)pos[j] * nvec + c0 + 32 * u] = v[u];
+        if (j < k && pos[j] >= 0) x_perm[(int64_t)pos[j] * nvec + c0 + 32 * u] = v[u];
     }
   }
 }

@@ -16,7 +16,8 @@
 // each token sets its bit in a per-expert 128-bit mask in shared memory; one
 // popcount per expert gives this tile's count (one global atomic per expert
 // per CTA) and the stable within-tile rank of every (token, expert) pair that
-// the permutation (K2) needs.
+// the permutation (K2) needs.  NEXT-2 gate re-routing (§7, R14): with a remap table
+// the picks are sent to the compact model's slots in the same epilogue, repeated slots folded.
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -162,11 +163,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       psum += ps[j];
     }
 
+    // gate weights; with re-routing (NEXT-2, R14) every pick goes to remap[id] and a pick whose slot
+    // repeats an earlier (higher-logit) pick's is folded into it: weight added, pick emptied (-1)
+    float wt[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) wt[j] = j < k ? (a.norm ? ps[j] / psum : ps[j]) : 0.f;
+    if (a.remap) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) ids[j] = __ldg(&a.remap[ids[j]]);
+#pragma unroll
+      for (int j = 1; j < 8; ++j) {
+        if (j >= k) continue;
+        bool done = false;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i < j && !done && ids[i] >= 0 && ids[i] == ids[j]) {
+            wt[i] += wt[j];
+            wt[j] = 0.f;
+            ids[j] = -1;
+            done = true;
+          }
+      }
+    }
+
     named_bar_sync(1, 128);  // masks zeroed
     if (valid) {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < k) atomicOr(&masks[ids[j] * 4 + (row >> 5)], 1u << (row & 31));
+        if (j < k && ids[j] >= 0) atomicOr(&masks[ids[j] * 4 + (row >> 5)], 1u << (row & 31));
     }
     named_bar_sync(1, 128);
 
@@ -178,11 +203,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         if (j >= k) continue;
-        const uint32_t* m = &masks[ids[j] * 4];
-        int r = __popc(m[row >> 5] & below);
-        for (int wd = 0; wd < (row >> 5); ++wd) r += __popc(m[wd]);
+        int r = 0;
+        if (ids[j] >= 0) {
+          const uint32_t* m = &masks[ids[j] * 4];
+          r = __popc(m[row >> 5] & below);
+          for (int wd = 0; wd < (row >> 5); ++wd) r += __popc(m[wd]);
+        }
         gid[j] = ids[j];
-        gw[j] = a.norm ? ps[j] / psum : ps[j];
+        gw[j] = wt[j];
         grk[j] = r;
       }
       if (a.logits) {
@@ -192,10 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (e < E) gl[e] = z[e];
       }
     }
-    if (et < E) {
+    if (et < a.E_slots) {
       const uint32_t* m = &masks[et * 4];
       const int cnt = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
-      a.tile_counts[(int64_t)tile * E + et] = cnt;
+      a.tile_counts[(int64_t)tile * a.E_slots + et] = cnt;
       if (cnt) atomicAdd(reinterpret_cast<unsigned long long*>(a.hist + et), (unsigned long long)cnt);
     }
   }

@@ -17,8 +17,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import (FLUX_OK, Comm, LayerOut, QLayer, cluster_experts, expert_features, layer_budget, make_cfg,
-               merge_experts, profile_layer, profile_layer_workspace, quantize_weights)
+from . import (FLUX_OK, Comm, LayerOut, QLayer, cluster_experts, compact_experts, expert_features, layer_budget,
+               make_cfg, merge_experts, output_error, profile_layer, profile_layer_workspace, quantize_weights)
 
 
 @dataclass
@@ -32,6 +32,7 @@ class ModelShape:
     wbits: int
     group_size: int
     norm_topk: int
+    n_router: int = 0  # > 0: gate re-routing (NEXT-2): the router scores n_router original experts
 
     @staticmethod
     def of(cfg) -> "ModelShape":
@@ -40,7 +41,7 @@ class ModelShape:
 
     def ccfg(self):
         return make_cfg(self.hidden, self.ffn, self.n_experts, self.top_k, self.shared_ffn, self.wbits,
-                        self.group_size, self.norm_topk)
+                        self.group_size, self.norm_topk, self.n_router)
 
 
 @dataclass
@@ -112,6 +113,56 @@ class QuantizedModel:
                       p(self.sh_up_s), p(self.sh_down_s))
 
 
+class DenseWeights:
+    """Full-precision (bf16) expert weights run by flux_profile_layer with wbits = 16 (NEXT-2): the original
+    model (remap None) or the compact model after merging (slots = tuning experts + clusters; the router keeps
+    the E original experts and remap [L][E] re-routes its picks, §7)."""
+
+    def __init__(self, shape: ModelShape, router, gate, up, down, sh_gate=None, sh_up=None, sh_down=None,
+                 remap=None):
+        self.shape = shape
+        self.router, self.gate, self.up, self.down = router, gate, up, down
+        self.sh_gate, self.sh_up, self.sh_down = sh_gate, sh_up, sh_down
+        self.remap = remap
+
+    def qlayer(self, l: int) -> QLayer:
+        p = lambda t: None if t is None else t[l].data_ptr()  # noqa: E731
+        q = QLayer(p(self.router), p(self.gate), p(self.up), p(self.down), None, None, None, p(self.sh_gate),
+                   p(self.sh_up), p(self.sh_down), None, None, None)
+        q.remap = p(self.remap)
+        return q
+
+
+def dense_model(m: MasterWeights) -> DenseWeights:
+    """The original model in full precision (the reference for the merge output error)."""
+    s = m.shape
+    shape = ModelShape(s.n_layers, s.hidden, s.n_experts, s.top_k, s.ffn, s.shared_ffn, 16, 0, s.norm_topk)
+    return DenseWeights(shape, m.router, m.gate, m.up, m.down, m.sh_gate, m.sh_up, m.sh_down)
+
+
+def compact_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tensor, n_clusters: int,
+                  n_tuning: int = 0, stream=None) -> DenseWeights:
+    """NEXT-2: the compact model (§7 "Customized MoE construction" + "Gate re-routing"): per layer the slots
+    [n_tuning tuning experts (ascending id), n_clusters eq.(2) merges] of every weight family
+    (flux_compact_experts) and the remap of the router's picks.  Every layer must keep n_tuning experts."""
+    s = m.shape
+    L, E, F, H = s.n_layers, s.n_experts, s.ffn, s.hidden
+    S = n_tuning + n_clusters
+    dev = m.gate.device
+    gate = torch.empty(L, S, F, H, dtype=m.gate.dtype, device=dev)
+    up = torch.empty_like(gate)
+    down = torch.empty(L, S, H, F, dtype=m.gate.dtype, device=dev)
+    remap = torch.empty(L, E, dtype=torch.int32, device=dev)
+    for l in range(L):
+        compact_experts(m.gate[l].view(E, -1), cluster_of[l], alpha[l], n_clusters, gate[l].view(S, -1), remap[l],
+                        stream)
+        compact_experts(m.up[l].view(E, -1), cluster_of[l], alpha[l], n_clusters, up[l].view(S, -1), None, stream)
+        compact_experts(m.down[l].view(E, -1), cluster_of[l], alpha[l], n_clusters, down[l].view(S, -1), None,
+                        stream)
+    shape = ModelShape(L, H, S, s.top_k, F, s.shared_ffn, 16, 0, s.norm_topk, n_router=E)
+    return DenseWeights(shape, m.router, gate, up, down, m.sh_gate, m.sh_up, m.sh_down, remap)
+
+
 class Profiler:
     """Buffers for profiling T tokens through all layers (a1-a6) on one GPU."""
 
@@ -127,7 +178,8 @@ class Profiler:
         self.hist = torch.zeros(L, E, dtype=torch.int64, device=device)
         self.offsets = torch.empty(L, E + 1, dtype=torch.int32, device=device) if with_de else None
         self.token_index = torch.empty(L, T * k, dtype=torch.int32, device=device) if with_de else None
-        self.logits = torch.empty(L, T, E, dtype=torch.float32, device=device) if with_logits else None
+        E_r = s.n_router or E  # the router scores the original experts under gate re-routing
+        self.logits = torch.empty(L, T, E_r, dtype=torch.float32, device=device) if with_logits else None
 
     def out(self, l: int) -> LayerOut:
         p = lambda t: None if t is None else t[l].data_ptr()  # noqa: E731
@@ -222,4 +274,5 @@ def budgets(hist_host: np.ndarray, T_total: int, B_non: int, n_non=None):
 
 
 __all__ = ["ModelShape", "MasterWeights", "QuantizedModel", "Profiler", "MergedModel", "merge_model", "frequencies",
-           "budgets", "feature_dim", "expert_features_model", "cluster_model", "Comm", "FLUX_OK"]
+           "budgets", "feature_dim", "expert_features_model", "cluster_model", "DenseWeights", "dense_model",
+           "compact_model", "output_error", "Comm", "FLUX_OK"]
