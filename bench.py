@@ -8,7 +8,7 @@ One step = one participant round of the hot path (all rows):
   a7 all-reduce the int64 histograms         flux_reduce_stats (NCCL)
   a8-pre eq.(1) layer budgets (host)         flux_layer_budget
   §5.2 expert clustering (NEXT-1): PCA features of every layer's experts
-        (side stream, overlapping a1-a6) + fused K-Means into 16 clusters
+        + fused K-Means into 16 clusters from the reduced counts
                                              flux_expert_features, flux_cluster_experts
   a8 eq.(2) merge 64 -> 16 experts per layer, α = f (bf16)   flux_merge_experts
 Data parallel over tokens, weak scaling: every rank profiles its own shard of
@@ -151,6 +151,10 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=32)  # oracle sample: ~10 s of host CPU work
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--clusters", type=int, default=0)
+    ap.add_argument("--error-tokens", type=int, default=8192,
+                    help="tokens for the merged model's output error after the timed run (0 = skip)")
+    ap.add_argument("--features-stream", default="main", choices=["main", "side"],
+                    help="PCA features in stream order (default) or on a side stream overlapping the profiling")
     ap.add_argument("--clustering", default="pca", choices=["pca", "seeded"],
                     help="pca: §5.2 PCA + K-Means on the GPU inside the step; seeded: a fixed balanced partition")
     args = ap.parse_args()
@@ -205,13 +209,16 @@ def main():
 
     def step(x_in):
         nonlocal merged, cluster_of
-        if args.clustering == "pca":                                # §5.2 C1 on a side stream (reads masters only)
+        if args.clustering == "pca" and args.features_stream == "side":  # §5.2 C1 overlapping a0-a7
             ev_start.record(stream)
             side.wait_event(ev_start)
             with torch.cuda.stream(side):
                 feats, _, _ = expert_features_model(masters, d_feat, stream=side)
                 ev_feat.record(side)
             feats.record_stream(stream)
+        elif args.clustering == "pca":                              # §5.2 C1 in stream order (reads masters only)
+            feats, _, _ = expert_features_model(masters, d_feat)
+            ev_feat.record(stream)
         qm.quantize_from(masters)                                   # a0
         prof.run(qm, x_in)                                          # a1-a6 (hist zeroed first)
         comm.reduce_stats(prof.hist)                                # a7
@@ -289,6 +296,25 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
 
+    # ---- merge quality of the round's merged model (not timed): the paper's output error —
+    #      mean cosine distance between the final outputs of the compact model (tuning experts + the
+    #      eq.(2) merges, gate re-routed, bf16) and of the original bf16 model on the first tokens of x
+    merr = None
+    if args.error_tokens > 0 and rank == 0:
+        from paper_2508_19078_b200.driver import compact_model, dense_model
+        n_err = min(args.error_tokens, T)
+        dense = dense_model(masters)
+        comp = compact_model(masters, alpha, cluster_of, C, 0)
+        outs = []
+        for mdl in (dense, comp):
+            pr = Profiler(mdl.shape, n_err, with_de=False)
+            outs.append(pr.run(mdl, x[:n_err]).clone())
+            del pr
+        merr = {"value": float(F.output_error(outs[1], outs[0]).item()), "tokens": n_err,
+                "clusters_per_layer": C, "alpha": "f", "clustering": args.clustering,
+                "what": "mean cosine distance of final token outputs, merged vs original bf16 model (P:686-689)"}
+        del comp, outs
+
     if rank == 0:
         peaks, peak_src = load_peaks()
         value = T_total * args.steps / (ms / 1000.0)
@@ -319,6 +345,7 @@ def main():
             "clocks": clk,
             "kernels": kernels,
             "budget_C": [int(c) for c in budget_out.get("C", [])][:4],
+            "merge_output_error": merr,
         }
         if world == 1 and not args.no_cpu_baseline:
             r, threads, sample, dt = oracle_rate(cfg, args.ref_tokens, args.ref_layers, T)

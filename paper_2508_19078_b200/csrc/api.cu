@@ -469,8 +469,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   // ---- (f) K6 combine: fused into the shared-MLP down GEMM when there is one, else standalone
   if (!fuse_combine) {
     KernelTimer kt(K_COMBINE, s);
-    if ((e = launch_combine(T, H, k, resid, sh ? y_sh : nullptr, y_perm, out->topk_w, inv_pos, out->y, s)) !=
-        cudaSuccess) {
+    if ((e = launch_combine(T, H, k, resid, sh ? y_sh : nullptr, y_perm, out->topk_w, inv_pos, out->y, s,
+                            c.n_router > 0)) != cudaSuccess) {
       set_last_error("combine", e);
       return FLUX_E_CUDA;
     }

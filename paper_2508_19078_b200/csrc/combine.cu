@@ -19,6 +19,9 @@ __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
   }
 }
 
+// EMPTY: picks may be empty (pos -1, folded by gate re-routing, NEXT-2).  The plain path keeps
+// every load unconditional so all (k + 2) x 2 loads issue before any is used.
+template <bool EMPTY>
 __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, const uint4* __restrict__ residual,
                                                       const uint4* __restrict__ y_sh, const uint4* __restrict__ y_perm,
                                                       const float* __restrict__ w, const int32_t* __restrict__ inv_pos,
@@ -51,7 +54,7 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
       if (y_sh) sv[u] = __ldg(&y_sh[t * nvec + c]);
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < k && pos[j] >= 0) ov[j][u] = __ldcs(&y_perm[(int64_t)pos[j] * nvec + c]);  // read once: streaming
+        if (j < k && (!EMPTY || pos[j] >= 0)) ov[j][u] = __ldcs(&y_perm[(int64_t)pos[j] * nvec + c]);  // streaming
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (j < k && pos[j] >= 0) {  // pos -1: a pick folded by gate re-routing
+        if (j < k && (!EMPTY || pos[j] >= 0)) {  // pos -1: a pick folded by gate re-routing
           unpack8(ov[j][u], f);
 #pragma unroll
           for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt[j], f[i], acc[i]);
@@ -83,11 +86,15 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
 }  // namespace
 
 cudaError_t launch_combine(int64_t T, int H, int k, const void* residual, const void* y_sh, const void* y_perm,
-                           const float* w, const int32_t* inv_pos, void* y, cudaStream_t st) {
+                           const float* w, const int32_t* inv_pos, void* y, cudaStream_t st, bool empty_picks) {
   if (T == 0) return cudaSuccess;
   const unsigned grid = (unsigned)((T + 7) / 8);
-  combine_kernel<<<grid, 256, 0, st>>>(T, H, k, (const uint4*)residual, (const uint4*)y_sh, (const uint4*)y_perm, w,
-                                       inv_pos, (uint4*)y);
+  if (empty_picks)
+    combine_kernel<true><<<grid, 256, 0, st>>>(T, H, k, (const uint4*)residual, (const uint4*)y_sh,
+                                               (const uint4*)y_perm, w, inv_pos, (uint4*)y);
+  else
+    combine_kernel<false><<<grid, 256, 0, st>>>(T, H, k, (const uint4*)residual, (const uint4*)y_sh,
+                                                (const uint4*)y_perm, w, inv_pos, (uint4*)y);
   return cudaGetLastError();
 }
 

@@ -116,7 +116,8 @@ cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const 
 
 // K6 (combine.cu)
 cudaError_t launch_combine(int64_t T, int H, int k, const void* residual, const void* y_sh, const void* y_perm,
-                           const float* w, const int32_t* inv_pos, void* y, cudaStream_t st);
+                           const float* w, const int32_t* inv_pos, void* y, cudaStream_t st,
+                           bool empty_picks = false);
 
 // K3/K4/K5 (gemm.cu)
 enum GemmEpi { EPI_SWIGLU = 0, EPI_STORE = 1, EPI_COMBINE = 2 };
