@@ -125,7 +125,7 @@ int pad128(int v) { return (v + 127) / 128 * 128; }
 WsPlan plan(const flux_moe_cfg& c, int64_t T) {
   Layout L;
   WsPlan p;
-  const int64_t n_rt = (T + 127) / 128;
+  const int64_t n_rt = (T + kRouterTile - 1) / kRouterTile;
   const int64_t Tk = T * c.top_k;
   const int n_groups = c.n_experts + (c.shared_ffn > 0);
   p.tile_counts = L.take(sizeof(int32_t) * n_rt * c.n_experts);
@@ -233,7 +233,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   const int E_r = c.n_router > 0 ? c.n_router : E;           // experts the router scores
   const int g_h = per_channel ? H : c.group_size, g_f = per_channel ? F : c.group_size,
             g_fs = per_channel ? Fs : c.group_size;
-  const int64_t n_rt = (T + 127) / 128;
+  const int64_t n_rt = (T + kRouterTile - 1) / kRouterTile;
   const int64_t Tk = T * k;
   const int n_groups = E + (sh ? 1 : 0);
 
@@ -278,7 +278,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   // ---- (b) K1 router + top-k + histogram
   const int npad = E_r <= 16 ? 16 : E_r <= 32 ? 32 : E_r <= 64 ? 64 : 128;
   CUtensorMap tm_x, tm_wr;
-  if (!tmap_bf16(&tm_x, x, T, H, 128) || !tmap_bf16(&tm_wr, w->router_w, E_r, H, npad)) { set_last_error("router tensor map", cudaErrorInvalidValue); return FLUX_E_CUDA; }
+  if (!tmap_bf16(&tm_x, x, T, H, kRouterTile) || !tmap_bf16(&tm_wr, w->router_w, E_r, H, npad)) { set_last_error("router tensor map", cudaErrorInvalidValue); return FLUX_E_CUDA; }
   RouterArgs ra{T, H, E_r, k, c.norm_topk, out->topk_ids, out->topk_w, out->router_logits, out->hist, tile_counts, rank,
                 E, c.n_router > 0 ? w->remap : nullptr};
   {

@@ -9,6 +9,7 @@
 namespace flux {
 
 constexpr int kNumSMs = 148;
+constexpr int kRouterTile = 256;  // tokens per router tile: the unit of tile_counts / tile_base / rank
 
 // TMA descriptor for a row-major 2D tensor [rows][cols] of `elem_bytes` elements,
 // box = box_cols x box_rows, 128-byte swizzle (box_cols * elem_bytes must be 128 or
@@ -80,7 +81,7 @@ struct RouterArgs {
   float* logits;        // [T][E] or null
   int64_t* hist;        // [E] (+=)
   int32_t* tile_counts; // [n_tiles][E]
-  int32_t* rank;        // [T][k] rank of t inside its 128-token tile among tokens choosing the same expert
+  int32_t* rank;        // [T][k] rank of t inside its router tile among tokens choosing the same expert
   int E_slots;           // experts of the weights (hist, tile counts); == E unless re-routing
   const int32_t* remap;  // [E] pick -> slot (NEXT-2 gate re-routing) or null
 };
@@ -91,7 +92,7 @@ cudaError_t launch_router(const CUtensorMap& tmap_x, const CUtensorMap& tmap_wr,
 struct ScheduleArgs {
   int E, k;
   int64_t T;
-  int n_tiles;              // router tiles (128 tokens)
+  int n_tiles;              // router tiles (kRouterTile tokens)
   const int32_t* tile_counts;
   int32_t* tile_base;       // [n_tiles][E]
   int32_t* offsets;         // [E+1] internal

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= T) return;
   const int lane = threadIdx.x & 31;
-  const int tile = (int)(t / 128);
+  const int tile = (int)(t / kRouterTile);
   int pos[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
