@@ -21,7 +21,8 @@ NAMES = [("grouped_gemm_pair_kernel<0>", "K3/K5 gate/up GEMM (pair)"), ("grouped
          ("grouped_gemm_pair_q_kernel<(int)1", "K4/K5 down GEMM (fused dequant)"),
          ("grouped_gemm_kernel<(int)0>", "K3/K5 gate/up GEMM (1-CTA)"), ("grouped_gemm_kernel<(int)1>", "K4/K5 down GEMM (1-CTA)"),
          ("combine_kernel", "K6 combine"), ("quantize_kernel", "K0 quantize"), ("dequant_kernel", "K3/K4 dequant pass"),
-         ("merge_kernel", "K7 merge")]
+         ("merge_kernel", "K7 merge"), ("gram_reduce_kernel", "K8b Gram reduce"), ("gram_kernel", "K8 Gram (PCA)"),
+         ("eig_kernel", "K8c Jacobi eigen"), ("kmeans_kernel", "K9 K-Means"), ("cosine_distance_kernel", "output error")]
 
 
 def label(name):
@@ -38,7 +39,11 @@ def launches(path, out):
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
     agg = collections.OrderedDict()
+    setup = collections.Counter()
     for r in rows[i + 1:]:
+        if "synth_kernel" in r[ki]:  # input generation during setup (not part of a step)
+            setup[r[ki][:40]] += 1
+            continue
         ms = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6)
         agg.setdefault(label(r[ki]), []).append(ms)
     total = sum(sum(v) for v in agg.values())
@@ -50,6 +55,9 @@ def launches(path, out):
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| {k} | {len(v)} | {sum(v) / len(v):.3f} | {sum(v):.1f} | {100 * sum(v) / total:.1f}% |")
     lines.append(f"| **all** | {sum(len(v) for v in agg.values())} | | {total:.1f} | 100% |")
+    if setup:
+        lines += ["", f"Excluded (setup, not in a step): {dict(setup)}. `FillFunctor` = the per-round "
+                      "histogram zeroing (`hist.zero_()`, the caller's duty per include/flux.h)."]
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
