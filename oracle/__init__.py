@@ -56,6 +56,7 @@ def lib():
         L.orc_quantize.argtypes = [_I, _I64, _I64, _I64, _P, _P, _P]
         L.orc_quantize.restype = _I
         L.orc_pack_int4.argtypes = [_I64, _I64, _P, _P]
+        L.orc_pack_int2.argtypes = [_I64, _I64, _P, _P]
         L.orc_router.argtypes = [_I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]
         L.orc_router.restype = _I
         L.orc_permute.argtypes = [_I64, _I, _I, _P, _P, _P, _P, _P]
@@ -93,6 +94,20 @@ def quantize(w, wbits: int, group_size: int):
     if lib().orc_quantize(wbits, g, R, K, w.ctypes.data, q.ctypes.data, s.ctypes.data):
         raise ValueError("bad quantization arguments")
     return q, s
+
+
+def pack_int2(q):
+    """Canonical INT2 storage: four codes per byte, element k in bits 2·(k mod 4)."""
+    q = _c(q, np.int8)
+    R, K = q.shape
+    out = np.empty((R, K // 4), np.uint8)
+    lib().orc_pack_int2(R, K, q.ctypes.data, out.ctypes.data)
+    return out
+
+
+def pack(q, wbits: int):
+    """Canonical storage of codes at a bit level (INT8 unpacked)."""
+    return pack_int2(q) if wbits == 2 else pack_int4(q) if wbits == 4 else _c(q, np.int8)
 
 
 def pack_int4(q):

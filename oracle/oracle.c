@@ -54,14 +54,14 @@ void orc_bf16_round_array(int64_t n, const double* in, double* out) {
 
 /* ----------------------------------------------------------------------------
  * O1. Quantize (R1).  w: [R][K] real values; groups of g consecutive k in a row
- * (g == K: per output channel).  qmax = 2^(b-1) - 1.
+ * (g == K: per output channel).  qmax = 2^(b-1) - 1, b in {2, 4, 8} (b = 2: NEXT-3).
  *   a = max_{k in group} |w|           (exact, the inputs are fp32 numbers)
  *   s = fl32(a / qmax)                 (one IEEE fp32 division, RNE)
  *   q = 0 if s == 0 else clamp(RNE(fl32(w / s)), -qmax-1, qmax)
  * Outputs: q [R][K] int8 (unpacked), s [R][K/g] fp32.
  * -------------------------------------------------------------------------- */
 int orc_quantize(int wbits, int64_t g, int64_t R, int64_t K, const float* w, int8_t* q, float* s) {
-  if ((wbits != 4 && wbits != 8) || g <= 0 || K % g != 0) return 1;
+  if ((wbits != 2 && wbits != 4 && wbits != 8) || g <= 0 || K % g != 0) return 1;
   const int qmax = (1 << (wbits - 1)) - 1;
   const int64_t G = K / g;
 #pragma omp parallel for schedule(static)
@@ -88,6 +88,17 @@ int orc_quantize(int wbits, int64_t g, int64_t R, int64_t K, const float* w, int
     }
   }
   return 0;
+}
+
+/* Canonical INT2 storage (NEXT-3, "2-bit"): four per byte, element k
+ * in bits 2·(k mod 4), two's complement. */
+void orc_pack_int2(int64_t R, int64_t K, const int8_t* q, uint8_t* packed) {
+  for (int64_t r = 0; r < R; ++r)
+    for (int64_t k = 0; k < K; k += 4) {
+      unsigned b = 0;
+      for (int j = 0; j < 4; ++j) b |= (unsigned)(q[r * K + k + j] & 0x3) << (2 * j);
+      packed[r * (K / 4) + k / 4] = (uint8_t)b;
+    }
 }
 
 /* Canonical INT4 storage (boundary, include/flux.h): two per byte, even k in

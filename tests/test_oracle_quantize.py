@@ -45,7 +45,13 @@ def test_pack_int4_example():
     assert list(out[0]) == g["bytes"]
 
 
-@pytest.mark.parametrize("wbits,g", [(8, 0), (4, 128), (4, 32), (8, 64)])
+def test_pack_int2_example():
+    g = json.load(open(os.path.join(GOLD, "quantize_examples.json")))["pack_int2"]
+    out = oracle.pack_int2(np.array([g["q"]], np.int8))
+    assert list(out[0]) == g["bytes"]
+
+
+@pytest.mark.parametrize("wbits,g", [(8, 0), (4, 128), (4, 32), (8, 64), (2, 128), (2, 0)])
 def test_round_trip_bound_and_range(wbits, g):
     rng = np.random.default_rng(wbits * 1000 + g)
     R, K = 37, 256
@@ -110,3 +116,15 @@ def test_bf16_round_matches_torch_on_fp32_values():
     v = (rng.standard_normal(10000) * 10.0 ** rng.uniform(-6, 6, 10000)).astype(np.float32)
     ref = torch.from_numpy(v).to(torch.bfloat16).to(torch.float64).numpy()
     assert np.array_equal(oracle.bf16_round(v.astype(np.float64)), ref)
+
+
+def test_pack_int2_roundtrip_random():
+    rng = np.random.default_rng(6)
+    q = rng.integers(-2, 2, size=(7, 64)).astype(np.int8)
+    p = oracle.pack_int2(q).astype(np.int16)
+    back = np.empty_like(q)
+    for j in range(4):
+        v = (p >> (2 * j)) & 0x3
+        v[v > 1] -= 4
+        back[:, j::4] = v
+    assert np.array_equal(back, q)
