@@ -151,6 +151,8 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=32)  # oracle sample: ~10 s of host CPU work
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--clusters", type=int, default=0)
+    ap.add_argument("--wbits", type=int, default=0, choices=[0, 2, 4, 8],
+                    help="override the config's bit level (2 = the paper's bit-2 ablation, NEXT-3)")
     ap.add_argument("--error-tokens", type=int, default=8192,
                     help="tokens for the merged model's output error after the timed run (0 = skip)")
     ap.add_argument("--features-stream", default="main", choices=["main", "side"],
@@ -161,6 +163,8 @@ def main():
 
     import synth
     cfg = synth.CONFIGS[args.config]
+    if args.wbits:
+        cfg = cfg.with_(wbits=args.wbits, name=f"{cfg.name}_int{args.wbits}")
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))

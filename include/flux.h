@@ -60,7 +60,8 @@ typedef struct {
   int32_t n_experts;  /* E, routed experts                                    */
   int32_t top_k;      /* k, experts per token                                 */
   int32_t shared_ffn; /* F_s of the always-on shared experts (0 = none), R5   */
-  int32_t wbits;      /* 8 or 4 (bit level chosen per participant); 16 = bf16
+  int32_t wbits;      /* 8, 4 or 2 (bit level chosen per participant; 2 = the "2-bit"
+                         of P:1516-1517, NEXT-3: four codes per byte, needs H, F, F_s % 64); 16 = bf16
                          weights, not quantized (the compact model after merging, NEXT-2) */
   int32_t group_size; /* 0 = per output channel, else g along the contraction (0 for wbits 16) */
   int32_t norm_topk;  /* 0: w = softmax prob; 1: renormalised over top-k (R2) */
@@ -73,9 +74,9 @@ typedef struct {
 
 /* Quantized weights of one layer, canonical layout (device pointers):
  *   router_w  bf16 [E_r][H]             (not quantized, R1; E_r = n_router or n_experts)
- *   gate_q    [E][F][H']   up_q [E][F][H']   H' = H (int8) or H/2 bytes (int4)
+ *   gate_q    [E][F][H']   up_q [E][F][H']   H' = H (int8), H/2 (int4) or H/4 bytes (int2)
  *   gate_s    fp32 [E][F][H/g]          (g = H when group_size == 0)
- *   down_q    [E][H][F']                F' = F or F/2
+ *   down_q    [E][H][F']                F' = F, F/2 or F/4
  *   down_s    fp32 [E][H][F/g]
  *   sh_*      same for the shared MLP with F_s instead of F (NULL if F_s == 0)
  *   wbits 16: *_q are bf16 [E][F][H] / [E][H][F] weights and the scales are ignored (may be NULL)
@@ -219,8 +220,9 @@ flux_status flux_comm_destroy(flux_comm* comm);
 /* Weight quantizer, reading R1: symmetric, per row,
  * groups of g along K (g = K if group_size == 0):
  *   s = fl32(max|w| / qmax), q = clamp(RNE(fl32(w/s)), -qmax-1, qmax), s = 0 -> q = 0
- * w: [R][K] bf16 or fp32 device; q: [R][K] int8 or [R][K/2] packed int4; s: fp32 [R][K/g].
- * Bit-exact (IEEE division, no fast-math).  Needs K % 2 == 0 for INT4. */
+ * w: [R][K] bf16 or fp32 device; q: [R][K] int8, [R][K/2] packed int4 or [R][K/4] packed int2
+ * (element k in bits 2(k mod 4)); s: fp32 [R][K/g].  wbits 8, 4 or 2 (qmax = 2^(b-1) - 1).
+ * Bit-exact (IEEE division, no fast-math).  Needs K % 8 == 0 for INT2. */
 flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype in_dtype, const void* w, int64_t R,
                                   int64_t K, void* q, float* s, void* stream);
 

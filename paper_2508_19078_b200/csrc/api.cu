@@ -76,7 +76,7 @@ static bool env_on(const char* name) {
 // Policy: pass when the average routed rows per expert reach 8 tile rows (2048); overrides:
 // FLUX_GEMM_DEQUANT_PASS=1 / FLUX_GEMM_FUSED_DEQUANT=1 (FLUX_GEMM_1SM=1 implies the pass).
 static bool dequant_pass(const flux_moe_cfg& c, int64_t T) {
-  if (c.wbits == 16) return true;  // bf16 weights: the pass is a layout copy; the fused kernel is for codes
+  if (c.wbits == 16 || c.wbits == 2) return true;  // bf16 copy / INT2 codes: the fused kernel does INT4/INT8
   if (env_on("FLUX_GEMM_DEQUANT_PASS") || env_on("FLUX_GEMM_1SM")) return true;
   if (env_on("FLUX_GEMM_FUSED_DEQUANT")) return false;
   return T * c.top_k >= (int64_t)2048 * c.n_experts;
@@ -159,7 +159,7 @@ flux_status validate_cfg(const flux_moe_cfg* c) {
   if (!c) return FLUX_E_INVALID;
   if (c->hidden <= 0 || c->ffn <= 0 || c->n_experts <= 0 || c->top_k <= 0 || c->shared_ffn < 0)
     return FLUX_E_INVALID;
-  if (c->wbits != 4 && c->wbits != 8 && c->wbits != 16) return FLUX_E_UNSUPPORTED;
+  if (c->wbits != 2 && c->wbits != 4 && c->wbits != 8 && c->wbits != 16) return FLUX_E_UNSUPPORTED;
   if (c->wbits == 16 && c->group_size != 0) return FLUX_E_UNSUPPORTED;
   if (c->n_router < 0) return FLUX_E_INVALID;
   if (c->n_router > 0 && (c->n_router > 128 || c->n_experts > c->n_router || c->top_k > c->n_router))
@@ -174,6 +174,7 @@ flux_status validate_cfg(const flux_moe_cfg* c) {
       return FLUX_E_UNSUPPORTED;
   }
   if (c->wbits == 4 && (c->hidden % 32 || c->ffn % 32 || c->shared_ffn % 32)) return FLUX_E_UNSUPPORTED;
+  if (c->wbits == 2 && (c->hidden % 64 || c->ffn % 64 || c->shared_ffn % 64)) return FLUX_E_UNSUPPORTED;
   return FLUX_OK;
 }
 }  // namespace
@@ -480,8 +481,9 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
 
 flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype in_dtype, const void* w, int64_t R,
                                   int64_t K, void* q, float* s, void* stream) {
-  if (wbits != 4 && wbits != 8) return FLUX_E_UNSUPPORTED;
+  if (wbits != 2 && wbits != 4 && wbits != 8) return FLUX_E_UNSUPPORTED;
   if (in_dtype != FLUX_BF16 && in_dtype != FLUX_FP32) return FLUX_E_INVALID;
+  if (wbits == 2 && K % 8) return FLUX_E_UNSUPPORTED;
   if (R < 0 || K <= 0 || group_size < 0) return FLUX_E_INVALID;
   const int64_t g = group_size ? group_size : K;
   if (K % g || g % 8 || g > 4096) return FLUX_E_UNSUPPORTED;

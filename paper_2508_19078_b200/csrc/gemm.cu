@@ -204,13 +204,15 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
     for (int v0 = lane; v0 < vec_per_row; v0 += 128) {
       uint32_t r4[4];
       uint2 r8[4];
+      uint32_t r2[4];
       float sc[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int v = v0 + 32 * u;
         if (v >= vec_per_row) continue;
         sc[u] = per_channel ? 0.f : __ldg(&srow_s[v / vec_per_grp]);
-        if (WBITS == 4) r4[u] = __ldg(reinterpret_cast<const uint32_t*>(q + srow * (K / 2)) + v);
+        if (WBITS == 2) r2[u] = __ldg(reinterpret_cast<const uint16_t*>(q + srow * (K / 4)) + v);
+        else if (WBITS == 4) r4[u] = __ldg(reinterpret_cast<const uint32_t*>(q + srow * (K / 2)) + v);
         else r8[u] = __ldg(reinterpret_cast<const uint2*>(q + srow * K) + v);
       }
 #pragma unroll
@@ -218,7 +220,10 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
         const int v = v0 + 32 * u;
         if (v >= vec_per_row) continue;
         const float s = __bfloat162float(__float2bfloat16_rn(sc[u]));
-        if (WBITS == 4) {
+        if (WBITS == 2) {
+          dst[v] = per_channel ? deq_int2x8<false>(r2[u], __floats2bfloat162_rn(0.f, 0.f))
+                               : deq_int2x8<true>(r2[u], __floats2bfloat162_rn(s, s));
+        } else if (WBITS == 4) {
           dst[v] = per_channel ? deq_int4x8<false>(r4[u], __floats2bfloat162_rn(0.f, 0.f))
                                : deq_int4x8<true>(r4[u], __floats2bfloat162_rn(s, s));
         } else {
@@ -243,6 +248,8 @@ cudaError_t launch_dequant(int wbits, const uint8_t* q0, const float* s0, const 
     dequant_kernel<16><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
   else if (wbits == 8)
     dequant_kernel<8><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
+  else if (wbits == 2)
+    dequant_kernel<2><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
   else
     dequant_kernel<4><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
   return cudaGetLastError();

@@ -241,6 +241,31 @@ __device__ __forceinline__ uint4 deq_int4x8(uint32_t w, __nv_bfloat162 s2) {
   return o;
 }
 
+// 8 INT2 codes (16 bits, element k in bits 2k) -> 8 bf16 (16 bytes), same scheme as INT4: offset
+// binary q + 2 in the mantissa of bf16 128, minus 130 exactly.
+template <bool GROUPED>
+__device__ __forceinline__ uint4 deq_int2x8(uint32_t w16, __nv_bfloat162 s2) {
+  const uint32_t x = (w16 ^ 0xAAAAu) & 0xFFFFu;          // two's complement -> offset binary (q + 2)
+  const uint32_t x2 = (x & 0xFFu) | ((x & 0xFF00u) << 8);  // codes 0-3 in bits 0-7, codes 4-7 in bits 16-23
+  uint32_t p[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) p[i] = ((x2 >> (2 * i)) & 0x00030003u) | 0x43004300u;  // bf16 {130+q_i, 130+q_{i+4}}
+  const __nv_bfloat162 off = __floats2bfloat162_rn(130.0f, 130.0f);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&p[i]);
+    v = __hsub2(v, off);               // exact q
+    if (GROUPED) v = __hmul2(v, s2);   // bf16(q * bf16(s)): exact product, one rounding
+    p[i] = *reinterpret_cast<uint32_t*>(&v);
+  }
+  uint4 o;
+  o.x = __byte_perm(p[0], p[1], 0x5410);
+  o.y = __byte_perm(p[2], p[3], 0x5410);
+  o.z = __byte_perm(p[0], p[1], 0x7632);
+  o.w = __byte_perm(p[2], p[3], 0x7632);
+  return o;
+}
+
 // 4 INT8 codes (one word, k order) -> 2 bf16x2 words; q exact via the fp32 2^23 magic.
 template <bool GROUPED>
 __device__ __forceinline__ uint2 deq_int8x4(uint32_t w, float s) {

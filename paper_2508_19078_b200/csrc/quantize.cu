@@ -5,7 +5,7 @@
 //   s = fl32(max|w| / qmax),  q = clamp(RNE(fl32(w / s)), -qmax-1, qmax),  s == 0 -> q = 0
 // IEEE division (__fdiv_rn) and round-to-nearest-even conversion, so the
 // result is bit-identical to any correct implementation of that definition.
-// INT4 output is packed two per byte, even k in the low nibble.
+// INT4 output is packed two per byte, even k in the low nibble; INT2 (NEXT-3) four per byte.
 //
 // HBM-bound: a team of lanes owns one (row, group); every lane loads 16 B
 // vectors of the group once into registers, the team max-reduces with
@@ -94,7 +94,12 @@ __global__ void __launch_bounds__(256) quantize_kernel(const void* __restrict__ 
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) qi[j] = max(-qmax - 1, min(qmax, qi[j]));
-      if constexpr (WBITS == 8) {
+      if constexpr (WBITS == 2) {  // four codes per byte, element k in bits 2(k mod 4)
+        uint32_t o = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o |= (uint32_t)(qi[j] & 0x3) << (2 * j);
+        *reinterpret_cast<uint16_t*>(q + (base + c * 8) / 4) = (uint16_t)o;
+      } else if constexpr (WBITS == 8) {
         uint2 o;
         o.x = (qi[0] & 0xFF) | ((qi[1] & 0xFF) << 8) | ((qi[2] & 0xFF) << 16) | ((uint32_t)(qi[3] & 0xFF) << 24);
         o.y = (qi[4] & 0xFF) | ((qi[5] & 0xFF) << 8) | ((qi[6] & 0xFF) << 16) | ((uint32_t)(qi[7] & 0xFF) << 24);
@@ -148,6 +153,8 @@ cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, i
   if (R == 0) return cudaSuccess;
   if (wbits == 8)
     return in_fp32 ? dispatch<8, true>(g, w, R, K, q, s, st) : dispatch<8, false>(g, w, R, K, q, s, st);
+  if (wbits == 2)
+    return in_fp32 ? dispatch<2, true>(g, w, R, K, q, s, st) : dispatch<2, false>(g, w, R, K, q, s, st);
   return in_fp32 ? dispatch<4, true>(g, w, R, K, q, s, st) : dispatch<4, false>(g, w, R, K, q, s, st);
 }
 

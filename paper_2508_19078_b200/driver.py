@@ -72,8 +72,8 @@ class QuantizedModel:
     def __init__(self, shape: ModelShape, device="cuda"):
         self.shape = s = shape
         L, E, H, F, Fs = s.n_layers, s.n_experts, s.hidden, s.ffn, s.shared_ffn
-        qdiv = 2 if s.wbits == 4 else 1
-        qdt = torch.uint8 if s.wbits == 4 else torch.int8
+        qdiv = {2: 4, 4: 2}.get(s.wbits, 1)  # codes per byte
+        qdt = torch.int8 if s.wbits == 8 else torch.uint8
         gh = s.group_size or H
         gf = s.group_size or F
         gfs = s.group_size or (Fs or 1)

@@ -25,6 +25,9 @@ SMALL = {
     "int4_shared": synth.MoEConfig("mid_int4_shared", 2, 256, 16, 4, 192, 384, 4, 64, 0, 1000, synth.BASE_SEED + 11),
     "int8_ragged": synth.MoEConfig("mid_int8", 2, 128, 12, 3, 80, 0, 8, 0, 1, 777, synth.BASE_SEED + 12),
     "int4_e64": synth.MoEConfig("e64_int4", 1, 128, 64, 6, 128, 256, 4, 128, 0, 650, synth.BASE_SEED + 13),
+    # NEXT-3: the paper's bit-2, grouped and per-channel
+    "int2_g64": synth.MoEConfig("int2_g64", 2, 128, 16, 4, 128, 192, 2, 64, 1, 600, synth.BASE_SEED + 14),
+    "int2_pc": synth.MoEConfig("int2_pc", 2, 192, 8, 2, 64, 0, 2, 0, 0, 300, synth.BASE_SEED + 15),
 }
 
 
@@ -54,7 +57,7 @@ def test_quantized_weights_bit_exact(name):
                                   ("down", qm.down_q, qm.down_s)):
                 w = om.master_f32(synth.spec_expert(cfg, l, e, fam))
                 q, s = oracle.quantize(w, cfg.wbits, cfg.group_size)
-                qq = oracle.pack_int4(q) if cfg.wbits == 4 else q
+                qq = oracle.pack(q, cfg.wbits)
                 assert np.array_equal(q_t[l, e].cpu().numpy().view(np.uint8), qq.view(np.uint8)), (l, e, fam)
                 assert np.array_equal(s_t[l, e].cpu().numpy(), s), (l, e, fam)
 
@@ -189,7 +192,7 @@ def test_quantizer_ties_and_extremes_bit_exact():
     import paper_2508_19078_b200 as F
     gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "quantize_examples.json")))
     rng = np.random.default_rng(11)
-    for wbits in (4, 8):
+    for wbits in (2, 4, 8):
         qmax = (1 << (wbits - 1)) - 1
         rows = []
         for c in gold["cases"]:
@@ -203,10 +206,10 @@ def test_quantizer_ties_and_extremes_bit_exact():
         w = np.stack(rows)
         q_ref, s_ref = oracle.quantize(w, wbits, 64)
         tw = torch.from_numpy(w).cuda()
-        q = torch.empty(w.shape[0], 64 // (2 if wbits == 4 else 1), dtype=torch.uint8, device="cuda")
+        q = torch.empty(w.shape[0], 64 * wbits // 8, dtype=torch.uint8, device="cuda")
         s = torch.empty(w.shape[0], 1, dtype=torch.float32, device="cuda")
         F.quantize_weights(tw, wbits, 64, q, s)
-        qq = oracle.pack_int4(q_ref) if wbits == 4 else q_ref.view(np.uint8)
+        qq = oracle.pack(q_ref, wbits).view(np.uint8)
         assert np.array_equal(q.cpu().numpy(), qq), wbits
         assert np.array_equal(s.cpu().numpy(), s_ref), wbits
 
@@ -214,7 +217,8 @@ def test_quantizer_ties_and_extremes_bit_exact():
 def test_quantizer_direct_bit_exact():
     import paper_2508_19078_b200 as F
     rng = np.random.default_rng(3)
-    for wbits, g, dt in [(8, 0, "bf16"), (4, 128, "bf16"), (4, 64, "f32"), (8, 64, "f32"), (4, 0, "bf16")]:
+    for wbits, g, dt in [(8, 0, "bf16"), (4, 128, "bf16"), (4, 64, "f32"), (8, 64, "f32"), (4, 0, "bf16"),
+                         (2, 128, "bf16"), (2, 0, "f32"), (2, 64, "bf16")]:
         R, K = 37, 640
         w = (rng.standard_normal((R, K)) * rng.uniform(0.001, 10, (R, 1))).astype(np.float32)
         w[5] = 0
@@ -222,9 +226,9 @@ def test_quantizer_direct_bit_exact():
             w = oracle.bf16_round(w).astype(np.float32)
         q_ref, s_ref = oracle.quantize(w, wbits, g)
         tw = torch.from_numpy(w).cuda().to(torch.bfloat16 if dt == "bf16" else torch.float32)
-        q = torch.empty(R, K // (2 if wbits == 4 else 1), dtype=torch.uint8, device="cuda")
+        q = torch.empty(R, K * wbits // 8, dtype=torch.uint8, device="cuda")
         s = torch.empty(R, K // (g or K), dtype=torch.float32, device="cuda")
         F.quantize_weights(tw, wbits, g, q, s)
-        qq = oracle.pack_int4(q_ref) if wbits == 4 else q_ref.view(np.uint8)
+        qq = oracle.pack(q_ref, wbits).view(np.uint8)
         assert np.array_equal(q.cpu().numpy(), qq), (wbits, g, dt)
         assert np.array_equal(s.cpu().numpy(), s_ref), (wbits, g, dt)
