@@ -57,6 +57,8 @@ def lib():
         L.orc_quantize.restype = _I
         L.orc_pack_int4.argtypes = [_I64, _I64, _P, _P]
         L.orc_pack_int2.argtypes = [_I64, _I64, _P, _P]
+        L.orc_attention_hist.argtypes = [_I64, _I, _P, _P, _P]
+        L.orc_attention_hist.restype = None
         L.orc_router.argtypes = [_I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]
         L.orc_router.restype = _I
         L.orc_permute.argtypes = [_I64, _I, _I, _P, _P, _P, _P, _P]
@@ -213,6 +215,16 @@ def compact_tokens(x, wr, remap, gate, up, down, shared=None, *, k: int, norm: i
     if rc:
         raise ValueError(f"orc_compact_tokens failed ({rc})")
     return y, ids, w, z, m
+
+
+def attention_hist(ids, attn, E: int, A=None):
+    """O13: A [E] int64 += Σ over live picks of RNE(a_t·2^24) (α_e = A_e / (2^24·T) = f_e·ā_e)."""
+    ids = _c(ids, np.int32)
+    T, k = ids.shape
+    a = _c(attn, np.float32)
+    A = np.zeros(E, np.int64) if A is None else A
+    lib().orc_attention_hist(T, k, ids.ctypes.data, a.ctypes.data, A.ctypes.data)
+    return A
 
 
 def layer_budget(hist, T: int, B_non: int, n_non=None):

@@ -400,6 +400,24 @@ int orc_compact_tokens(int64_t n, int H, int Er, int k, int S, int F, int Fs, in
 }
 
 /* ----------------------------------------------------------------------------
+ * O13 (NEXT-3). Attention-weighted importance of eq.(2): α_e = f_e·ā_e,
+ * ā_e = "the average attention value of tokens assigned to expert e", f_e = |D_e|/T
+ * (P:296-298), so α_e = (1/T) Σ_{t∈D_e} a_t.  Reading R15: a_t is the per-token
+ * attention value the model's attention layer supplies (the path has none); the sum is
+ * kept like the histogram, as exact integers in fixed point:
+ *   A_e += RNE(a_t · 2^24)   for every live pick (t, j) with S_tj = e
+ * so α_e = A_e / (2^24 · T) up to the 2^-25 rounding of each a_t, and A is order-free.
+ * ids [T][k] (-1 = empty pick), attn [T] fp32 (>= 0), A [E] accumulated.
+ * -------------------------------------------------------------------------- */
+void orc_attention_hist(int64_t T, int k, const int32_t* ids, const float* attn, int64_t* A) {
+  for (int64_t t = 0; t < T; ++t) {
+    const int64_t a = (int64_t)nearbyint((double)attn[t] * 16777216.0);
+    for (int j = 0; j < k; ++j)
+      if (ids[t * k + j] >= 0) A[ids[t * k + j]] += a;
+  }
+}
+
+/* ----------------------------------------------------------------------------
  * O9. Adaptive expert layer size, eq.(1), reading R9:
  *   f_l[e] = hist[l][e] / T
  *   v_l    = (1/E) Σ_e (f_l[e] - mean_l)^2       (population variance)

@@ -35,7 +35,7 @@ COL0_ONE = 1
 ROW0_ZERO = 2
 COL0_C0 = 4
 
-KIND_X, KIND_ROUTER, KIND_GATE, KIND_UP, KIND_DOWN, KIND_MASTER_F32 = 1, 2, 3, 4, 5, 6
+KIND_X, KIND_ROUTER, KIND_GATE, KIND_UP, KIND_DOWN, KIND_MASTER_F32, KIND_ATTN = 1, 2, 3, 4, 5, 6, 7
 SHARED_SLOT = 1023
 BASE_SEED = 0x250819078
 
@@ -109,6 +109,12 @@ class Spec:
 
 def spec_x(cfg: MoEConfig):
     return Spec(cfg.tokens, cfg.hidden, cfg.seed, stream_id(KIND_X, 0, 0), scale_c(1.0), COL0_ONE, 0.0)
+
+
+def spec_attn(cfg: MoEConfig, layer: int):
+    """Per-token attention values a_t (NEXT-3, α = f·ā): |N(0, 1)| -> take abs() of the fp32 output.
+    The path has no attention layers; these stand in for the values the model's attention supplies."""
+    return Spec(cfg.tokens, 1, cfg.seed, stream_id(KIND_ATTN, layer, 0), scale_c(1.0), 0, 0.0)
 
 
 def spec_router(cfg: MoEConfig, layer: int):
