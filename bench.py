@@ -151,6 +151,8 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=32)  # oracle sample: ~10 s of host CPU work
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--clusters", type=int, default=0)
+    ap.add_argument("--alpha", default="f", choices=["f", "attn"],
+                    help="merge importance: activation frequency (BASELINE config) or f·ā with synthetic attention")
     ap.add_argument("--wbits", type=int, default=0, choices=[0, 2, 4, 8],
                     help="override the config's bit level (2 = the paper's bit-2 ablation, NEXT-3)")
     ap.add_argument("--error-tokens", type=int, default=8192,
@@ -202,6 +204,8 @@ def main():
     alpha = torch.empty(L, E, dtype=torch.float32, device="cuda")
     alpha_host = torch.empty(L, E, dtype=torch.float32).pin_memory()
     hist_host = torch.empty(L, E, dtype=torch.int64).pin_memory()
+    ahist_host = torch.empty(L, E, dtype=torch.int64).pin_memory()
+    attn = synthetic.attention_values(cfg, t0, T) if args.alpha == "attn" else None
     merged = None
     uid = F.Comm.unique_id() if rank == 0 else None
     if world > 1:
@@ -224,15 +228,21 @@ def main():
             feats, _, _ = expert_features_model(masters, d_feat)
             ev_feat.record(stream)
         qm.quantize_from(masters)                                   # a0
-        prof.run(qm, x_in)                                          # a1-a6 (hist zeroed first)
+        prof.run(qm, x_in, attn=attn)                               # a1-a6 (hist zeroed first)
         comm.reduce_stats(prof.hist)                                # a7
+        if attn is not None:                                        # NEXT-3: Σ_{t∈D_e} a_t, fixed point
+            comm.reduce_stats(prof.ahist)
+            ahist_host.copy_(prof.ahist, non_blocking=True)
         if args.clustering == "pca":                                # §5.2 C2: K-Means from the reduced counts
             stream.wait_event(ev_feat)
             cluster_of = cluster_model(feats, prof.hist, C)
         hist_host.copy_(prof.hist, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         h = hist_host.numpy()
-        alpha_host.copy_(torch.from_numpy((h / float(T_total)).astype(np.float32)))  # f
+        if attn is None:
+            alpha_host.copy_(torch.from_numpy((h / float(T_total)).astype(np.float32)))  # α = f
+        else:  # α = f·ā = Σ_{t∈D_e} a_t / T (eq.(2); R15)
+            alpha_host.copy_(torch.from_numpy((ahist_host.numpy() / (16777216.0 * T_total)).astype(np.float32)))
         Cl, over = budgets(h, T_total, C * L)                       # a8-pre, eq.(1)
         budget_out["C"] = Cl
         alpha.copy_(alpha_host, non_blocking=True)
@@ -315,7 +325,7 @@ def main():
             outs.append(pr.run(mdl, x[:n_err]).clone())
             del pr
         merr = {"value": float(F.output_error(outs[1], outs[0]).item()), "tokens": n_err,
-                "clusters_per_layer": C, "alpha": "f", "clustering": args.clustering,
+                "clusters_per_layer": C, "alpha": args.alpha, "clustering": args.clustering,
                 "what": "mean cosine distance of final token outputs, merged vs original bf16 model (P:686-689)"}
         del comp, outs
 

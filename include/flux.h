@@ -201,6 +201,19 @@ flux_status flux_cluster_experts(int32_t n_layers, int32_t n_experts, int32_t d,
                                  int32_t max_iter, int32_t* cluster_of, int32_t* iterations, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * NEXT-3: attention-weighted importance α_e = f_e·ā_e of eq.(2), reading R15.
+ * ------------------------------------------------------------------------- */
+/* attn_hist[e] += Σ over live picks (t, j) with ids[t][j] == e of RNE(attn[t]·2^24), int64.
+ * ā_e = the average attention value of the tokens assigned to e, f_e = count_e / T, so
+ * α_e = f_e·ā_e = attn_hist[e] / (2^24·T): an integer statistic, exact, order-free and
+ * additive over ranks (reduce it with flux_reduce_stats like the histogram).
+ * ids: device int32 [T][top_k] (flux_profile_layer's topk_ids; -1 = folded pick, skipped);
+ * attn: device fp32 [T], 0 <= a_t < 2^30 (the per-token attention value of the model's
+ * attention layer — outside this path); attn_hist: device int64 [n_experts], accumulated. */
+flux_status flux_attention_hist(int64_t T, int32_t top_k, int32_t n_experts, const int32_t* ids, const float* attn,
+                                int64_t* attn_hist, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Statistics all-reduce over the GPUs of one box (NCCL over NVLink/NVSwitch).
  * The counts are additive integers, so the reduced histogram equals the
  * single-GPU histogram of the union of the shards bit for bit.

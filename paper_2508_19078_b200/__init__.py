@@ -71,6 +71,7 @@ def _lib():
         L.flux_merge_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
         L.flux_quantize_weights.argtypes = [I32, I32, ctypes.c_int, P, I64, I64, P, P, P]
         L.flux_compact_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
+        L.flux_attention_hist.argtypes = [I64, I32, I32, P, P, P, P]
         L.flux_output_error_workspace.argtypes = []
         L.flux_output_error_workspace.restype = SZ
         L.flux_output_error.argtypes = [I64, I32, P, P, P, P, SZ, P]
@@ -85,6 +86,7 @@ def _lib():
         L.flux_comm_destroy.argtypes = [P]
         for f in ("flux_profile_layer", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
                   "flux_expert_features", "flux_cluster_experts", "flux_compact_experts", "flux_output_error",
+                  "flux_attention_hist",
                   "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
             getattr(L, f).restype = ctypes.c_int
         L.flux_timing_enable.argtypes = [ctypes.c_int]
@@ -173,6 +175,13 @@ def compact_experts(experts, cluster_of, alpha, n_clusters: int, compact, remap=
     st = _lib().flux_compact_experts(dt, E, numel, _ptr(experts), _ptr(cluster_of), _ptr(alpha), n_clusters,
                                      _ptr(compact), _ptr(remap), _stream(stream))
     _check(st, "flux_compact_experts")
+
+
+def attention_hist(ids, attn, n_experts: int, out, stream=None):
+    """NEXT-3: out int64 [E] += fixed-point attention-weighted counts (α = f·ā = out / (2^24·T))."""
+    T, k = ids.shape
+    st = _lib().flux_attention_hist(T, k, n_experts, _ptr(ids), _ptr(attn), _ptr(out), _stream(stream))
+    _check(st, "flux_attention_hist")
 
 
 def output_error(a, b, result=None, ws=None, stream=None):

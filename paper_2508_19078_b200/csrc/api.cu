@@ -527,6 +527,19 @@ flux_status flux_compact_experts(flux_dtype dtype, int32_t n_experts, int64_t nu
                                   compact, remap, (cudaStream_t)stream, 1));
 }
 
+flux_status flux_attention_hist(int64_t T, int32_t top_k, int32_t n_experts, const int32_t* ids, const float* attn,
+                                int64_t* attn_hist, void* stream) {
+  if (T < 0 || top_k < 1 || top_k > 8 || n_experts < 1 || n_experts > 1024) return FLUX_E_INVALID;
+  if (T == 0) return FLUX_OK;
+  if (!ids || !attn || !attn_hist) return FLUX_E_INVALID;
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  KernelTimer kt(K_ATTN_HIST, (cudaStream_t)stream);
+  cudaError_t e = launch_attention_hist(T, top_k, n_experts, ids, attn, attn_hist, (cudaStream_t)stream);
+  if (e != cudaSuccess) set_last_error("attention_hist", e);
+  return cuda_status(e);
+}
+
 size_t flux_output_error_workspace(void) { return cosine_workspace(); }
 
 flux_status flux_output_error(int64_t T, int32_t hidden, const void* a, const void* b, double* result, void* ws,

@@ -1,4 +1,6 @@
-// eval.cu — the paper's merge-quality measure (NEXT-2): "the average cosine distance between the
+// eval.cu — statistics beside the layer forward:
+//  * attention_hist_kernel (NEXT-3): the attention-weighted activation counts of eq.(2)'s α = f·ā;
+//  * cosine_distance_kernel (NEXT-2): the paper's merge-quality measure, "the average cosine distance between the
 // final token embeddings from the MoE model with merged experts and those from the original full
 // model":  err = (1/T) Σ_t (1 - a_t·b_t / (|a_t| |b_t|)).
 //
@@ -63,7 +65,36 @@ __global__ void __launch_bounds__(kCosThreads) cosine_distance_kernel(int64_t T,
     *ticket = 0;  // ready for the next call
   }
 }
+
+// NEXT-3 (eq.(2) α = f·ā, reading R15): A_e += RNE(a_t · 2^24) over the live picks of
+// every token.  Integer sums: exact and order-free (deterministic and identical under any split of
+// the tokens, like the histogram).  Per-CTA shared-memory accumulators, one global atomic per expert.
+__global__ void __launch_bounds__(256) attention_hist_kernel(int64_t T, int k, int E, const int32_t* __restrict__ ids,
+                                                             const float* __restrict__ attn,
+                                                             unsigned long long* __restrict__ A) {
+  __shared__ unsigned long long acc[1024];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) acc[e] = 0ull;
+  __syncthreads();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    const long long a = __double2ll_rn((double)__ldg(&attn[t]) * 16777216.0);  // exact product, RNE
+    for (int j = 0; j < k; ++j) {
+      const int e = __ldg(&ids[t * k + j]);
+      if (e >= 0) atomicAdd(&acc[e], (unsigned long long)a);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (acc[e]) atomicAdd(&A[e], acc[e]);
+}
 }  // namespace
+
+cudaError_t launch_attention_hist(int64_t T, int k, int E, const int32_t* ids, const float* attn, int64_t* A,
+                                  cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((T + 255) / 256, kNumSMs * 2));
+  attention_hist_kernel<<<grid, 256, 0, st>>>(T, k, E, ids, attn, reinterpret_cast<unsigned long long*>(A));
+  return cudaGetLastError();
+}
 
 size_t cosine_workspace() { return (kCosBlocks + 2) * sizeof(double); }
 

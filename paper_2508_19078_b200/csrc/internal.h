@@ -23,7 +23,7 @@ inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_O
 // ---------------------------------------------------------------- per-kernel timing (timing.cpp)
 enum KernelKind {
   K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_SCHEDULE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
-  K_GEMM_DN_SH_COMBINE, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, K_COSINE, FLUX_NUM_KERNELS
+  K_GEMM_DN_SH_COMBINE, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, K_COSINE, K_ATTN_HIST, FLUX_NUM_KERNELS
 };
 // RAII: counts one launch; when timing is enabled records CUDA events around it on `st`.
 class KernelTimer {
@@ -50,6 +50,8 @@ cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, i
 cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
                          const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st, int compact = 0);
 // output error of a merged model: mean over tokens of 1 - cos(a_t, b_t)
+cudaError_t launch_attention_hist(int64_t T, int k, int E, const int32_t* ids, const float* attn, int64_t* A,
+                                  cudaStream_t st);
 size_t cosine_workspace();
 cudaError_t launch_cosine_distance(int64_t T, int H, const void* a, const void* b, double* ws, double* out,
                                    cudaStream_t st);

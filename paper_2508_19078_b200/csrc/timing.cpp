@@ -15,7 +15,7 @@ static const char* kernel_name(int kind) {
   static const char* names[FLUX_NUM_KERNELS] = {"quantize", "dequant", "router", "schedule", "scatter",
                                                 "gemm_gate_up", "gemm_down", "combine", "merge",
                                                 "gemm_down_shared_combine", "gram", "gram_reduce", "eig",
-                                                "kmeans", "cosine_distance"};
+                                                "kmeans", "cosine_distance", "attention_hist"};
   return kind >= 0 && kind < FLUX_NUM_KERNELS ? names[kind] : "?";
 }
 namespace {

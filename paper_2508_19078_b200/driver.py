@@ -17,7 +17,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import (FLUX_OK, Comm, LayerOut, QLayer, cluster_experts, compact_experts, expert_features, layer_budget,
+from . import (FLUX_OK, Comm, LayerOut, QLayer, attention_hist, cluster_experts, compact_experts, expert_features,
+               layer_budget,
                make_cfg, merge_experts, output_error, profile_layer, profile_layer_workspace, quantize_weights)
 
 
@@ -180,19 +181,30 @@ class Profiler:
         self.token_index = torch.empty(L, T * k, dtype=torch.int32, device=device) if with_de else None
         E_r = s.n_router or E  # the router scores the original experts under gate re-routing
         self.logits = torch.empty(L, T, E_r, dtype=torch.float32, device=device) if with_logits else None
+        self.ahist = None  # [L][E] int64 attention-weighted counts when run(attn=...) is used (NEXT-3)
 
     def out(self, l: int) -> LayerOut:
         p = lambda t: None if t is None else t[l].data_ptr()  # noqa: E731
         return LayerOut(self.y[l % 2].data_ptr(), p(self.ids), p(self.w), p(self.hist), p(self.offsets),
                         p(self.token_index), p(self.logits))
 
-    def run(self, qm: QuantizedModel, x: torch.Tensor, stream=None, on_layer=None, zero_hist: bool = True):
-        """Profile x [T][H] (bf16, device) through every layer; returns the last layer's y."""
+    def run(self, qm: QuantizedModel, x: torch.Tensor, stream=None, on_layer=None, zero_hist: bool = True,
+            attn: torch.Tensor | None = None):
+        """Profile x [T][H] (bf16, device) through every layer; returns the last layer's y.
+        attn [L][T] fp32 (optional, NEXT-3): per-token attention values -> self.ahist, the fixed-point
+        attention-weighted counts of eq.(2)'s α = f·ā (flux_attention_hist)."""
         if zero_hist:
             self.hist.zero_()
+        if attn is not None:
+            if self.ahist is None:
+                self.ahist = torch.zeros_like(self.hist)
+            elif zero_hist:
+                self.ahist.zero_()
         cur = x
         for l in range(self.shape.n_layers):
             profile_layer(self.cfg, qm.qlayer(l), cur, None, self.T, self.out(l), self.ws, stream)
+            if attn is not None:
+                attention_hist(self.ids[l], attn[l], self.shape.n_experts, self.ahist[l], stream)
             cur = self.y[l % 2]
             if on_layer is not None:
                 on_layer(l, cur)

@@ -40,3 +40,12 @@ def tokens(cfg, t0: int, n: int, device="cuda", out=None) -> torch.Tensor:
 def cluster_assignment(cfg, n_clusters: int, n_tuning: int = 0) -> np.ndarray:
     """cluster_of [L][E] (an input of the merge; see synth.cluster_assignment)."""
     return synth.cluster_assignment(cfg, n_clusters, n_tuning)
+
+
+def attention_values(cfg, t0: int, n: int, device="cuda") -> torch.Tensor:
+    """Per-layer, per-token attention values a_t >= 0 [L][n] fp32 for tokens [t0, t0+n) (synth.spec_attn;
+    NEXT-3's α = f·ā needs them from the model's attention layers, which this path does not have)."""
+    out = torch.empty(cfg.n_layers, n, 1, dtype=torch.float32, device=device)
+    for l in range(cfg.n_layers):
+        synth.gpu_fill(out[l], synth.spec_attn(cfg, l), row0=t0)
+    return out.abs_().view(cfg.n_layers, n)

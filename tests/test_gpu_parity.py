@@ -232,3 +232,45 @@ def test_quantizer_direct_bit_exact():
         qq = oracle.pack(q_ref, wbits).view(np.uint8)
         assert np.array_equal(q.cpu().numpy(), qq), (wbits, g, dt)
         assert np.array_equal(s.cpu().numpy(), s_ref), (wbits, g, dt)
+
+
+def test_attention_hist_unit_bit_exact():
+    """NEXT-3 (α = f·ā, R15): integer fixed-point sums, so the GPU must equal the oracle bit for bit,
+    including empty (-1) picks and ties in the 2^-24 rounding."""
+    import paper_2508_19078_b200 as F
+    rng = np.random.default_rng(21)
+    for T, E, k in ((1, 4, 2), (3000, 64, 6), (70001, 128, 8), (5000, 16, 4)):
+        ids = np.stack([rng.choice(E, size=k, replace=False) for _ in range(T)]).astype(np.int32)
+        ids[rng.random((T, k)) < 0.1] = -1
+        a = np.abs(rng.standard_normal(T)).astype(np.float32)
+        a[: T // 10] = (rng.integers(0, 64, T // 10) * 2.0 ** -25).astype(np.float32)  # exact ties
+        want = oracle.attention_hist(ids, a, E)
+        got = torch.zeros(E, dtype=torch.int64, device="cuda")
+        F.attention_hist(torch.from_numpy(ids).cuda(), torch.from_numpy(a).cuda(), E, got)
+        assert np.array_equal(got.cpu().numpy(), want), (T, E, k)
+
+
+@pytest.mark.parametrize("name", ["toy", "int4_shared"])
+def test_attention_weighted_alpha_through_the_profile(name):
+    """Per layer A_e from the profiled routing: equal to the oracle's (its own routing and its own copy
+    of the attention values) where every token routes identically, and always consistent with the
+    GPU's own picks."""
+    import paper_2508_19078_b200 as F  # noqa: F401
+    from paper_2508_19078_b200 import synthetic
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
+    cfg = SMALL[name]
+    T = cfg.tokens
+    qm = QuantizedModel(ModelShape.of(cfg))
+    qm.quantize_from(synthetic.master_weights(cfg))
+    prof = Profiler(ModelShape.of(cfg), T)
+    attn = synthetic.attention_values(cfg, 0, T)
+    prof.run(qm, synthetic.tokens(cfg, 0, T), attn=attn)
+    torch.cuda.synchronize()
+    ref = om.profile_all(cfg)
+    for l in range(cfg.n_layers):
+        a_ref = np.abs(synth.cpu_matrix(synth.spec_attn(cfg, l), dtype="f32")[:, 0])
+        ids_gpu = prof.ids[l].cpu().numpy()
+        A_gpu = prof.ahist[l].cpu().numpy()
+        assert np.array_equal(A_gpu, oracle.attention_hist(ids_gpu, a_ref, cfg.n_experts))
+        if np.array_equal(np.sort(ids_gpu, 1), np.sort(ref[l]["ids"], 1)):
+            assert np.array_equal(A_gpu, oracle.attention_hist(ref[l]["ids"], a_ref, cfg.n_experts))
