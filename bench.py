@@ -151,6 +151,8 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=32)  # oracle sample: ~10 s of host CPU work
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--clusters", type=int, default=0)
+    ap.add_argument("--rounds", type=int, default=2,
+                    help="NEXT-4: serial vs stale-profiling participant rounds measured after the run (0 = skip)")
     ap.add_argument("--alpha", default="f", choices=["f", "attn"],
                     help="merge importance: activation frequency (BASELINE config) or f·ā with synthetic attention")
     ap.add_argument("--wbits", type=int, default=0, choices=[0, 2, 4, 8],
@@ -329,6 +331,26 @@ def main():
                 "what": "mean cosine distance of final token outputs, merged vs original bf16 model (P:686-689)"}
         del comp, outs
 
+    # ---- NEXT-4 stale profiling (not part of the timed step): participant rounds, serial (Fig. 7a) vs
+    #      stale (Fig. 7b), each round = profile + merge into the compact model + its forward over the
+    #      local fine-tuning tokens (the first quarter of x); CUDA events on the round's streams
+    stale = None
+    if args.rounds > 0 and world == 1:
+        from paper_2508_19078_b200.rounds import Participant
+        part = Participant(masters, x, x[: max(1, T // 4)], comm, C, T_total, clustering=args.clustering,
+                           seeded_cluster_of=cluster_of)
+        part.round_serial()  # warm-up; leaves f^r for the first stale round
+        ser = [part.round_serial() for _ in range(args.rounds)]
+        stl = [part.round_stale() for _ in range(args.rounds)]
+        med = lambda rs, k: statistics.median(r[k] for r in rs)  # noqa: E731
+        stale = {"serial_round_ms": med(ser, "round_ms"), "serial_ft_start_ms": med(ser, "ft_start_ms"),
+                 "stale_round_ms": med(stl, "round_ms"), "stale_ft_start_ms": med(stl, "ft_start_ms"),
+                 "stale_profile_done_ms": med(stl, "profile_done_ms"), "rounds": args.rounds,
+                 "finetune_tokens": int(max(1, T // 4)),
+                 "what": "participant round = profile + merge (compact model) + compact-model forward over the "
+                         "fine-tuning tokens; stale = merge with f^(r-1) at once, profile on a low-priority stream"}
+        del part
+
     if rank == 0:
         peaks, peak_src = load_peaks()
         value = T_total * args.steps / (ms / 1000.0)
@@ -360,6 +382,7 @@ def main():
             "kernels": kernels,
             "budget_C": [int(c) for c in budget_out.get("C", [])][:4],
             "merge_output_error": merr,
+            "stale_profiling": stale,
         }
         if world == 1 and not args.no_cpu_baseline:
             r, threads, sample, dt = oracle_rate(cfg, args.ref_tokens, args.ref_layers, T)

@@ -142,7 +142,7 @@ def dense_model(m: MasterWeights) -> DenseWeights:
 
 
 def compact_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tensor, n_clusters: int,
-                  n_tuning: int = 0, stream=None) -> DenseWeights:
+                  n_tuning: int = 0, stream=None, out: DenseWeights | None = None) -> DenseWeights:
     """NEXT-2: the compact model (§7 "Customized MoE construction" + "Gate re-routing"): per layer the slots
     [n_tuning tuning experts (ascending id), n_clusters eq.(2) merges] of every weight family
     (flux_compact_experts) and the remap of the router's picks.  Every layer must keep n_tuning experts."""
@@ -150,10 +150,13 @@ def compact_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tenso
     L, E, F, H = s.n_layers, s.n_experts, s.ffn, s.hidden
     S = n_tuning + n_clusters
     dev = m.gate.device
-    gate = torch.empty(L, S, F, H, dtype=m.gate.dtype, device=dev)
-    up = torch.empty_like(gate)
-    down = torch.empty(L, S, H, F, dtype=m.gate.dtype, device=dev)
-    remap = torch.empty(L, E, dtype=torch.int32, device=dev)
+    if out is not None and out.gate.shape[1] == S:  # reuse the buffers of a previous round
+        gate, up, down, remap = out.gate, out.up, out.down, out.remap
+    else:
+        gate = torch.empty(L, S, F, H, dtype=m.gate.dtype, device=dev)
+        up = torch.empty_like(gate)
+        down = torch.empty(L, S, H, F, dtype=m.gate.dtype, device=dev)
+        remap = torch.empty(L, E, dtype=torch.int32, device=dev)
     for l in range(L):
         compact_experts(m.gate[l].view(E, -1), cluster_of[l], alpha[l], n_clusters, gate[l].view(S, -1), remap[l],
                         stream)
