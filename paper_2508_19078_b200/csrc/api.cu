@@ -45,8 +45,9 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype,
   return r == CUDA_SUCCESS;
 }
 
-static bool tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-  return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, cols * 2, 64, box_rows,
+static bool tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                      uint64_t ld = 0 /* row length in elements, default cols */) {
+  return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, (ld ? ld : cols) * 2, 64, box_rows,
                       CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
@@ -121,6 +122,11 @@ struct WsPlan {
   size_t total;
 };
 int pad128(int v) { return (v + 127) / 128 * 128; }
+// Row length (elements) of the bf16 buffers whose K is F or F_s (act, act_sh, the down-projection B
+// operands): padded to 64 elements so every row starts on a 128-byte line.  F = 688 (LLaMA shape)
+// has 1376-byte rows, and every 128-byte TMA row segment of an unpadded buffer straddles two lines.
+// The tensor maps keep the logical width F, so the pad columns are never read (no zeroing needed).
+int pad64(int v) { return (v + 63) / 64 * 64; }
 
 WsPlan plan(const flux_moe_cfg& c, int64_t T) {
   Layout L;
@@ -142,15 +148,15 @@ WsPlan plan(const flux_moe_cfg& c, int64_t T) {
   // x_perm (routed A rows materialised by K2) unless the GEMM gathers them; y_perm always.
   p.x_perm = L.take(gather_routed_a() ? 0 : 2ull * Tk * c.hidden);
   p.y_perm = L.take(2ull * Tk * c.hidden);
-  p.act = L.take(2ull * Tk * c.ffn);
-  p.act_sh = L.take(2ull * T * c.shared_ffn);
+  p.act = L.take(2ull * Tk * pad64(c.ffn));
+  p.act_sh = L.take(2ull * T * pad64(c.shared_ffn));
   p.sh_sched = L.take(4 * sizeof(int32_t));  // sched_sh[2], row0_sh[1], rows_sh[1]
   p.y_sh = L.take(c.shared_ffn && !fused_combine() ? 2ull * T * c.hidden : 0);
   const size_t pass = dequant_pass(c, T) ? 1 : 0;  // bf16 B operands only for the separate-pass path
   p.wgu_r = L.take(pass * 2ull * c.n_experts * 2 * pad128(c.ffn) * c.hidden);
-  p.wdn_r = L.take(pass * 2ull * c.n_experts * c.hidden * c.ffn);
+  p.wdn_r = L.take(pass * 2ull * c.n_experts * c.hidden * pad64(c.ffn));
   p.wgu_s = L.take(pass * 2ull * 2 * pad128(c.shared_ffn) * c.hidden);
-  p.wdn_s = L.take(pass * 2ull * c.hidden * c.shared_ffn);
+  p.wdn_s = L.take(pass * 2ull * c.hidden * pad64(c.shared_ffn));
   p.total = L.off;
   return p;
 }
@@ -230,6 +236,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   uint8_t* W = (uint8_t*)ws;
   const int H = c.hidden, F = c.ffn, Fs = c.shared_ffn, E = c.n_experts, k = c.top_k;
   const int Fp = pad128(F), Fsp = pad128(Fs);
+  const int Fld = pad64(F), Fsld = pad64(Fs);  // row lengths of act / act_sh / the down B operands
   const bool per_channel = c.group_size == 0 && quantized;  // per-channel scales applied in the epilogue
   const int E_r = c.n_router > 0 ? c.n_router : E;           // experts the router scores
   const int g_h = per_channel ? H : c.group_size, g_f = per_channel ? F : c.group_size,
@@ -263,16 +270,16 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   if (pass) {
   KernelTimer kt(K_DEQUANT, s);
   e = launch_dequant(c.wbits, (const uint8_t*)w->gate_q, w->gate_s, (const uint8_t*)w->up_q, w->up_s, E, F, H, Fp, 1,
-                     g_h, per_channel, wgu_r, s);
+                     g_h, per_channel, H, wgu_r, s);
   if (e == cudaSuccess)
     e = launch_dequant(c.wbits, (const uint8_t*)w->down_q, w->down_s, nullptr, nullptr, E, H, F, 0, 0, g_f,
-                       per_channel, wdn_r, s);
+                       per_channel, Fld, wdn_r, s);
   if (e == cudaSuccess && sh)
     e = launch_dequant(c.wbits, (const uint8_t*)w->sh_gate_q, w->sh_gate_s, (const uint8_t*)w->sh_up_q, w->sh_up_s,
-                       1, Fs, H, Fsp, 1, g_h, per_channel, wgu_s, s);
+                       1, Fs, H, Fsp, 1, g_h, per_channel, H, wgu_s, s);
   if (e == cudaSuccess && sh)
     e = launch_dequant(c.wbits, (const uint8_t*)w->sh_down_q, w->sh_down_s, nullptr, nullptr, 1, H, Fs, 0, 0, g_fs,
-                       per_channel, wdn_s, s);
+                       per_channel, Fsld, wdn_s, s);
   }
   if (e != cudaSuccess) { set_last_error("dequant", e); return FLUX_E_CUDA; }
 
@@ -343,8 +350,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.cs1_s = per_channel ? w->sh_up_s : nullptr;
   ga.out_r = act;
   ga.out_s = act_sh;
-  ga.ld_r = F;
-  ga.ld_s = Fs;
+  ga.ld_r = Fld;
+  ga.ld_s = Fsld;
   ga.grid = kNumSMs;
   ga.bm = sa.gemm_bm;
   ga.gather_idx = gather_a ? token_index : nullptr;
@@ -395,8 +402,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
       KernelTimer kt(K_GEMM_GU, s);
       if ((e = launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s)) != cudaSuccess) { set_last_error("gemm_gate_up", e); return FLUX_E_CUDA; }
     }
-    if (!tmap_bf16(&a_r, act, Tk, F, 128) || !tmap_bf16(&b_r, wdn_r, (uint64_t)E * H, F, bbox) ||
-        (sh && (!tmap_bf16(&a_s, act_sh, T, Fs, 128) || !tmap_bf16(&b_s, wdn_s, H, Fs, bbox)))) {
+    if (!tmap_bf16(&a_r, act, Tk, F, 128, Fld) || !tmap_bf16(&b_r, wdn_r, (uint64_t)E * H, F, bbox, Fld) ||
+        (sh && (!tmap_bf16(&a_s, act_sh, T, Fs, 128, Fsld) || !tmap_bf16(&b_s, wdn_s, H, Fs, bbox, Fsld)))) {
       set_last_error("down tensor maps", cudaErrorInvalidValue);
       return FLUX_E_CUDA;
     }
@@ -440,8 +447,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
       if ((e = launch_gemm_q(EPI_SWIGLU, a_r, a_s, q_r0, q_r1, q_s0, q_s1, qa, s)) != cudaSuccess) { set_last_error("gemm_gate_up", e); return FLUX_E_CUDA; }
     }
     // down
-    if (!tmap_bf16(&a_r, act, Tk, F, 128) || !tmap_u8(&q_r0, w->down_q, (uint64_t)E * H, Fq, qb) ||
-        (sh && (!tmap_bf16(&a_s, act_sh, T, Fs, 128) || !tmap_u8(&q_s0, w->sh_down_q, H, Fsq, qb)))) {
+    if (!tmap_bf16(&a_r, act, Tk, F, 128, Fld) || !tmap_u8(&q_r0, w->down_q, (uint64_t)E * H, Fq, qb) ||
+        (sh && (!tmap_bf16(&a_s, act_sh, T, Fs, 128, Fsld) || !tmap_u8(&q_s0, w->sh_down_q, H, Fsq, qb)))) {
       set_last_error("down tensor maps", cudaErrorInvalidValue);
       return FLUX_E_CUDA;
     }

@@ -160,7 +160,7 @@ template <int WBITS>
 __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict__ q0, const float* __restrict__ s0,
                                                       const uint8_t* __restrict__ q1, const float* __restrict__ s1,
                                                       int G, int N, int K, int Fp, int interleave, int gsz,
-                                                      int per_channel, uint4* __restrict__ out) {
+                                                      int per_channel, int ldo, uint4* __restrict__ out) {
   // one warp per output row; lanes walk the row in 8-element (16-byte) vectors
   const int64_t rows_out = interleave ? 2LL * Fp : N;
   const int64_t n_rows = (int64_t)G * rows_out;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
       src_row = blk * 128 + (w & 127);
       if (w >= 128) { q = q1; s = s1; }
     }
-    uint4* dst = out + orow * vec_per_row;
+    uint4* dst = out + orow * (ldo / 8);  // output rows padded to ldo elements (128-B aligned rows)
     if (src_row >= N) {  // padding rows of the interleaved layout
       for (int v = lane; v < vec_per_row; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
       continue;
@@ -238,20 +238,20 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
 }  // namespace
 
 cudaError_t launch_dequant(int wbits, const uint8_t* q0, const float* s0, const uint8_t* q1, const float* s1, int G,
-                           int N, int K, int Fp, int interleave, int gsz, int per_channel, void* out,
+                           int N, int K, int Fp, int interleave, int gsz, int per_channel, int ldo, void* out,
                            cudaStream_t st) {
   const int64_t rows_out = interleave ? 2LL * Fp : N;
   const int64_t n_rows = (int64_t)G * rows_out;
   if (n_rows == 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>((n_rows + 7) / 8, (int64_t)kNumSMs * 16);
   if (wbits == 16)
-    dequant_kernel<16><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
+    dequant_kernel<16><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, ldo, (uint4*)out);
   else if (wbits == 8)
-    dequant_kernel<8><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
+    dequant_kernel<8><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, ldo, (uint4*)out);
   else if (wbits == 2)
-    dequant_kernel<2><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
+    dequant_kernel<2><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, ldo, (uint4*)out);
   else
-    dequant_kernel<4><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, (uint4*)out);
+    dequant_kernel<4><<<grid, 256, 0, st>>>(q0, s0, q1, s1, G, N, K, Fp, interleave, gsz, per_channel, ldo, (uint4*)out);
   return cudaGetLastError();
 }
 

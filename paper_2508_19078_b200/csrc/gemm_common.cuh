@@ -49,6 +49,21 @@ __device__ __forceinline__ TileInfo decode(int tile, const int32_t* s_sched, int
   return {lo, local / nt, local % nt};
 }
 
+// Output columns one MMA of tile ti must produce (CTA-pair kernels).  The last n-tile of a group
+// whose width is not a multiple of the tile issues only its valid columns: for gate/up the pair's
+// B halves hold gate features [0, f) (CTA 0) and up features [0, f) (CTA 1) of the tile, so an
+// N = 2f MMA reads the first f rows of each half and leaves gate in accumulator columns [0, f) and
+// up in [f, 2f) (e.g. F = 688: the sixth tile runs N = 96 instead of 256).  N % 16 == 0 and
+// F % 16 == 0 (validate_cfg) keep every N a legal M=256 MMA width.
+template <int EPI>
+__device__ __forceinline__ int pair_tile_cols(const Params& p, const TileInfo& ti) {
+  const int N = ti.g < p.E ? p.N_r : p.N_s;
+  if constexpr (EPI == EPI_SWIGLU) return 2 * min(kBN / 2, N - ti.n * (kBN / 2));
+  else return min(kBN, N - ti.n * kBN);
+}
+// K=16 MMAs of K slice kb (the last slice of a K that is not a multiple of 64 is partly empty)
+__device__ __forceinline__ int slice_k16(int K, int kb) { return min(kBK / 16, (K - kb * kBK) / 16); }
+
 // SiLU(v) = v / (1 + e^-v) with the SFU exp and the fast reciprocal-divide: ~2 ulp fp32 (far below
 // the bf16 rounding of a that follows), and ~5x fewer issue slots than expf + IEEE division, which
 // matters because the epilogue shares the SM's issue bandwidth with the next tile's producers.
@@ -60,7 +75,7 @@ __device__ __forceinline__ float silu(float v) { return __fdividef(v, 1.0f + __e
 // features n*128 + j; EPI_STORE: columns = output features n*256 + j.
 template <int EPI>
 __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, const TileInfo& ti, bool valid,
-                                               int64_t orow) {
+                                               int64_t orow, int up_col = kBN / 2) {
   const bool routed = ti.g < p.E;
   const int N = routed ? p.N_r : p.N_s;
   const int64_t ld = routed ? p.ld_r : p.ld_s;
@@ -69,13 +84,14 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
   const float* cs1 = routed ? p.cs1_r : p.cs1_s;
   const int64_t cs_base = routed ? (int64_t)ti.g * N : 0;
   if constexpr (EPI == EPI_SWIGLU) {
+    // gate in accumulator columns [0, up_col), up in [up_col, 2·up_col) (pair_tile_cols)
     for (int j = 0; j < kBN / 2; j += 16) {
       const int f0 = ti.n * (kBN / 2) + j;
+      if (j >= up_col || f0 >= N) break;  // warp-uniform (N % 16 == 0)
       float gv[16], uv[16];
       tmem_ld16(taddr + j, gv);
-      tmem_ld16(taddr + kBN / 2 + j, uv);
+      tmem_ld16(taddr + up_col + j, uv);
       tmem_ld_wait();
-      if (f0 >= N) continue;  // warp-uniform (N % 16 == 0)
       uint32_t pk[8];
 #pragma unroll
       for (int i = 0; i < 16; i += 2) {

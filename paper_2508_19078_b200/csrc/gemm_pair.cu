@@ -88,7 +88,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool gather = routed && p.gather_idx != nullptr;
       const int first = ti.m * kPairM + (int)rank * kHalfM;
       const int arow = s_row0[ti.g] + first;
-      const int brow = (routed ? ti.g * p.b_rows_r : 0) + ti.n * kBN + (int)rank * (kBN / 2);
+      // CTA 1's half starts at the tile's second half of B rows: the up features (gate/up layout)
+      // or output column cols/2 (a trimmed last tile reads cols/2 rows from each CTA)
+      const int half = EPI == EPI_SWIGLU ? kBN / 2 : pair_tile_cols<EPI>(p, ti) / 2;
+      const int brow = (routed ? ti.g * p.b_rows_r : 0) + ti.n * kBN + (int)rank * half;
       const CUtensorMap* ta = routed ? &tm_a_r : &tm_a_s;
       const CUtensorMap* tb = routed ? &tm_b_r : &tm_b_s;
       const int nkb = routed ? nkb_r : nkb_s;
@@ -108,11 +111,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (leader) {
-      constexpr uint32_t idesc = umma_idesc_bf16(kPairM, kBN);
       uint32_t it = 0, tc = 0;
       for (int tile = cid; tile < total; tile += ncl, ++tc) {
         const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
         const int nkb = ti.g < p.E ? nkb_r : nkb_s;
+        const int K = ti.g < p.E ? p.K_r : p.K_s;
+        const uint32_t idesc = umma_idesc_bf16(kPairM, (uint32_t)pair_tile_cols<EPI>(p, ti));
         const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
@@ -125,8 +129,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (elect_one()) {
             const uint32_t sa = smem_u32(smem + s * kStageBytes);
             const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + kABytes);
+            const int nk = slice_k16(K, kb);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k)
+              if (k < nk) umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
             umma_commit_pair_mc(&empty[s], 0x3);
             if (kb == nkb - 1) umma_commit_pair_mc(&tfull[acc], 0x3);
           }
@@ -146,7 +152,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int r_local = ti.m * kPairM + (int)rank * kHalfM + q * 32 + (int)lane_id();
       epilogue_slice<EPI>(p, tmem + acc * kBN + lane_base, ti, r_local < s_rows[ti.g],
-                          (int64_t)s_row0[ti.g] + r_local);
+                          (int64_t)s_row0[ti.g] + r_local, pair_tile_cols<EPI>(p, ti) / 2);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);

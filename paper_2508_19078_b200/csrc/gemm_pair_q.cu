@@ -115,7 +115,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   auto qrow_of = [&](const TileInfo& ti) -> int {
     const bool routed = ti.g < p.E;
     const int grp_base = routed ? ti.g * qp.qrows_r : 0;
-    return qp.gate_up ? grp_base + ti.n * (kBN / 2) : grp_base + ti.n * kBN + (int)rank * (kBN / 2);
+    // STORE: CTA 1 holds output columns [cols/2, cols) of the tile (pair_tile_cols)
+    return qp.gate_up ? grp_base + ti.n * (kBN / 2)
+                      : grp_base + ti.n * kBN + (int)rank * (pair_tile_cols<EPI>(p, ti) / 2);
   };
 
   if (warp == 0) {
@@ -171,11 +173,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
     if (leader) {
-      constexpr uint32_t idesc = umma_idesc_bf16(kPairM, kBN);
       uint32_t it = 0, tc = 0;
       for (int tile = cid; tile < total; tile += ncl, ++tc) {
         const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
         const int nkb = ti.g < p.E ? nkb_r : nkb_s;
+        const int K = ti.g < p.E ? p.K_r : p.K_s;
+        const uint32_t idesc = umma_idesc_bf16(kPairM, (uint32_t)pair_tile_cols<EPI>(p, ti));
         const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);  // CTA-scope acquire: a cluster-scope one invalidates L1
         tc_fence_after();
@@ -188,8 +191,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (elect_one()) {
             const uint32_t sa = smem_u32(smem + s * kStageBytes);
             const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + kABytes);
+            const int nk = slice_k16(K, kb);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k)
+              if (k < nk) umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
             umma_commit_pair_mc(&empty[s], 0x3);
             if (kb == nkb - 1) umma_commit_pair_mc(&tfull[acc], 0x3);
           }
@@ -210,7 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int r_local = ti.m * kPairM + (int)rank * kHalfM + q * 32 + (int)lane_id();
       epilogue_slice<EPI>(p, tmem + acc * kBN + lane_base, ti, r_local < s_rows[ti.g],
-                          (int64_t)s_row0[ti.g] + r_local);
+                          (int64_t)s_row0[ti.g] + r_local, pair_tile_cols<EPI>(p, ti) / 2);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);

@@ -168,7 +168,7 @@ cudaError_t launch_gemm_q(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap
                           const CUtensorMap& q_r1, const CUtensorMap& q_s0, const CUtensorMap& q_s1,
                           const QGemmArgs& a, cudaStream_t st);
 cudaError_t launch_dequant(int wbits, const uint8_t* q0, const float* s0, const uint8_t* q1, const float* s1, int G,
-                           int N, int K, int Fp, int interleave, int gsz, int per_channel, void* out,
+                           int N, int K, int Fp, int interleave, int gsz, int per_channel, int ldo, void* out,
                            cudaStream_t st);
 
 }  // namespace flux

@@ -35,6 +35,12 @@ __device__ __forceinline__ void load8(const void* w, int64_t elem, float (&f)[8]
   }
 }
 
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 // TS lanes per (row, group), CPL 8-element chunks per lane.
 template <int WBITS, bool F32IN, int TS, int CPL>
 __global__ void __launch_bounds__(256) quantize_kernel(const void* __restrict__ w, int64_t R, int64_t K, int64_t g,
@@ -49,8 +55,20 @@ __global__ void __launch_bounds__(256) quantize_kernel(const void* __restrict__ 
   // (row, grp) advanced incrementally: no 64-bit division per item
   int64_t row = team0 / G, grp = team0 - row * G;
   const int64_t drow = nteams / G, dgrp = nteams - drow * G;
+  // Items are consecutive (row, group) pairs, i.e. consecutive g-element slices of w: a warp's
+  // teams read one contiguous span per iteration.  Lane 0 prefetches the span kAhead iterations
+  // ahead into L2, which keeps ~4x more HBM bytes in flight than the registers alone can (80
+  // registers/thread cap residency at 24 warps/SM, each holding one 2 KB span).
+  constexpr int kAhead = 4;
+  const uint32_t span_bytes = (uint32_t)((32 / TS) * g * (F32IN ? 4 : 2));
+  const int64_t warp_item0 = team0 - (threadIdx.x % 32) / TS;
   for (int64_t item = team0; item < n_items; item += nteams) {
     const int64_t base = row * K + grp * g;
+    if ((threadIdx.x & 31) == 0) {
+      const int64_t pf = warp_item0 + (item - team0) + kAhead * nteams;  // first item of the span
+      if (pf + 32 / TS <= n_items)
+        bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(w) + pf * g * (F32IN ? 4 : 2), span_bytes);
+    }
     float v[CPL][8];
     float amax = 0.f;
     // chunk i of this lane is c = lane_t + i*TS: a team reads TS consecutive 16-byte vectors per load
@@ -72,43 +90,49 @@ __global__ void __launch_bounds__(256) quantize_kernel(const void* __restrict__ 
     for (int i = 0; i < CPL; ++i) {
       const int c = lane_t + i * TS;
       if (c >= nchunks) continue;
-      // RNE(fl32(w/s)) without a division on the common path: t' = w·fl32(1/s) differs from
-      // fl32(w/s) by < 2^-15 (|quotient| <= 127.5), so both round to the same integer unless t'
-      // lies within 2^-14 of a half-integer; those (rare) elements redo the IEEE division.  One
-      // rarely-taken branch per 8 elements keeps the common path straight-line.
-      int qi[8];
-      uint32_t need = 0;
+      // RNE(fl32(w/s)) without a division or a float->int conversion on the common path (the
+      // conversion pipe runs at a quarter of the FMA rate and bounded the previous version):
+      //   t = fma(w, fl32(1/s), 1.5·2^23) rounds the exact product w·fl32(1/s) to an integer, and
+      //   the low byte of t's bit pattern is that integer in two's complement (|q| <= 127);
+      //   d = fma(w, fl32(1/s), -(t - 1.5·2^23)) is the product's distance to it.
+      // w·fl32(1/s) differs from fl32(w/s) by < 2^-16 (|quotient| <= 127.5, two 2^-24 relative
+      // errors), so both round to the same integer unless |d| >= 1/2 - 2^-14; those (rare) chunks
+      // redo the IEEE division per element.  |fl32(w/s)| <= qmax·(1 + 2^-23) < qmax + 1/2 (s is
+      // max|w|/qmax rounded), so the fast path never needs the clamp.  s == 0 (1/s = inf) and
+      // non-finite inputs (d = NaN, kept by the NaN-propagating max) take the slow path.
+      constexpr float kMagic = 12582912.0f;  // 1.5·2^23
+      uint32_t tb[8];
+      float dmax = 0.f;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float tq = v[i][j] * rcp;
-        qi[j] = __float2int_rn(tq);
-        need |= (uint32_t)!(fabsf(tq - rintf(tq)) <= 0.5f - 6.103515625e-05f) << j;  // also NaN/inf
+        const float t = fmaf(v[i][j], rcp, kMagic);
+        const float d = fmaf(v[i][j], rcp, kMagic - t);
+        dmax = fmax_nan(dmax, fabsf(d));
+        tb[j] = __float_as_uint(t);
       }
-      if (sc == 0.f) {
+      if (!(dmax < 0.5f - 6.103515625e-05f) || !(rcp < INFINITY)) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) qi[j] = 0;
-      } else if (need) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if ((need >> j) & 1u) qi[j] = __float2int_rn(__fdiv_rn(v[i][j], sc));
+        for (int j = 0; j < 8; ++j) {
+          const int qi = sc == 0.f ? 0 : max(-qmax - 1, min(qmax, __float2int_rn(__fdiv_rn(v[i][j], sc))));
+          tb[j] = (uint32_t)qi;  // only the low byte is used below
+        }
       }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) qi[j] = max(-qmax - 1, min(qmax, qi[j]));
+      // gather the low bytes: bl = codes 0-3, bh = codes 4-7 (one byte each, two's complement)
+      const uint32_t bl = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+      const uint32_t bh = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
       if constexpr (WBITS == 2) {  // four codes per byte, element k in bits 2(k mod 4)
         uint32_t o = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o |= (uint32_t)(qi[j] & 0x3) << (2 * j);
+        for (int j = 0; j < 8; ++j) o |= (tb[j] & 0x3u) << (2 * j);
         *reinterpret_cast<uint16_t*>(q + (base + c * 8) / 4) = (uint16_t)o;
       } else if constexpr (WBITS == 8) {
-        uint2 o;
-        o.x = (qi[0] & 0xFF) | ((qi[1] & 0xFF) << 8) | ((qi[2] & 0xFF) << 16) | ((uint32_t)(qi[3] & 0xFF) << 24);
-        o.y = (qi[4] & 0xFF) | ((qi[5] & 0xFF) << 8) | ((qi[6] & 0xFF) << 16) | ((uint32_t)(qi[7] & 0xFF) << 24);
-        *reinterpret_cast<uint2*>(q + base + c * 8) = o;
+        *reinterpret_cast<uint2*>(q + base + c * 8) = make_uint2(bl, bh);
       } else {
-        uint32_t o = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o |= (uint32_t)(qi[j] & 0xF) << (4 * j);
-        *reinterpret_cast<uint32_t*>(q + (base + c * 8) / 2) = o;
+        // byte i of (b >> 4) carries byte i+1's low nibble in its high nibble: one bitwise mux
+        // per word puts codes (0,1) in byte 0 and (2,3) in byte 2; a final permute packs them
+        const uint32_t xl = (bl & 0x0F0F0F0Fu) | ((bl >> 4) & 0xF0F0F0F0u);
+        const uint32_t xh = (bh & 0x0F0F0F0Fu) | ((bh >> 4) & 0xF0F0F0F0u);
+        *reinterpret_cast<uint32_t*>(q + (base + c * 8) / 2) = __byte_perm(xl, xh, 0x6420);
       }
     }
     row += drow;

@@ -78,10 +78,10 @@ def features():
           f"kmeans {ms_k:.3f} ms;", {n: round(v[0] / max(v[1], 1), 4) for n, v in k.items() if v[1]})
 
 
-def layer():
+def layer(name="deepseek_moe"):
     from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
     from paper_2508_19078_b200 import synthetic
-    cfg = synth.CONFIGS["deepseek_moe"].with_(n_layers=1)
+    cfg = synth.CONFIGS[name].with_(n_layers=1)
     shape = ModelShape.of(cfg)
     qm = QuantizedModel(shape)
     qm.quantize_from(synthetic.master_weights(cfg))
@@ -92,8 +92,12 @@ def layer():
     ms = timed(lambda: prof.run(qm, x), reps=5, warm=2)
     F.timing_enable(False)
     k = F.timing_read(reset=True)
-    print(f"one DeepSeek layer, 262144 tokens: {ms:.2f} ms;",
+    print(f"one {name} layer, {cfg.tokens} tokens: {ms:.2f} ms;",
           {n: round(v[0] / max(v[1], 1), 3) for n, v in k.items() if v[1]})
+
+
+def layer_llama():
+    layer("llama_moe")
 
 
 if __name__ == "__main__":
