@@ -30,7 +30,7 @@ constexpr int kABytes = kBM * kBK * 2;   // 16 KB
 constexpr int kBBytes = kBN * kBK * 2;   // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 256;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64 + 16 + kScaleSmemBytes;
 
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   int32_t* s_sched = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 256);
   int32_t* s_row0 = s_sched + kMaxGroups;
   int32_t* s_rows = s_row0 + kMaxGroups;
+  float* s_scales =  // [2][kScaleFloats] (stage_tile_scales), 16-byte aligned
+      reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_rows + kMaxGroups) + 15) & ~uintptr_t(15));
 
   const int warp = warp_id();
   for (int i = threadIdx.x; i <= p.n_groups; i += kThreads) s_sched[i] = p.sched[i];
@@ -132,11 +134,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
       const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
       const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
+      const float* sc = stage_tile_scales<EPI>(p, ti, s_scales, tc, (int)threadIdx.x - 128);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const int r_local = ti.m * kBM + q * 32 + (int)lane_id();
       epilogue_slice<EPI>(p, tmem + acc * kBN + lane_base, ti, r_local < s_rows[ti.g],
-                          (int64_t)s_row0[ti.g] + r_local);
+                          (int64_t)s_row0[ti.g] + r_local, kBN / 2, sc);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&tempty[acc]);

@@ -64,6 +64,51 @@ __device__ __forceinline__ int pair_tile_cols(const Params& p, const TileInfo& t
 // K=16 MMAs of K slice kb (the last slice of a K that is not a multiple of 64 is partly empty)
 __device__ __forceinline__ int slice_k16(int K, int kb) { return min(kBK / 16, (K - kb * kBK) / 16); }
 
+// Per-channel scales (INT8/INT4/INT2 with group_size 0, reading R1b: the fp32 scale multiplies the
+// accumulator) of one tile, staged once per tile in shared memory by the 128 epilogue threads
+// instead of one dependent global load per 16 columns per thread (those loads serialised ~16 L2
+// round trips into every tile's epilogue: 34% tensor-pipe activity on the LLaMA-shape down GEMM).
+// Layout per tile: [0, 256) = cs0 of the tile's local columns (STORE) or gate features (SWIGLU),
+// [256, 384) = cs1 of the up features; two buffers alternate by tile parity (a buffer is rewritten
+// two tiles later, after every epilogue thread passed the next tile's barrier).
+constexpr int kScaleFloats = 512;
+constexpr int kScaleSmemBytes = 2 * kScaleFloats * 4;
+template <int EPI>
+__device__ __forceinline__ const float* stage_tile_scales(const Params& p, const TileInfo& ti, float* s_scales,
+                                                          uint32_t tc, int et /* epilogue thread 0..127 */) {
+  const bool routed = ti.g < p.E;
+  const float* cs0 = routed ? p.cs0_r : p.cs0_s;
+  if (!cs0) return nullptr;  // uniform per launch (grouped scales are folded into the B operand)
+  const float* cs1 = routed ? p.cs1_r : p.cs1_s;
+  const int N = routed ? p.N_r : p.N_s;
+  const int64_t base = routed ? (int64_t)ti.g * N : 0;
+  float* sc = s_scales + (tc & 1) * kScaleFloats;
+  if constexpr (EPI == EPI_SWIGLU) {
+    const int f = ti.n * (kBN / 2) + et;  // 128 threads: one gate and one up feature each
+    sc[et] = f < N ? __ldg(&cs0[base + f]) : 0.f;
+    sc[256 + et] = f < N ? __ldg(&cs1[base + f]) : 0.f;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int c = ti.n * kBN + et + 128 * i;
+      sc[et + 128 * i] = c < N ? __ldg(&cs0[base + c]) : 0.f;
+    }
+  }
+  named_bar_sync(2, 128);
+  return sc;
+}
+__device__ __forceinline__ void lds16(const float* sc, float (&v)[16]) {
+  const float4* q = reinterpret_cast<const float4*>(sc);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 t = q[i];
+    v[4 * i] = t.x;
+    v[4 * i + 1] = t.y;
+    v[4 * i + 2] = t.z;
+    v[4 * i + 3] = t.w;
+  }
+}
+
 // SiLU(v) = v / (1 + e^-v) with the SFU exp and the fast reciprocal-divide: ~2 ulp fp32 (far below
 // the bf16 rounding of a that follows), and ~5x fewer issue slots than expf + IEEE division, which
 // matters because the epilogue shares the SM's issue bandwidth with the next tile's producers.
@@ -75,14 +120,11 @@ __device__ __forceinline__ float silu(float v) { return __fdividef(v, 1.0f + __e
 // features n*128 + j; EPI_STORE: columns = output features n*256 + j.
 template <int EPI>
 __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, const TileInfo& ti, bool valid,
-                                               int64_t orow, int up_col = kBN / 2) {
+                                               int64_t orow, int up_col, const float* sc) {
   const bool routed = ti.g < p.E;
   const int N = routed ? p.N_r : p.N_s;
   const int64_t ld = routed ? p.ld_r : p.ld_s;
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(routed ? p.out_r : p.out_s) + orow * ld;
-  const float* cs0 = routed ? p.cs0_r : p.cs0_s;
-  const float* cs1 = routed ? p.cs1_r : p.cs1_s;
-  const int64_t cs_base = routed ? (int64_t)ti.g * N : 0;
   if constexpr (EPI == EPI_SWIGLU) {
     // gate in accumulator columns [0, up_col), up in [up_col, 2·up_col) (pair_tile_cols)
     for (int j = 0; j < kBN / 2; j += 16) {
@@ -92,18 +134,19 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
       tmem_ld16(taddr + j, gv);
       tmem_ld16(taddr + up_col + j, uv);
       tmem_ld_wait();
+      if (sc) {
+        float gs[16], us[16];
+        lds16(sc + j, gs);
+        lds16(sc + 256 + j, us);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          gv[i] *= gs[i];
+          uv[i] *= us[i];
+        }
+      }
       uint32_t pk[8];
 #pragma unroll
-      for (int i = 0; i < 16; i += 2) {
-        float g0 = gv[i], g1 = gv[i + 1], u0 = uv[i], u1 = uv[i + 1];
-        if (cs0) {
-          g0 *= __ldg(&cs0[cs_base + f0 + i]);
-          g1 *= __ldg(&cs0[cs_base + f0 + i + 1]);
-          u0 *= __ldg(&cs1[cs_base + f0 + i]);
-          u1 *= __ldg(&cs1[cs_base + f0 + i + 1]);
-        }
-        pk[i / 2] = pack_bf16x2(silu(g0) * u0, silu(g1) * u1);
-      }
+      for (int i = 0; i < 16; i += 2) pk[i / 2] = pack_bf16x2(silu(gv[i]) * uv[i], silu(gv[i + 1]) * uv[i + 1]);
       if (valid) {
         uint4* dst = reinterpret_cast<uint4*>(out + f0);
         dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -154,6 +197,12 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
           acc[8 * h + 2 * i + 1] = f.y;
         }
       }
+      if (sc) {  // per-channel scale of the shared MLP's down projection (reading R1b)
+        float cs[16];
+        lds16(sc + j, cs);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= cs[i];
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc[i] += __bfloat162float(__float2bfloat16_rn(v[i]));  // o_sh = bf16(a·ŵ)
 #pragma unroll
@@ -183,16 +232,15 @@ __device__ __forceinline__ void epilogue_slice(const Params& p, uint32_t taddr, 
       tmem_ld16(taddr + j, v);
       tmem_ld_wait();
       if (c0 >= N) continue;
+      if (sc) {
+        float cs[16];
+        lds16(sc + j, cs);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= cs[i];
+      }
       uint32_t pk[8];
 #pragma unroll
-      for (int i = 0; i < 16; i += 2) {
-        float a0 = v[i], a1 = v[i + 1];
-        if (cs0) {
-          a0 *= __ldg(&cs0[cs_base + c0 + i]);
-          a1 *= __ldg(&cs0[cs_base + c0 + i + 1]);
-        }
-        pk[i / 2] = pack_bf16x2(a0, a1);
-      }
+      for (int i = 0; i < 16; i += 2) pk[i / 2] = pack_bf16x2(v[i], v[i + 1]);
       if (valid) {
         uint4* dst = reinterpret_cast<uint4*>(out + c0);
         dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);

@@ -25,7 +25,7 @@ constexpr int kABytes = kHalfM * kBK * 2;     // 16 KB: this CTA's A rows
 constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 256;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64 + 128 * 4 + 16;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64 + 128 * 4 + 16 + kScaleSmemBytes;
 
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -44,6 +44,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   int32_t* s_rows = s_row0 + kMaxGroups;
   int32_t* s_idx =  // [128] gathered token ids, 16-byte aligned
       reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(s_rows + kMaxGroups) + 15) & ~uintptr_t(15));
+  float* s_scales = reinterpret_cast<float*>(s_idx + 128);  // [2][kScaleFloats] (stage_tile_scales)
 
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();
@@ -148,11 +149,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int tile = cid; tile < total; tile += ncl, ++tc) {
       const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
       const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
+      const float* sc = stage_tile_scales<EPI>(p, ti, s_scales, tc, (int)threadIdx.x - 128);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const int r_local = ti.m * kPairM + (int)rank * kHalfM + q * 32 + (int)lane_id();
       epilogue_slice<EPI>(p, tmem + acc * kBN + lane_base, ti, r_local < s_rows[ti.g],
-                          (int64_t)s_row0[ti.g] + r_local, pair_tile_cols<EPI>(p, ti) / 2);
+                          (int64_t)s_row0[ti.g] + r_local, pair_tile_cols<EPI>(p, ti) / 2, sc);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
