@@ -234,6 +234,76 @@ def test_quantizer_direct_bit_exact():
         assert np.array_equal(s.cpu().numpy(), s_ref), (wbits, g, dt)
 
 
+def _quantize_both(w, wbits, g, dtype):
+    """GPU codes/scales and the oracle's for the same (already representable) values."""
+    import paper_2508_19078_b200 as F
+    R, K = w.shape
+    q_ref, s_ref = oracle.quantize(w, wbits, g)
+    tw = torch.from_numpy(w).cuda().to(dtype)
+    q = torch.empty(R, K * wbits // 8, dtype=torch.uint8, device="cuda")
+    s = torch.empty(R, K // (g or K), dtype=torch.float32, device="cuda")
+    F.quantize_weights(tw, wbits, g, q, s)
+    return q.cpu().numpy(), s.cpu().numpy(), oracle.pack(q_ref, wbits).view(np.uint8), s_ref
+
+
+def test_quantizer_exhaustive_bf16():
+    """Every (w, s) pair a bf16 group can produce, up to a common power of two: max|w| = a with each
+    of the 128 bf16 mantissas, w every bf16 value with |w| <= a over the 10 binades where |w/s| can
+    reach 1/2 at qmax = 127 (below them every code is 0), both signs.  The GPU's division-free
+    quotient (Markstein correction, quantize.cu) must give the oracle's codes (IEEE division, RNE)
+    bit for bit at INT8/INT4/INT2, grouped and per channel."""
+    mant = 1.0 + np.arange(128) / 128.0
+    cand = np.concatenate([mant * 2.0 ** -e for e in range(10)])
+    cand = np.concatenate([cand, -cand, [0.0]]).astype(np.float32)
+    rows = []
+    for a in mant.astype(np.float32):
+        ws = cand[np.abs(cand) <= a]
+        for i in range(0, len(ws), 127):
+            chunk = ws[i:i + 127]
+            rows.append(np.concatenate([[a], chunk, np.zeros(127 - len(chunk), np.float32)]))
+    w = np.stack(rows).astype(np.float32)  # every value is exactly representable in bf16
+    assert np.array_equal(oracle.bf16_round(w).astype(np.float32), w)
+    for wbits in (8, 4, 2):
+        for g in (128, 0):
+            q, s, q_ref, s_ref = _quantize_both(w, wbits, g, torch.bfloat16)
+            assert np.array_equal(s, s_ref), (wbits, g)
+            assert np.array_equal(q, q_ref), (wbits, g, int((q != q_ref).sum()))
+
+
+def test_quantizer_near_ties_f32():
+    """fp32 masters: quotients within a few ulps of every half-integer n + 1/2 (the only places where
+    a quotient that is not correctly rounded would change a code), for random scales."""
+    rng = np.random.default_rng(5)
+    for wbits in (8, 4, 2):
+        qmax = (1 << (wbits - 1)) - 1
+        rows = []
+        for _ in range(400):
+            a = np.float32(rng.uniform(0.5, 1.0) * 2.0 ** rng.integers(-30, 30))
+            s = np.float32(a / np.float32(qmax))
+            vals = []
+            for n in range(-qmax - 1, qmax):
+                h = np.float32((n + 0.5) * np.float64(s))
+                v = h
+                for _k in range(3):
+                    v = np.nextafter(v, np.float32(np.inf))
+                    vals.append(v)
+                v = h
+                for _k in range(3):
+                    v = np.nextafter(v, np.float32(-np.inf))
+                    vals.append(v)
+                vals.append(h)
+            vals = np.array([v for v in vals if abs(v) <= a], np.float32)
+            for i in range(0, len(vals), 255):  # rows of 256: max|w| = a, then 255 probes
+                row = np.zeros(256, np.float32)
+                row[0] = a
+                row[1:1 + len(vals[i:i + 255])] = vals[i:i + 255]
+                rows.append(row)
+        w = np.stack(rows)
+        q, s, q_ref, s_ref = _quantize_both(w, wbits, 0, torch.float32)
+        assert np.array_equal(s, s_ref), wbits
+        assert np.array_equal(q, q_ref), (wbits, int((q != q_ref).sum()))
+
+
 def test_attention_hist_unit_bit_exact():
     """NEXT-3 (α = f·ā, R15): integer fixed-point sums, so the GPU must equal the oracle bit for bit,
     including empty (-1) picks and ties in the 2^-24 rounding."""
