@@ -352,6 +352,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.out_s = act_sh;
   ga.ld_r = Fld;
   ga.ld_s = Fsld;
+  ga.rows_r = Tk;
+  ga.rows_s = T;
   ga.grid = kNumSMs;
   ga.bm = sa.gemm_bm;
   ga.gather_idx = gather_a ? token_index : nullptr;

@@ -25,12 +25,91 @@ constexpr int kABytes = kHalfM * kBK * 2;     // 16 KB: this CTA's A rows
 constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 256;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 3 * kMaxGroups * 4 + 64 + 128 * 4 + 16 + kScaleSmemBytes;
+// after the ring: barriers, schedule copies, gather ids and scales (< 8 KB), then one 4 KB TMA-store
+// staging buffer per epilogue warp (1024-byte aligned: 128-byte swizzle atoms)
+constexpr int kMiscBytes = 8192;
+static_assert(256 + 3 * kMaxGroups * 4 + 16 + 128 * 4 + kScaleSmemBytes <= kMiscBytes, "smem layout");
+constexpr int kStageOutBytes = 4096;  // 32 rows x 64 bf16 columns
+constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kMiscBytes + 4 * kStageOutBytes;
+
+// TMA-store epilogue of one 32-row slice (a warp's TMEM lanes) whose rows all lie inside the group:
+// per 64-column chunk the warp converts its accumulator columns to bf16, writes them to its staging
+// buffer in the 128-byte-swizzled layout of the output tensor map (conflict-free: the 16-byte chunk
+// index is XORed with row % 8), and one lane issues a TMA store of the 32x64 box.  Versus one STG
+// per thread-row (32 scattered rows per instruction) this keeps the LSU out of the epilogue, which
+// bounded the LLaMA-shape down GEMM.  Same values and roundings as epilogue_slice.
+template <int EPI>
+__device__ __forceinline__ void epilogue_tma(const Params& p, uint32_t taddr, const TileInfo& ti, int up_col,
+                                             const float* sc, const CUtensorMap* tmo, uint32_t stage, int out_row) {
+  const int N = ti.g < p.E ? p.N_r : p.N_s;
+  const uint32_t lane = lane_id();
+  constexpr int kChunks = EPI == EPI_SWIGLU ? 2 : 4;  // 64-column output chunks per tile
+  for (int cc = 0; cc < kChunks; ++cc) {
+    const int j0 = cc * 64;
+    const int col0 = (EPI == EPI_SWIGLU ? ti.n * (kBN / 2) : ti.n * kBN) + j0;
+    if ((EPI == EPI_SWIGLU && j0 >= up_col) || col0 >= N) break;  // warp-uniform
+    uint32_t pk[32];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int j = j0 + 16 * h;
+      const bool live = (EPI != EPI_SWIGLU || j < up_col) && col0 + 16 * h < N;  // warp-uniform
+      if (!live) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pk[8 * h + i] = 0u;
+        continue;
+      }
+      if constexpr (EPI == EPI_SWIGLU) {
+        float gv[16], uv[16];
+        tmem_ld16(taddr + j, gv);
+        tmem_ld16(taddr + up_col + j, uv);
+        tmem_ld_wait();
+        if (sc) {
+          float gs[16], us[16];
+          lds16(sc + j, gs);
+          lds16(sc + 256 + j, us);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            gv[i] *= gs[i];
+            uv[i] *= us[i];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) pk[8 * h + i / 2] = pack_bf16x2(silu(gv[i]) * uv[i], silu(gv[i + 1]) * uv[i + 1]);
+      } else {
+        float v[16];
+        tmem_ld16(taddr + j, v);
+        tmem_ld_wait();
+        if (sc) {
+          float cs[16];
+          lds16(sc + j, cs);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] *= cs[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) pk[8 * h + i / 2] = pack_bf16x2(v[i], v[i + 1]);
+      }
+    }
+    if (lane == 0) bulk_wait_group_read0();  // the previous chunk's store has read the buffer
+    __syncwarp();
+    const uint32_t row_addr = stage + lane * 128;
+#pragma unroll
+    for (int c16 = 0; c16 < 8; ++c16)
+      st_shared_v4(row_addr + ((c16 ^ (lane & 7)) << 4),
+                   make_uint4(pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]));
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmo, stage, col0, out_row);
+      bulk_commit_group();
+    }
+  }
+}
 
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tm_a_r, const __grid_constant__ CUtensorMap tm_a_s,
                              const __grid_constant__ CUtensorMap tm_b_r, const __grid_constant__ CUtensorMap tm_b_s,
+                             const __grid_constant__ CUtensorMap tm_o_r, const __grid_constant__ CUtensorMap tm_o_s,
                              Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -45,6 +124,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   int32_t* s_idx =  // [128] gathered token ids, 16-byte aligned
       reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(s_rows + kMaxGroups) + 15) & ~uintptr_t(15));
   float* s_scales = reinterpret_cast<float*>(s_idx + 128);  // [2][kScaleFloats] (stage_tile_scales)
+  uint8_t* s_out = smem + kStages * kStageBytes + kMiscBytes;  // [4 warps][kStageOutBytes]
 
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();
@@ -145,6 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t stage_out = smem_u32(s_out) + q * kStageOutBytes;
     uint32_t tc = 0;
     for (int tile = cid; tile < total; tile += ncl, ++tc) {
       const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
@@ -152,13 +233,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float* sc = stage_tile_scales<EPI>(p, ti, s_scales, tc, (int)threadIdx.x - 128);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int r_local = ti.m * kPairM + (int)rank * kHalfM + q * 32 + (int)lane_id();
-      epilogue_slice<EPI>(p, tmem + acc * kBN + lane_base, ti, r_local < s_rows[ti.g],
-                          (int64_t)s_row0[ti.g] + r_local, pair_tile_cols<EPI>(p, ti) / 2, sc);
+      const int r_warp = ti.m * kPairM + (int)rank * kHalfM + q * 32;  // this warp's first row in the group
+      const int half = pair_tile_cols<EPI>(p, ti) / 2;
+      if (EPI != EPI_COMBINE && r_warp + 32 <= s_rows[ti.g]) {
+        epilogue_tma<EPI>(p, tmem + acc * kBN + lane_base, ti, half, sc, ti.g < p.E ? &tm_o_r : &tm_o_s,
+                          stage_out, s_row0[ti.g] + r_warp);
+      } else {  // a group's last rows (masked per thread) and the fused combine
+        const int r_local = r_warp + (int)lane_id();
+        epilogue_slice<EPI>(p, tmem + acc * kBN + lane_base, ti, r_local < s_rows[ti.g],
+                            (int64_t)s_row0[ti.g] + r_local, half, sc);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
     }
+    if (lane_id() == 0) bulk_wait_group0();  // every TMA store of this warp is complete
   }
   tc_fence_before();
   cluster_sync();
@@ -174,12 +263,26 @@ cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& 
   if (g.bm == 128) return launch_gemm_1sm(epi, a_r, a_s, b_r, b_s, g, st);
   if (g.bm != 256 || g.n_groups > kMaxGroups - 1) return cudaErrorInvalidValue;
   const Params p = make_params(g);
+  // output tensor maps of the TMA-store epilogue: bf16 [rows][N], row stride ld, 32x64 boxes
+  CUtensorMap o_r, o_s;
+  auto omap = [](CUtensorMap* m, void* base, int64_t rows, int N, int64_t ld) {
+    return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)rows, (uint64_t)N, (uint64_t)ld * 2, 64,
+                        32, CU_TENSOR_MAP_SWIZZLE_128B);
+  };
+  if (epi != EPI_COMBINE) {
+    if (!omap(&o_r, g.out_r, g.rows_r, g.N_r, g.ld_r)) return cudaErrorInvalidValue;
+    o_s = o_r;
+    if (g.n_groups > g.E && !omap(&o_s, g.out_s, g.rows_s, g.N_s, g.ld_s)) return cudaErrorInvalidValue;
+  } else {
+    o_r = a_r;  // unused by the fused-combine epilogue
+    o_s = a_r;
+  }
   auto kern = epi == EPI_SWIGLU  ? grouped_gemm_pair_kernel<EPI_SWIGLU>
               : epi == EPI_STORE ? grouped_gemm_pair_kernel<EPI_STORE>
                                  : grouped_gemm_pair_kernel<EPI_COMBINE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (e != cudaSuccess) return e;
-  kern<<<(g.grid / 2) * 2, kThreads, kSmemBytes, st>>>(a_r, a_s, b_r, b_s, p);
+  kern<<<(g.grid / 2) * 2, kThreads, kSmemBytes, st>>>(a_r, a_s, b_r, b_s, o_r, o_s, p);
   return cudaGetLastError();
 }
 

@@ -138,6 +138,7 @@ struct GemmArgs {
   const float *cs0_r, *cs1_r, *cs0_s, *cs1_s;  // per-channel scales [group][N] or null
   void *out_r, *out_s;      // bf16 [rows][ld]
   int64_t ld_r, ld_s;
+  int64_t rows_r, rows_s;   // rows of out_r / out_s (TMA-store tensor maps of the CTA-pair kernel)
   int grid;
   int bm;                   // rows per tile: 128 (1-CTA kernel) or 256 (CTA-pair kernel)
   // EPI_COMBINE only (shared-MLP down GEMM whose epilogue writes the layer output)
