@@ -28,6 +28,11 @@ SMALL = {
     # NEXT-3: the paper's bit-2, grouped and per-channel
     "int2_g64": synth.MoEConfig("int2_g64", 2, 128, 16, 4, 128, 192, 2, 64, 1, 600, synth.BASE_SEED + 14),
     "int2_pc": synth.MoEConfig("int2_pc", 2, 192, 8, 2, 64, 0, 2, 0, 0, 300, synth.BASE_SEED + 15),
+    # enough rows per expert for the dequant-pass GEMMs (T·k >= 2048·E): partial last n-tiles
+    # (F = 176 -> 128 + 48, F_s = 208 -> 128 + 80, H = 320 -> 256 + 64: trimmed MMAs), full 32-row
+    # TMA-store slices and ragged per-thread slices, per-channel scales staged in the epilogue
+    "pass_tails": synth.MoEConfig("pass_tails", 1, 320, 4, 2, 176, 208, 8, 0, 1, 4500, synth.BASE_SEED + 16),
+    "pass_tails_g64": synth.MoEConfig("pass_tails_g64", 1, 320, 3, 2, 192, 0, 4, 64, 0, 3300, synth.BASE_SEED + 17),
 }
 
 
@@ -111,7 +116,7 @@ def test_chunk_and_run_invariance():
     assert torch.equal(torch.cat([ya, yb]), y_full)
 
 
-@pytest.mark.parametrize("name", ["int4_shared", "int8_ragged", "int4_e64"])
+@pytest.mark.parametrize("name", ["int4_shared", "int8_ragged", "int4_e64", "pass_tails", "pass_tails_g64"])
 def test_weight_paths_bit_identical(name, monkeypatch):
     """Fused in-GEMM dequantization, the separate dequant pass (CTA-pair GEMM) and the 1-CTA GEMM all
     produce bit-identical layers: the choice between them is a pure performance policy."""

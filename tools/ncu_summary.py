@@ -49,7 +49,7 @@ def launches(path, out):
     total = sum(sum(v) for v in agg.values())
     lines = [f"# ncu launch list — {path.split('/')[-1]}", "",
              "`ncu --metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 1 --warmup 1`"
-             " (warm-up + timed + e2e step: 3 profiling rounds). Launches are serialised and cold-cache: compare"
+             " (warm-up + timed + e2e steps, `--rounds 0 --error-tokens 0`). Launches are serialised and cold-cache: compare"
              " SHARES with bench.py's live per-kernel CUDA-event times, not absolutes.", "",
              "| kernel | launches | mean ms | total ms | share |", "|---|---:|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):

@@ -5,9 +5,11 @@
 tag=${1:-r1}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv \
-  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --error-tokens 0 > gpurun_out/prof_bench_$tag.log 2>&1
+  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --error-tokens 0 --rounds 0 > gpurun_out/prof_bench_$tag.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"router|scatter|grouped_gemm|combine" -c 5 \
   -o gpurun_out/layer_$tag -f python tools/micro.py layer > gpurun_out/prof_layer_$tag.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"router|scatter|grouped_gemm|combine" -c 5 \
+  -o gpurun_out/llama_layer_$tag -f python tools/micro.py layer_llama > gpurun_out/prof_llama_$tag.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"quantize_kernel|dequant_kernel" -c 2 \
   -o gpurun_out/quant_$tag -f python tools/micro.py layer > gpurun_out/prof_quant_$tag.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"merge_kernel" -c 1 \
