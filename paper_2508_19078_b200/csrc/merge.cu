@@ -8,8 +8,8 @@
 // HBM-bound (read Σ|W_e| once, write Σ|W_c| once).  Every CTA builds the
 // member lists and fp32 weights of all clusters in shared memory (members in
 // ascending expert id, Σα accumulated in that order: deterministic); threads
-// then own 8 consecutive elements of one cluster output, load each member's
-// 16-byte vector, accumulate w_e·W_e in fp32 (FMA chain in member order) and
+// then own 2 × 8 elements of one cluster output, load up to 4 members' 16-byte
+// vectors at once, accumulate w_e·W_e in fp32 (FMA chain in member order) and
 // round once.  A singleton cluster has w = α/α = 1 exactly, so its output is
 // the input bit for bit.
 #include "internal.h"
@@ -19,17 +19,32 @@ namespace flux {
 namespace {
 
 constexpr int kMaxE = 1024;
+constexpr int kVecPerThread = 2;
+
+// One 8-element vector kept raw until its FMA (bf16: one uint4 = 4 registers), so a thread can
+// hold many loads in flight.
+template <bool F32> struct Raw;
+template <> struct Raw<false> { uint4 a; };
+template <> struct Raw<true> { float4 a, b; };
 
 template <bool F32>
-__device__ __forceinline__ void load_vec(const void* base, int64_t elem, float (&f)[8]) {
+__device__ __forceinline__ void load_raw(const void* base, int64_t elem, Raw<F32>& r) {
   if constexpr (F32) {
     const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + elem);
-    const float4 a = __ldcs(p), b = __ldcs(p + 1);
-    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
-    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+    r.a = __ldcs(p);
+    r.b = __ldcs(p + 1);
   } else {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + elem));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    r.a = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + elem));
+  }
+}
+
+template <bool F32>
+__device__ __forceinline__ void to_f32(const Raw<F32>& r, float (&f)[8]) {
+  if constexpr (F32) {
+    f[0] = r.a.x; f[1] = r.a.y; f[2] = r.a.z; f[3] = r.a.w;
+    f[4] = r.b.x; f[5] = r.b.y; f[6] = r.b.z; f[7] = r.b.w;
+  } else {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r.a);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float2 p = __bfloat1622float2(h[i]);
@@ -67,8 +82,12 @@ __global__ void __launch_bounds__(256) merge_kernel(int E, int64_t numel, const 
   __shared__ float s_w[kMaxE];       // weight of member slot
   __shared__ int s_mem[kMaxE];       // member expert ids grouped by cluster
   __shared__ int s_start[kMaxE + 1]; // cluster -> first member slot
+  __shared__ float s_alpha[kMaxE];
   __shared__ int s_ntun;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) s_cl[e] = cluster_of[e];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    s_cl[e] = cluster_of[e];
+    s_alpha[e] = alpha[e];
+  }
   __syncthreads();
   if (compact) {  // relabel: tuning expert -> its rank among tuning experts, cluster c -> n_tun + c
     if (threadIdx.x == 0) {
@@ -103,12 +122,12 @@ __global__ void __launch_bounds__(256) merge_kernel(int E, int64_t numel, const 
     int cnt = 0;
     for (int e = 0; e < E; ++e)
       if (s_cl[e] == c) {
-        asum += __ldg(&alpha[e]);
+        asum += s_alpha[e];
         s_mem[s_start[c] + cnt++] = e;
       }
     for (int i = 0; i < cnt; ++i) {
       const int e = s_mem[s_start[c] + i];
-      s_w[s_start[c] + i] = asum > 0.f ? __fdiv_rn(__ldg(&alpha[e]), asum) : __fdiv_rn(1.f, (float)cnt);
+      s_w[s_start[c] + i] = asum > 0.f ? __fdiv_rn(s_alpha[e], asum) : __fdiv_rn(1.f, (float)cnt);
     }
   }
   __syncthreads();
@@ -123,29 +142,64 @@ __global__ void __launch_bounds__(256) merge_kernel(int E, int64_t numel, const 
         if (s_cl[e] >= 0) remap[e] = slot + s_cl[e];
     }
   }
+  // Main loop: a CTA owns chunks of kVecPerThread·blockDim.x consecutive 16-byte vectors of one
+  // output (chunks dealt round-robin, so at any moment the CTAs stream neighbouring addresses);
+  // each thread issues the loads of up to 4 members × kVecPerThread vectors before the first FMA
+  // (bytes in flight per SM to cover HBM latency), then accumulates in member order — the same FMA
+  // chain as one member at a time, so results are unchanged bit for bit.
   const int64_t nvec = numel / 8;
-  const int64_t items = (int64_t)C * nvec;
-  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(it / nvec);
-    const int64_t v = it - (int64_t)c * nvec;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int m = s_start[c]; m < s_start[c + 1]; ++m) {
-      float f[8];
-      load_vec<F32>(experts, (int64_t)s_mem[m] * numel + v * 8, f);
-      const float wm = s_w[m];
+  const int64_t per_chunk = (int64_t)kVecPerThread * blockDim.x;
+  const int64_t chunks_per_c = (nvec + per_chunk - 1) / per_chunk;
+  const int64_t chunks = (int64_t)C * chunks_per_c;
+  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    const int c = (int)(ch / chunks_per_c);
+    const int64_t v0 = (ch - (int64_t)c * chunks_per_c) * per_chunk + threadIdx.x;
+    float acc[kVecPerThread][8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = fmaf(wm, f[i], acc[i]);
+    for (int u = 0; u < kVecPerThread; ++u)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
+    const int m_end = s_start[c + 1];
+    for (int m0 = s_start[c]; m0 < m_end; m0 += 4) {
+      Raw<F32> r[4][kVecPerThread];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (m0 + j < m_end) {
+          const int64_t base = (int64_t)s_mem[m0 + j] * numel;
+#pragma unroll
+          for (int u = 0; u < kVecPerThread; ++u) {
+            const int64_t v = v0 + (int64_t)u * blockDim.x;
+            if (v < nvec) load_raw<F32>(experts, base + v * 8, r[j][u]);
+          }
+        }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (m0 + j < m_end) {
+          const float wm = s_w[m0 + j];
+#pragma unroll
+          for (int u = 0; u < kVecPerThread; ++u) {
+            float f[8];
+            to_f32<F32>(r[j][u], f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[u][i] = fmaf(wm, f[i], acc[u][i]);
+          }
+        }
     }
-    store_vec<F32>(merged, (int64_t)c * numel + v * 8, acc);
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+      const int64_t v = v0 + (int64_t)u * blockDim.x;
+      if (v < nvec) store_vec<F32>(merged, (int64_t)c * numel + v * 8, acc[u]);
+    }
   }
 }
 }  // namespace
 
 cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
                          const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st, int compact) {
-  const int64_t items = (int64_t)(compact ? E : C) * (numel / 8);  // upper bound for the compact case
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)kNumSMs * 8));
+  const int64_t per_chunk = (int64_t)kVecPerThread * 256;
+  const int64_t chunks = (int64_t)(compact ? E : C) * ((numel / 8 + per_chunk - 1) / per_chunk);  // upper bound (compact)
+  const unsigned grid = (unsigned)std::max<int64_t>(  // one resident wave: 3 (bf16) / 2 (fp32) CTAs per SM
+      1, std::min<int64_t>(chunks, (int64_t)kNumSMs * (fp32 ? 2 : 3)));
   if (fp32)
     merge_kernel<true><<<grid, 256, 0, st>>>(E, numel, experts, cluster_of, alpha, C, merged, remap, compact);
   else

@@ -55,7 +55,7 @@ class MoEConfig:
     norm_topk: int   # 0: w = softmax prob (DeepSeek-MoE); 1: renormalised over the top-k
     tokens: int
     seed: int
-    skew: str = "fig2"  # "fig2" | "balanced"
+    skew: str = "fig2"  # "fig2" | "balanced" | "hot" (layer 0: a few experts take most tokens, others none)
 
     def with_(self, **kw) -> "MoEConfig":
         return replace(self, **kw)
@@ -88,6 +88,8 @@ def scale_c(sigma: float) -> float:
 def router_skew_sigma(cfg: MoEConfig, layer: int) -> float:
     if cfg.skew == "balanced":
         return 0.0
+    if cfg.skew == "hot" and layer == 0:  # SURVEY §8d hot-expert variant: σ_β = 2.5 >> the unit logit noise
+        return 2.5
     if cfg.n_layers == 1:
         return 0.35
     return 0.35 + (0.10 - 0.35) * layer / (cfg.n_layers - 1)

@@ -1,0 +1,69 @@
+"""GPU parity on the degenerate cases of the method (SURVEY §8c O2/O3 special cases), through the
+C ABI against the CPU oracle on the same seeded inputs: a single token, a tile plus one token,
+k = E (every expert sees every token, hist = T), E = k = 1 (the layer is a dense SwiGLU MLP),
+top-1 routing, and the hot-expert skew of SURVEY §8d (one expert takes most tokens of layer 0 and
+several experts receive none: empty D_e segments and empty GEMM groups)."""
+import numpy as np
+import pytest
+
+import oracle.model as om
+import synth
+
+from _parity import check_hist_and_de, compare_layer, input_bound
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+S = synth.BASE_SEED
+EDGE = {
+    "one_token": synth.CONFIGS["toy"].with_(tokens=1, name="one_token"),
+    "tile_plus_one": synth.MoEConfig("tile_plus_one", 2, 128, 8, 2, 96, 0, 8, 0, 1, 129, S + 21),
+    "k_eq_E": synth.MoEConfig("k_eq_E", 2, 64, 8, 8, 128, 0, 8, 0, 1, 300, S + 22),
+    "dense_E1": synth.MoEConfig("dense_E1", 2, 128, 1, 1, 64, 0, 8, 0, 0, 200, S + 23),
+    "top1_int4": synth.MoEConfig("top1_int4", 2, 128, 16, 1, 128, 0, 4, 64, 0, 500, S + 24),
+    "hot_expert": synth.MoEConfig("hot_expert", 2, 128, 16, 2, 128, 128, 4, 128, 0, 700, S + 25, skew="hot"),
+}
+
+
+def _run_gpu(cfg):
+    import paper_2508_19078_b200 as F  # noqa: F401
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
+    from paper_2508_19078_b200 import synthetic
+    qm = QuantizedModel(ModelShape.of(cfg))
+    qm.quantize_from(synthetic.master_weights(cfg))
+    prof = Profiler(ModelShape.of(cfg), cfg.tokens, with_logits=True)
+    ys = []
+    prof.run(qm, synthetic.tokens(cfg, 0, cfg.tokens), on_layer=lambda l, y: ys.append(y.float().cpu().numpy()))
+    torch.cuda.synchronize()
+    return prof, ys
+
+
+@pytest.mark.parametrize("name", list(EDGE))
+def test_degenerate_case_parity(name):
+    cfg = EDGE[name]
+    prof, ys = _run_gpu(cfg)
+    ref = om.profile_all(cfg)
+    T, E, k = cfg.tokens, cfg.n_experts, cfg.top_k
+    alive = np.ones(T, bool)
+    for l in range(cfg.n_layers):
+        gpu = dict(logits=prof.logits[l].cpu().numpy(), ids=prof.ids[l].cpu().numpy(), w=prof.w[l].cpu().numpy(),
+                   y=ys[l])
+        wr = om.master_f32(synth.spec_router(cfg, l))
+        dz = input_bound(ys[l - 1] if l else None, ref[l]["x"], wr)
+        rep = compare_layer(l, ref[l], gpu, alive, dz)
+        assert rep.n_cmp >= 0.9 * T
+        hist = prof.hist[l].cpu().numpy()
+        check_hist_and_de(gpu["ids"], hist, prof.offsets[l].cpu().numpy(), prof.token_index[l].cpu().numpy(), E)
+        assert hist.sum() == T * k and hist.min() >= 0 and hist.max() <= T
+        if rep.n_div == 0 and np.all(alive):
+            assert np.array_equal(hist, ref[l]["hist"])
+            assert np.array_equal(prof.token_index[l].cpu().numpy(), ref[l]["token_index"])
+            assert np.array_equal(prof.offsets[l].cpu().numpy(), ref[l]["offsets"])
+        if k == E:  # every expert sees every token (O2 pin)
+            assert np.all(hist == T)
+        if E == 1:  # softmax over one expert: w = 1 exactly
+            assert np.all(gpu["w"] == 1.0)
+    if name == "hot_expert":  # the case is only covered if it really produced empty and hot experts
+        h0 = prof.hist[0].cpu().numpy()
+        assert (h0 == 0).sum() >= 2 and h0.max() >= 0.4 * T, h0

@@ -59,6 +59,30 @@ def merge():
     print(f"merge 64->16 bf16 one family/layer: {ms:.3f} ms  {by / ms / 1e6:.0f} GB/s  ({by / ms / 1e6 / peak():.2f})")
 
 
+def merge_model():
+    """a8 over all 28 DeepSeek layers × 3 families, balanced vs unbalanced clusters, cold vs power-capped."""
+    from paper_2508_19078_b200 import synthetic
+    from paper_2508_19078_b200.driver import merge_model as mm
+    cfg = synth.CONFIGS["deepseek_moe"]
+    m = synthetic.master_weights(cfg)
+    L, E, C = cfg.n_layers, cfg.n_experts, 16
+    alpha = torch.rand(L, E, device="cuda")
+    by = m.gate.numel() * 2 * 3 * (1 + C / E)
+    bal = (torch.arange(E, dtype=torch.int32, device="cuda") % C).repeat(L, 1).contiguous()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    unb = torch.randint(0, C, (L, E), generator=g, device="cuda", dtype=torch.int32)
+    unb[:, :C] = torch.arange(C, dtype=torch.int32, device="cuda")
+    out = mm(m, alpha, bal, C)
+    a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    for name, cl in (("balanced", bal), ("unbalanced", unb)):
+        ms = timed(lambda: mm(m, alpha, cl, C, out), reps=5, warm=2)
+        print(f"merge_model {name}: {ms:.2f} ms  {by / ms / 1e6:.0f} GB/s ({by / ms / 1e6 / peak():.2f})")
+        for _ in range(300):  # ~1 s of bf16 GEMMs: power-capped clocks, like inside the bench step
+            a @ a
+        ms = timed(lambda: mm(m, alpha, cl, C, out), reps=1, warm=0)
+        print(f"merge_model {name} after GEMM load: {ms:.2f} ms  {by / ms / 1e6:.0f} GB/s ({by / ms / 1e6 / peak():.2f})")
+
+
 def features():
     """§5.2 C1 over all 28 DeepSeek layers (gate|up|down of 64 experts) + C2 K-Means into 16 clusters."""
     from paper_2508_19078_b200 import synthetic
