@@ -87,12 +87,21 @@ static int gemm_bm() { return env_on("FLUX_GEMM_1SM") ? 128 : 256; }
 // copy roofline) or fused into the shared-MLP down GEMM's epilogue (FLUX_FUSED_COMBINE=1; bit-
 // identical, saves the y_sh round-trip, but its per-thread-row gathers are latency-bound today).
 static bool fused_combine() { return env_on("FLUX_FUSED_COMBINE"); }
-// Routed A rows of the gate/up GEMM: materialised in expert order by K2 (default) or gathered from
-// x inside the CTA-pair GEMM with TMA tile::gather4 (FLUX_GATHER_A=1; bit-identical).  Measured on
-// B200: gather4 delivers ~5 B/clk/SM (~100 cycles per 512-byte request), and each A tile is fetched
-// by every n-tile (11 for the DeepSeek shape), so the gathered GEMM runs ~2.5x slower than writing
-// x_perm once (1.4 ms per layer) — kept as an opt-in for small or latency-bound batches.
-static bool gather_routed_a() { return env_on("FLUX_GATHER_A") && gemm_bm() == 256; }
+// Routed A rows of the gate/up GEMM (all choices bit-identical, by test):
+//  * GATHER_CP (default whenever the dequant-pass CTA-pair kernel runs): gathered from x inside the
+//    GEMM by two producer warps with per-lane 16-byte cp.async (LDGSTS) into the swizzled stage, so
+//    K2 writes only the D_e indices.  Measured (B200, in the bench step): the gate/up GEMM runs ~1-3%
+//    slower than from a materialised x_perm, but K2's k·H·2 bytes per token disappear (1.4 ms per
+//    layer) and the lower HBM power lets the clocks rise: +5% tokens/s on both BASELINE shapes.
+//  * GATHER_TMA (FLUX_GATHER_A=1): TMA tile::gather4 (~5 B/clk/SM: ~2.5x slower GEMM).
+//  * NONE (FLUX_GATHER_A=0, the fused-dequant kernel, the 1-CTA kernel): K2 materialises x_perm.
+enum GatherMode { GATHER_NONE = 0, GATHER_TMA = 1, GATHER_CP = 2 };
+static GatherMode gather_mode(const flux_moe_cfg& c, int64_t T) {
+  const char* e = getenv("FLUX_GATHER_A");
+  if (gemm_bm() != 256 || (e && e[0] == '0')) return GATHER_NONE;
+  if (e && e[0] == '1') return GATHER_TMA;
+  return dequant_pass(c, T) ? GATHER_CP : GATHER_NONE;
+}
 
 static bool tmap_u8(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_bytes, uint32_t box_cols) {
   return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rows, cols_bytes, cols_bytes, box_cols, 128,
@@ -146,7 +155,7 @@ WsPlan plan(const flux_moe_cfg& c, int64_t T) {
   p.row0 = L.take(sizeof(int32_t) * n_groups);
   p.rows = L.take(sizeof(int32_t) * n_groups);
   // x_perm (routed A rows materialised by K2) unless the GEMM gathers them; y_perm always.
-  p.x_perm = L.take(gather_routed_a() ? 0 : 2ull * Tk * c.hidden);
+  p.x_perm = L.take(gather_mode(c, T) != GATHER_NONE ? 0 : 2ull * Tk * c.hidden);
   p.y_perm = L.take(2ull * Tk * c.hidden);
   p.act = L.take(2ull * Tk * pad64(c.ffn));
   p.act_sh = L.take(2ull * T * pad64(c.shared_ffn));
@@ -251,7 +260,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   int32_t* offsets = (int32_t*)(W + P.offsets);
   int32_t* token_index = out->token_index ? out->token_index : (int32_t*)(W + P.token_index);
   int32_t* inv_pos = (int32_t*)(W + P.inv_pos);
-  const bool gather_a = gather_routed_a();
+  const GatherMode gmode = gather_mode(*cfg, T);
+  const bool gather_a = gmode != GATHER_NONE;
   void* x_perm = gather_a ? nullptr : W + P.x_perm;
   void* y_perm = W + P.y_perm;
   void* act = W + P.act;
@@ -357,8 +367,12 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.grid = kNumSMs;
   ga.bm = sa.gemm_bm;
   ga.gather_idx = gather_a ? token_index : nullptr;
+  ga.gather_cp = gmode == GATHER_CP ? 1 : 0;
+  ga.a_src = x;
+  ga.a_ld = H;
   GemmArgs gd = ga;
   gd.gather_idx = nullptr;  // the down GEMM reads act, materialised in permuted order by K3
+  gd.gather_cp = 0;
   gd.sched = sa.sched_dn;
   gd.n_tiles_r = sa.n_tiles_dn;
   gd.n_tiles_s = sa.n_tiles_dn_sh;

@@ -31,6 +31,9 @@ struct Params {
   int k;
   // routed A rows gathered from x by token id (TMA tile::gather4) instead of a materialised x_perm
   const int32_t* gather_idx;  // token_index [T*k] or null
+  int gather_cp;               // 1: gather with cp.async (CTA-pair pass kernel) instead of TMA gather4
+  const __nv_bfloat16* a_src;  // gather source rows (x) and their stride in elements
+  int a_ld;
 };
 
 struct TileInfo {
@@ -374,6 +377,9 @@ inline Params make_params(const GemmArgs& g) {
   p.inv_pos = g.inv_pos;
   p.k = g.k;
   p.gather_idx = g.gather_idx;
+  p.gather_cp = g.gather_cp;
+  p.a_src = reinterpret_cast<const __nv_bfloat16*>(g.a_src);
+  p.a_ld = g.a_ld;
   return p;
 }
 

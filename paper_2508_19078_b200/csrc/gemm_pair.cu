@@ -24,7 +24,7 @@ constexpr int kHalfM = 128, kPairM = 256, kStages = 6;
 constexpr int kABytes = kHalfM * kBK * 2;     // 16 KB: this CTA's A rows
 constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kThreads = 256;
+constexpr int kThreads = 288;  // 9 warps: TMA, MMA, 2 gather producers, 4 epilogue, gather relay
 // after the ring: barriers, schedule copies, gather ids and scales (< 8 KB), then one 4 KB TMA-store
 // staging buffer per epilogue warp (1024-byte aligned: 128-byte swizzle atoms)
 constexpr int kMiscBytes = 8192;
@@ -105,6 +105,38 @@ __device__ __forceinline__ void epilogue_tma(const Params& p, uint32_t taddr, co
   }
 }
 
+// Routed A rows gathered from x with per-lane 16-byte cp.async (LDGSTS) instead of a materialised
+// x_perm: per 64-wide K slice this CTA's 128 rows x 128 bytes are copied by two producer warps
+// (warps 2 and 3, 64 rows each; one warp is issue-bound, and warp 0 keeps the TMA loads of B and
+// of the shared MLP's A), one warp instruction per 4 rows
+// (8 lanes per row, 16-byte chunk c of row r to r·128 + ((c ^ r%8)·16): the 128-byte swizzle a TMA
+// box would produce, conflict-free).  A lane's 16 row sources (token ids; rows past the group end
+// read token 0 and are masked in the epilogue) are loaded into registers once per tile, so a slice
+// is 16 independent address + LDGSTS pairs per lane.  H % 64 == 0: no K tail.
+constexpr int kGatherParts = 2;
+constexpr int kGatherRows = kHalfM / 4 / kGatherParts;  // row groups of 4 per warp
+__device__ __forceinline__ void gather_ids(const Params& p, int row0, int rows_in_grp, int first, int part,
+                                           int (&tok)[kGatherRows]) {
+  const int lane = (int)lane_id();
+#pragma unroll
+  for (int i = 0; i < kGatherRows; ++i) {
+    const int rl = first + part * (kHalfM / kGatherParts) + 4 * i + (lane >> 3);
+    tok[i] = rl < rows_in_grp ? __ldg(&p.gather_idx[row0 + rl]) : 0;
+  }
+}
+__device__ __forceinline__ void gather_a_cp(uint8_t* dst, const Params& p, const int (&tok)[kGatherRows], int kb,
+                                            int part) {
+  const int lane = (int)lane_id();
+  const int chunk = lane & 7;
+  const uint32_t base = smem_u32(dst);
+  const __nv_bfloat16* src0 = p.a_src + kb * kBK + chunk * 8;
+#pragma unroll
+  for (int i = 0; i < kGatherRows; ++i) {
+    const int row = part * (kHalfM / kGatherParts) + 4 * i + (lane >> 3);
+    cp_async16(base + row * 128 + ((chunk ^ (row & 7)) << 4), src0 + (int64_t)tok[i] * p.a_ld);
+  }
+}
+
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tm_a_r, const __grid_constant__ CUtensorMap tm_a_s,
@@ -118,6 +150,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* afull = full + 24;        // [kStages] (byte 192): this CTA's cp.async-gathered A rows landed
   int32_t* s_sched = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 256);
   int32_t* s_row0 = s_sched + kMaxGroups;
   int32_t* s_rows = s_row0 + kMaxGroups;
@@ -134,10 +167,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     s_row0[i] = p.grp_row0[i];
     s_rows[i] = p.grp_rows[i];
   }
+  // cp.async gather: full[s] also waits for one relay arrive per CTA (its A rows landed and were
+  // made visible to the async proxy), on top of the leader's expect_tx arrive
+  const bool cpg = EPI == EPI_SWIGLU && p.gather_idx != nullptr && p.gather_cp;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], cpg ? 3 : 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&afull[s], 32 * kGatherParts);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -176,15 +213,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const CUtensorMap* ta = routed ? &tm_a_r : &tm_a_s;
       const CUtensorMap* tb = routed ? &tm_b_r : &tm_b_s;
       const int nkb = routed ? nkb_r : nkb_s;
-      if (gather) stage_gather_rows(s_idx, p, s_row0[ti.g], s_rows[ti.g], first);
+      if (gather && !cpg) stage_gather_rows(s_idx, p, s_row0[ti.g], s_rows[ti.g], first);
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = (it + kb) % kStages;
         const uint32_t ph = ((it + kb) / kStages) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + s * kStageBytes;
-        if (leader && lane_id() == 0) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+        const bool a_cp = cpg && gather;  // A rows by cp.async: only the B halves are TMA bytes
+        if (leader && lane_id() == 0) mbar_arrive_expect_tx(&full[s], a_cp ? 2 * kBBytes : 2 * kStageBytes);
         __syncwarp();  // the transaction count is armed before any of this warp's copies can land
-        load_a_pair(st, ta, &full[s], kb, arow, gather, s_idx);
+        if (!a_cp) load_a_pair(st, ta, &full[s], kb, arow, gather, s_idx);  // else: warps 2 and 3
         if (lane_id() == 0) tma_load_2d_pair(st + kABytes, tb, &full[s], kb * kBK, brow);
       }
       it += nkb;
@@ -221,7 +259,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp == 2 || warp == 3) {
+    // cp.async gather producers (warp 2: rows 0..63 of this CTA's half, warp 3: rows 64..127);
+    // every lane arrives on afull every stage (at once for stages whose A comes by TMA)
+    if (cpg) {
+      const int part = warp - 2;
+      uint32_t it = 0;
+      for (int tile = cid; tile < total; tile += ncl) {
+        const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+        const bool gather = ti.g < p.E;
+        const int nkb = gather ? nkb_r : nkb_s;
+        int tok[kGatherRows];
+        if (gather) gather_ids(p, s_row0[ti.g], s_rows[ti.g], ti.m * kPairM + (int)rank * kHalfM, part, tok);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          if (gather) gather_a_cp(smem + s * kStageBytes, p, tok, kb, part);
+          cp_async_mbar_arrive_noinc(&afull[s]);
+        }
+      }
+    }
+  } else if (warp == 8) {
+    // cp.async gather relay: once this CTA's gathered rows of stage s have landed, make them visible
+    // to the async proxy (tcgen05.mma reads them) and arrive on the leader's full[s]
+    if (cpg && lane_id() == 0) {
+      const uint32_t full_leader0 = mapa(smem_u32(&full[0]), 0);
+      uint32_t it = 0;
+      for (int tile = cid; tile < total; tile += ncl) {
+        const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
+        const int nkb = ti.g < p.E ? nkb_r : nkb_s;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&afull[s], (it / kStages) & 1);
+          fence_proxy_async_smem();
+          mbar_arrive_cluster(full_leader0 + s * 8);
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);

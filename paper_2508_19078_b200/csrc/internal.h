@@ -150,6 +150,11 @@ struct GemmArgs {
   // routed A rows gathered from x (tm_a_r = gather map over x, box {64,1}) by token_index; null =
   // rows read contiguously from a materialised x_perm / act
   const int32_t* gather_idx;
+  // CTA-pair pass-path kernel only: gather the rows with per-lane 16-byte cp.async (LDGSTS) from
+  // a_src (bf16 [T][a_ld]) instead of TMA tile::gather4 (tm_a_r unused for routed tiles then)
+  int gather_cp;
+  const void* a_src;
+  int a_ld;
 };
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);

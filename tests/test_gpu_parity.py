@@ -118,8 +118,9 @@ def test_chunk_and_run_invariance():
 
 @pytest.mark.parametrize("name", ["int4_shared", "int8_ragged", "int4_e64", "pass_tails", "pass_tails_g64"])
 def test_weight_paths_bit_identical(name, monkeypatch):
-    """Fused in-GEMM dequantization, the separate dequant pass (CTA-pair GEMM) and the 1-CTA GEMM all
-    produce bit-identical layers: the choice between them is a pure performance policy."""
+    """Fused in-GEMM dequantization, the separate dequant pass (CTA-pair GEMM) and the 1-CTA GEMM, with
+    the routed A rows materialised (x_perm) or gathered inside the GEMM (cp.async: the pass-path
+    default; TMA gather4), all produce bit-identical layers: the choice is a pure performance policy."""
     from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
     from paper_2508_19078_b200 import synthetic
     cfg = SMALL[name]
@@ -132,7 +133,9 @@ def test_weight_paths_bit_identical(name, monkeypatch):
                 {"FLUX_FUSED_COMBINE": "1", "FLUX_GEMM_FUSED_DEQUANT": "1"},
                 {"FLUX_FUSED_COMBINE": "1", "FLUX_GEMM_DEQUANT_PASS": "1"},
                 {"FLUX_GATHER_A": "1", "FLUX_GEMM_FUSED_DEQUANT": "1"},
-                {"FLUX_GATHER_A": "1", "FLUX_GEMM_DEQUANT_PASS": "1"}):
+                {"FLUX_GATHER_A": "1", "FLUX_GEMM_DEQUANT_PASS": "1"},
+                {"FLUX_GATHER_A": "2", "FLUX_GEMM_DEQUANT_PASS": "1"},
+                {"FLUX_GATHER_A": "0", "FLUX_GEMM_DEQUANT_PASS": "1"}):
         for k in ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM", "FLUX_FUSED_COMBINE",
                   "FLUX_GATHER_A"):
             monkeypatch.delenv(k, raising=False)
