@@ -95,6 +95,15 @@ static bool fused_combine() { return env_on("FLUX_FUSED_COMBINE"); }
 //    layer) and the lower HBM power lets the clocks rise: +5% tokens/s on both BASELINE shapes.
 //  * GATHER_TMA (FLUX_GATHER_A=1): TMA tile::gather4 (~5 B/clk/SM: ~2.5x slower GEMM).
 //  * NONE (FLUX_GATHER_A=0, the fused-dequant kernel, the 1-CTA kernel): K2 materialises x_perm.
+// L2 cache policies of the CTA-pair pass kernel (GemmArgs::l2_hints).  Default 1: the act / y_perm
+// output tiles (4.4 / 6.4 GB per DeepSeek-shape layer, consumed by the next kernel long after they
+// left L2) are stored evict_first, which cut the down GEMM's DRAM reads by 1.4 GB per layer (ncu:
+// 12.1 -> 10.7 GB; more A re-reads hit L2).  evict_last on B (2) or evict_first on A (4) raised them
+// (15.3 / 26.8 GB).  FLUX_L2_HINTS overrides for experiments.
+static int l2_hints() {
+  const char* e = getenv("FLUX_L2_HINTS");
+  return e ? atoi(e) : 1;
+}
 enum GatherMode { GATHER_NONE = 0, GATHER_TMA = 1, GATHER_CP = 2 };
 static GatherMode gather_mode(const flux_moe_cfg& c, int64_t T) {
   const char* e = getenv("FLUX_GATHER_A");
@@ -368,6 +377,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.bm = sa.gemm_bm;
   ga.gather_idx = gather_a ? token_index : nullptr;
   ga.gather_cp = gmode == GATHER_CP ? 1 : 0;
+  ga.l2_hints = l2_hints();
   ga.a_src = x;
   ga.a_ld = H;
   GemmArgs gd = ga;

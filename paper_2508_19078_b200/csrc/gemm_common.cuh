@@ -34,6 +34,7 @@ struct Params {
   int gather_cp;               // 1: gather with cp.async (CTA-pair pass kernel) instead of TMA gather4
   const __nv_bfloat16* a_src;  // gather source rows (x) and their stride in elements
   int a_ld;
+  int l2_hints;                // GemmArgs::l2_hints
 };
 
 struct TileInfo {
@@ -380,6 +381,7 @@ inline Params make_params(const GemmArgs& g) {
   p.gather_cp = g.gather_cp;
   p.a_src = reinterpret_cast<const __nv_bfloat16*>(g.a_src);
   p.a_ld = g.a_ld;
+  p.l2_hints = g.l2_hints;
   return p;
 }
 

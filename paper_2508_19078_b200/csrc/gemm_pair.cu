@@ -40,7 +40,8 @@ constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kMiscBytes + 4 * kStag
 // bounded the LLaMA-shape down GEMM.  Same values and roundings as epilogue_slice.
 template <int EPI>
 __device__ __forceinline__ void epilogue_tma(const Params& p, uint32_t taddr, const TileInfo& ti, int up_col,
-                                             const float* sc, const CUtensorMap* tmo, uint32_t stage, int out_row) {
+                                             const float* sc, const CUtensorMap* tmo, uint32_t stage, int out_row,
+                                             bool hint, uint64_t pol) {
   const int N = ti.g < p.E ? p.N_r : p.N_s;
   const uint32_t lane = lane_id();
   constexpr int kChunks = EPI == EPI_SWIGLU ? 2 : 4;  // 64-column output chunks per tile
@@ -99,7 +100,10 @@ __device__ __forceinline__ void epilogue_tma(const Params& p, uint32_t taddr, co
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      tma_store_2d(tmo, stage, col0, out_row);
+      if (hint)
+        tma_store_2d_hint(tmo, stage, col0, out_row, pol);
+      else
+        tma_store_2d(tmo, stage, col0, out_row);
       bulk_commit_group();
     }
   }
@@ -199,6 +203,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tma_prefetch(&tm_a_s);
       tma_prefetch(&tm_b_s);
     }
+    const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
     uint32_t it = 0;
     for (int tile = cid; tile < total; tile += ncl) {
       const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
@@ -222,8 +227,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const bool a_cp = cpg && gather;  // A rows by cp.async: only the B halves are TMA bytes
         if (leader && lane_id() == 0) mbar_arrive_expect_tx(&full[s], a_cp ? 2 * kBBytes : 2 * kStageBytes);
         __syncwarp();  // the transaction count is armed before any of this warp's copies can land
-        if (!a_cp) load_a_pair(st, ta, &full[s], kb, arow, gather, s_idx);  // else: warps 2 and 3
-        if (lane_id() == 0) tma_load_2d_pair(st + kABytes, tb, &full[s], kb * kBK, brow);
+        if (!a_cp) {
+          if ((p.l2_hints & 4) && !gather) {
+            if (lane_id() == 0) tma_load_2d_pair_hint(st, ta, &full[s], kb * kBK, arow, pol_a);
+          } else {
+            load_a_pair(st, ta, &full[s], kb, arow, gather, s_idx);  // else: warps 2 and 3
+          }
+        }
+        if (lane_id() == 0) {
+          if (p.l2_hints & 2)
+            tma_load_2d_pair_hint(st + kABytes, tb, &full[s], kb * kBK, brow, pol_b);
+          else
+            tma_load_2d_pair(st + kABytes, tb, &full[s], kb * kBK, brow);
+        }
       }
       it += nkb;
       __syncwarp();  // s_idx is rewritten for the next tile only after this one was issued
@@ -301,6 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t stage_out = smem_u32(s_out) + q * kStageOutBytes;
+    const uint64_t pol_store = policy_evict_first();
     uint32_t tc = 0;
     for (int tile = cid; tile < total; tile += ncl, ++tc) {
       const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
@@ -312,7 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int half = pair_tile_cols<EPI>(p, ti) / 2;
       if (EPI != EPI_COMBINE && r_warp + 32 <= s_rows[ti.g]) {
         epilogue_tma<EPI>(p, tmem + acc * kBN + lane_base, ti, half, sc, ti.g < p.E ? &tm_o_r : &tm_o_s,
-                          stage_out, s_row0[ti.g] + r_warp);
+                          stage_out, s_row0[ti.g] + r_warp, (p.l2_hints & 1) != 0, pol_store);
       } else {  // a group's last rows (masked per thread) and the fused combine
         const int r_local = r_warp + (int)lane_id();
         epilogue_slice<EPI>(p, tmem + acc * kBN + lane_base, ti, r_local < s_rows[ti.g],

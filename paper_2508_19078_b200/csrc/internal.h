@@ -155,6 +155,8 @@ struct GemmArgs {
   int gather_cp;
   const void* a_src;
   int a_ld;
+  int l2_hints;  // L2 cache policies of the CTA-pair pass kernel: bit 0 = evict_first on the output
+                 // stores, bit 1 = evict_last on the B loads, bit 2 = evict_first on the A loads
 };
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);
