@@ -148,7 +148,7 @@ def main():
     ap.add_argument("--config", default="deepseek_moe")
     ap.add_argument("--tokens", type=int, default=0, help="tokens per GPU (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-tokens", type=int, default=32)  # oracle sample: ~10 s of host CPU work
+    ap.add_argument("--ref-tokens", type=int, default=64)  # oracle sample: ~10 s of host CPU work (16 cores)
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--clusters", type=int, default=0)
     ap.add_argument("--rounds", type=int, default=2,
