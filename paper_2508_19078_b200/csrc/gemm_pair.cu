@@ -24,7 +24,11 @@ constexpr int kHalfM = 128, kPairM = 256, kStages = 6;
 constexpr int kABytes = kHalfM * kBK * 2;     // 16 KB: this CTA's A rows
 constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kThreads = 288;  // 9 warps: TMA, MMA, 2 gather producers, 4 epilogue, gather relay
+// 9 warps for gate/up (TMA, MMA, 2 gather producers, 4 epilogue, gather relay); the other epilogues
+// run without the gather warps' relay: 8 warps, i.e. 2 per SM sub-partition, so each thread may use
+// up to 255 registers (a 9th warp puts 3 warps on one sub-partition and caps them at 168)
+template <int EPI>
+constexpr int kThreadsOf = EPI == EPI_SWIGLU ? 288 : 256;
 // after the ring: barriers, schedule copies, gather ids and scales (< 8 KB), then one 4 KB TMA-store
 // staging buffer per epilogue warp (1024-byte aligned: 128-byte swizzle atoms)
 constexpr int kMiscBytes = 8192;
@@ -109,6 +113,129 @@ __device__ __forceinline__ void epilogue_tma(const Params& p, uint32_t taddr, co
   }
 }
 
+// Fused K6 (EPI_COMBINE, the shared MLP's down GEMM; reading R6, same order and roundings as
+// combine.cu): y[t] = bf16(r_t + bf16(acc_t) + Σ_j w_tj·y_perm[inv_pos_tj]) for this warp's 32 token
+// rows x the tile's 256 columns.  Per 64-column chunk the warp first writes o_sh = bf16(acc·scale)
+// of its rows (one TMEM lane = one row per thread) into its 4 KB staging buffer (128-byte swizzle),
+// then switches to 8 lanes per row: 4 rows per warp instruction, every load of y_perm, of the
+// residual and every store of y a full 128-byte line, two row groups' loads in flight before the
+// first FMA.  Each row's picks (inv_pos, w) are loaded once per tile by the thread that owns the
+// row and handed to the 8 lanes working on it with shuffles.
+__device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __bfloat1622float2(b[i]);
+    f[2 * i] = x.x;
+    f[2 * i + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void epilogue_combine(const Params& p, uint32_t taddr, const TileInfo& ti, const float* sc,
+                                                 uint32_t stage, int r_warp, int rows_in_grp) {
+  const int lane = (int)lane_id();
+  const int H = p.N_s;
+  const int k = p.k;
+  int pos[8];
+  float wt[8];
+  {
+    const int t = r_warp + lane;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      pos[jj] = -1;
+      wt[jj] = 0.f;
+      if (t < rows_in_grp && jj < k) {
+        pos[jj] = __ldg(&p.inv_pos[(int64_t)t * k + jj]);
+        wt[jj] = __ldg(&p.topk_w[(int64_t)t * k + jj]);
+      }
+    }
+  }
+  __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.out_s);
+  const int chunk = lane & 7, sub = lane >> 3;
+  for (int cc = 0; cc < kBN / 64; ++cc) {
+    const int c0 = ti.n * kBN + cc * 64;
+    if (c0 >= H) break;  // warp-uniform (H % 64 == 0)
+    // phase 1: o_sh of this thread's row -> staging row `lane`
+    float v0[16], v1[16], v2[16], v3[16];
+    tmem_ld16(taddr + cc * 64, v0);
+    tmem_ld16(taddr + cc * 64 + 16, v1);
+    tmem_ld16(taddr + cc * 64 + 32, v2);
+    tmem_ld16(taddr + cc * 64 + 48, v3);
+    tmem_ld_wait();
+    const uint32_t row_addr = stage + lane * 128;
+    auto put = [&](float (&v)[16], int h) {
+      if (sc) {
+        float cs[16];
+        lds16(sc + cc * 64 + 16 * h, cs);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= cs[i];
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int c16 = 2 * h + c;
+        st_shared_v4(row_addr + ((c16 ^ (lane & 7)) << 4),
+                     make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                                pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7])));
+      }
+    };
+    put(v0, 0);
+    put(v1, 1);
+    put(v2, 2);
+    put(v3, 3);
+    __syncwarp();
+    // phase 2: 8 lanes per row, rows rr = 4·it + sub, 16-byte column chunk `chunk`; two row groups'
+    // loads are issued before the first FMA (measured: four groups spill at 255 registers and run
+    // 2.5x slower; fetching the picks by shuffle next to each load instead of up front: 2x slower)
+#pragma unroll 1
+    for (int it = 0; it < 8; it += 2) {
+      uint4 rv[2], ov[2][8];
+      int pj[2][8];
+      float wj[2][8];
+      bool ok[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int rr = 4 * (it + u) + sub;
+        const int t = r_warp + rr;
+        ok[u] = t < rows_in_grp;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          pj[u][jj] = __shfl_sync(0xffffffffu, pos[jj], rr);
+          wj[u][jj] = __shfl_sync(0xffffffffu, wt[jj], rr);
+        }
+        if (ok[u]) {
+          rv[u] = __ldg(reinterpret_cast<const uint4*>(p.resid + (int64_t)t * H + c0) + chunk);
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if (jj < k && pj[u][jj] >= 0)  // -1: a pick folded by gate re-routing (NEXT-2)
+              ov[u][jj] = __ldg(reinterpret_cast<const uint4*>(p.y_perm + (int64_t)pj[u][jj] * H + c0) + chunk);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+        const int rr = 4 * (it + u) + sub;
+        const uint4 sv = ld_shared_v4(stage + rr * 128 + ((chunk ^ (rr & 7)) << 4));
+        float acc[8], f[8];
+        unpack_bf16x8(rv[u], acc);
+        unpack_bf16x8(sv, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += f[i];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (jj < k && pj[u][jj] >= 0) {
+            unpack_bf16x8(ov[u][jj], f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = fmaf(wj[u][jj], f[i], acc[i]);
+          }
+        const int t = r_warp + rr;
+        *(reinterpret_cast<uint4*>(y + (int64_t)t * H + c0) + chunk) =
+            make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                       pack_bf16x2(acc[6], acc[7]));
+      }
+    }
+    __syncwarp();  // the staging buffer is rewritten by the next chunk
+  }
+}
+
 // Routed A rows gathered from x with per-lane 16-byte cp.async (LDGSTS) instead of a materialised
 // x_perm: per 64-wide K slice this CTA's 128 rows x 128 bytes are copied by two producer warps
 // (warps 2 and 3, 64 rows each; one warp is issue-bound, and warp 0 keeps the TMA loads of B and
@@ -142,7 +269,7 @@ __device__ __forceinline__ void gather_a_cp(uint8_t* dst, const Params& p, const
 }
 
 template <int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tm_a_r, const __grid_constant__ CUtensorMap tm_a_s,
                              const __grid_constant__ CUtensorMap tm_b_r, const __grid_constant__ CUtensorMap tm_b_s,
                              const __grid_constant__ CUtensorMap tm_o_r, const __grid_constant__ CUtensorMap tm_o_s,
@@ -166,6 +293,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  constexpr int kThreads = kThreadsOf<EPI>;
   for (int i = threadIdx.x; i <= p.n_groups; i += kThreads) s_sched[i] = p.sched[i];
   for (int i = threadIdx.x; i < p.n_groups; i += kThreads) {
     s_row0[i] = p.grp_row0[i];
@@ -327,7 +455,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int r_warp = ti.m * kPairM + (int)rank * kHalfM + q * 32;  // this warp's first row in the group
       const int half = pair_tile_cols<EPI>(p, ti) / 2;
-      if (EPI != EPI_COMBINE && r_warp + 32 <= s_rows[ti.g]) {
+      if constexpr (EPI == EPI_COMBINE) {
+        epilogue_combine(p, tmem + acc * kBN + lane_base, ti, sc, stage_out, r_warp, s_rows[ti.g]);
+      } else if (r_warp + 32 <= s_rows[ti.g]) {
         epilogue_tma<EPI>(p, tmem + acc * kBN + lane_base, ti, half, sc, ti.g < p.E ? &tm_o_r : &tm_o_s,
                           stage_out, s_row0[ti.g] + r_warp, (p.l2_hints & 1) != 0, pol_store);
       } else {  // a group's last rows (masked per thread) and the fused combine
@@ -374,7 +504,8 @@ cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& 
                                  : grouped_gemm_pair_kernel<EPI_COMBINE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (e != cudaSuccess) return e;
-  kern<<<(g.grid / 2) * 2, kThreads, kSmemBytes, st>>>(a_r, a_s, b_r, b_s, o_r, o_s, p);
+  const int threads = epi == EPI_SWIGLU ? kThreadsOf<EPI_SWIGLU> : kThreadsOf<EPI_STORE>;
+  kern<<<(g.grid / 2) * 2, threads, kSmemBytes, st>>>(a_r, a_s, b_r, b_s, o_r, o_s, p);
   return cudaGetLastError();
 }
 
