@@ -9,9 +9,16 @@
 // TMEM.  Versus the 1-CTA kernel this cuts the shared-memory operand traffic
 // per MMA FLOP by a third (each SM stages 32 KB per K slice instead of 48 KB).
 //
+// Warp roles (per CTA): 0 = TMA producer (B halves; A when it comes by TMA), 1 = MMA issuer
+// (leader CTA only), 2-3 = cp.async gather producers of the routed A rows (gate/up only; warp 2
+// also allocates TMEM), 4-7 = epilogue (TMEM lane quadrant warp % 4), 8 = gather relay (gate/up
+// only: the other epilogues launch 8 warps and keep 255 registers per thread).
+//
 // Synchronisation: full[s] lives in the leader (TMA bytes of both CTAs complete
-// on it; the leader's producer arms it with the pair's byte count); empty[s] and
+// on it; the leader's producer arms it with the pair's byte count; with the
+// cp.async gather it also takes one relay arrive per CTA); empty[s] and
 // tfull[a] exist in both CTAs and are signalled by a multicast tcgen05.commit;
+// afull[s] is CTA-local (64 cp.async noinc arrivals of the gather warps);
 // tempty[a] lives in the leader and collects one arrive per epilogue warp of
 // both CTAs.  The tile loop runs per cluster (static round-robin over 74 pairs).
 #include "gemm_common.cuh"
