@@ -61,44 +61,56 @@ __device__ __forceinline__ void epilogue_tma(const Params& p, uint32_t taddr, co
     const int col0 = (EPI == EPI_SWIGLU ? ti.n * (kBN / 2) : ti.n * kBN) + j0;
     if ((EPI == EPI_SWIGLU && j0 >= up_col) || col0 >= N) break;  // warp-uniform
     uint32_t pk[32];
+    // TMEM loads are batched before one wait: all four 16-column groups of the chunk (STORE) or two
+    // gate + two up groups (SWIGLU, whose 9-warp kernel is capped at 168 registers)
+    constexpr int kBatch = EPI == EPI_SWIGLU ? 2 : 4;
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const int j = j0 + 16 * h;
-      const bool live = (EPI != EPI_SWIGLU || j < up_col) && col0 + 16 * h < N;  // warp-uniform
-      if (!live) {
+    for (int h0 = 0; h0 < 4; h0 += kBatch) {
+      float gv[kBatch][16], uv[kBatch][16];
+      bool live[kBatch];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) pk[8 * h + i] = 0u;
-        continue;
+      for (int b = 0; b < kBatch; ++b) {
+        const int j = j0 + 16 * (h0 + b);
+        live[b] = (EPI != EPI_SWIGLU || j < up_col) && col0 + 16 * (h0 + b) < N;  // warp-uniform
+        if (live[b]) {
+          tmem_ld16(taddr + j, gv[b]);
+          if constexpr (EPI == EPI_SWIGLU) tmem_ld16(taddr + up_col + j, uv[b]);
+        }
       }
-      if constexpr (EPI == EPI_SWIGLU) {
-        float gv[16], uv[16];
-        tmem_ld16(taddr + j, gv);
-        tmem_ld16(taddr + up_col + j, uv);
-        tmem_ld_wait();
-        if (sc) {
-          float gs[16], us[16];
-          lds16(sc + j, gs);
-          lds16(sc + 256 + j, us);
+      tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            gv[i] *= gs[i];
-            uv[i] *= us[i];
+      for (int b = 0; b < kBatch; ++b) {
+        const int h = h0 + b;
+        const int j = j0 + 16 * h;
+        if (!live[b]) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pk[8 * h + i] = 0u;
+          continue;
+        }
+        if constexpr (EPI == EPI_SWIGLU) {
+          if (sc) {
+            float gs[16], us[16];
+            lds16(sc + j, gs);
+            lds16(sc + 256 + j, us);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              gv[b][i] *= gs[i];
+              uv[b][i] *= us[i];
+            }
           }
+#pragma unroll
+          for (int i = 0; i < 16; i += 2)
+            pk[8 * h + i / 2] = pack_bf16x2(silu(gv[b][i]) * uv[b][i], silu(gv[b][i + 1]) * uv[b][i + 1]);
+        } else {
+          if (sc) {
+            float cs[16];
+            lds16(sc + j, cs);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) gv[b][i] *= cs[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) pk[8 * h + i / 2] = pack_bf16x2(gv[b][i], gv[b][i + 1]);
         }
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) pk[8 * h + i / 2] = pack_bf16x2(silu(gv[i]) * uv[i], silu(gv[i + 1]) * uv[i + 1]);
-      } else {
-        float v[16];
-        tmem_ld16(taddr + j, v);
-        tmem_ld_wait();
-        if (sc) {
-          float cs[16];
-          lds16(sc + j, cs);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] *= cs[i];
-        }
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) pk[8 * h + i / 2] = pack_bf16x2(v[i], v[i + 1]);
       }
     }
     if (lane == 0) bulk_wait_group_read0();  // the previous chunk's store has read the buffer
