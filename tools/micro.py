@@ -106,6 +106,8 @@ def layer(name="deepseek_moe"):
     from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
     from paper_2508_19078_b200 import synthetic
     cfg = synth.CONFIGS[name].with_(n_layers=1)
+    if os.environ.get("MICRO_TOKENS"):  # token-count override for scaling experiments
+        cfg = cfg.with_(tokens=int(os.environ["MICRO_TOKENS"]))
     shape = ModelShape.of(cfg)
     qm = QuantizedModel(shape)
     qm.quantize_from(synthetic.master_weights(cfg))
