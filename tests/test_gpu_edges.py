@@ -67,3 +67,30 @@ def test_degenerate_case_parity(name):
     if name == "hot_expert":  # the case is only covered if it really produced empty and hot experts
         h0 = prof.hist[0].cpu().numpy()
         assert (h0 == 0).sum() >= 2 and h0.max() >= 0.4 * T, h0
+
+
+@pytest.mark.parametrize("name", list(EDGE))
+def test_degenerate_cases_on_every_gemm_path(name, monkeypatch):
+    """Small batches take the fused-dequant GEMM with materialised x_perm by policy; the same degenerate
+    inputs through the dequant-pass CTA-pair GEMM (routed rows gathered in-kernel with cp.async, or
+    materialised) must give bit-identical outputs, ids and histograms."""
+    from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
+    from paper_2508_19078_b200 import synthetic
+    cfg = EDGE[name]
+    shape = ModelShape.of(cfg)
+    qm = QuantizedModel(shape)
+    qm.quantize_from(synthetic.master_weights(cfg))
+    x = synthetic.tokens(cfg, 0, cfg.tokens)
+    outs = []
+    for env in ({"FLUX_GEMM_FUSED_DEQUANT": "1"}, {"FLUX_GEMM_DEQUANT_PASS": "1"},
+                {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GATHER_A": "0"}, {"FLUX_GEMM_1SM": "1"}):
+        for k in ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM", "FLUX_GATHER_A"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        prof = Profiler(shape, cfg.tokens)
+        prof.run(qm, x)
+        torch.cuda.synchronize()
+        outs.append((prof.y[(cfg.n_layers - 1) % 2].clone(), prof.ids.clone(), prof.hist.clone()))
+    for y, ids, hist in outs[1:]:
+        assert torch.equal(y, outs[0][0]) and torch.equal(ids, outs[0][1]) and torch.equal(hist, outs[0][2])
