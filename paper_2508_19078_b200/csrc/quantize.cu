@@ -10,8 +10,8 @@
 // HBM-bound: a team of TS lanes owns one (row, group) = one g-element slice of w (items are
 // consecutive slices, item i starts at element i·g); every lane holds CPL 16-byte chunks of it in
 // registers, the team max-reduces with shuffles, then each lane writes its packed codes.  The
-// common path computes fl32(w/s) exactly with three FMA-pipe operations per element (no division,
-// no float->int conversion, no branch).
+// common path computes fl32(w/s) exactly with three FMA-pipe operations per element pair (packed
+// f32x2; no division, no float->int conversion, no branch).
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -69,6 +69,30 @@ __device__ __forceinline__ void store_codes(uint8_t* q, int64_t e0, const uint32
       *reinterpret_cast<uint32_t*>(q + e0 / 2) = __byte_perm(xl, xh, 0x6420);
     }
   }
+}
+
+// Packed fp32 pairs (sm_100 FFMA2 / FMUL2 / FADD2): IEEE round-to-nearest per lane, subnormals kept
+// (no .ftz), so each lane is bit-identical to the scalar __fmul_rn / __fmaf_rn / __fadd_rn.
+__device__ __forceinline__ float2 mul2_rn(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fma2_rn(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 add2_rn(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
 }
 
 // The definition itself, per element (IEEE division, RNE conversion, clamp): groups with a zero,
@@ -144,13 +168,18 @@ __global__ void __launch_bounds__(256) quantize_kernel(const void* __restrict__ 
         continue;
       }
       uint32_t tb[8];
+      // two elements per packed op: q0 = w·y, r = q0·(−s) + w (= −q0·s + w exactly), q1 = r·y + q0,
+      // t = q1 + 1.5·2^23 — the same per-lane roundings as the scalar sequence
+      const float2 y2 = make_float2(rcp, rcp), ns2 = make_float2(-sc, -sc), m2 = make_float2(kMagic, kMagic);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float x = elem(ch[i], j);
-        const float q0 = __fmul_rn(x, rcp);
-        const float r = __fmaf_rn(-q0, sc, x);
-        const float q1 = __fmaf_rn(r, rcp, q0);
-        tb[j] = __float_as_uint(__fadd_rn(q1, kMagic));
+      for (int j = 0; j < 8; j += 2) {
+        const float2 x = make_float2(elem(ch[i], j), elem(ch[i], j + 1));
+        const float2 q0 = mul2_rn(x, y2);
+        const float2 r = fma2_rn(q0, ns2, x);
+        const float2 q1 = fma2_rn(r, y2, q0);
+        const float2 t = add2_rn(q1, m2);
+        tb[j] = __float_as_uint(t.x);
+        tb[j + 1] = __float_as_uint(t.y);
       }
       store_codes<WBITS>(q, base + c * 8, tb);
     }
