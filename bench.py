@@ -414,7 +414,12 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "gemm_gate_up (K3+K5)", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "peak_source": peak_src + ", bf16 sustained",
-                         "flop_per_launch": flop_gu},
+                         "flop_per_launch": flop_gu,
+                         # context for power-capped runs: the dense bf16 MMA peak at the median SM clock
+                         # seen under load (148 SMs x 8192 FLOP/clk/SM = 2.25 PFLOP/s at 1.856 GHz)
+                         "peak_at_clock": (148 * 8192 * clk["sm_mhz"] * 1e6 / 1e12) if clk else None,
+                         "frac_at_clock": (achieved / (148 * 8192 * clk["sm_mhz"] * 1e6 / 1e12))
+                         if (clk and achieved) else None},
             "e2e": {"value": T_total * args.steps / (ms_e2e / 1000.0), "unit": "tokens/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
