@@ -41,7 +41,8 @@ constexpr int kThreadsOf = EPI == EPI_SWIGLU ? 288 : 256;
 constexpr int kMiscBytes = 8192;
 static_assert(256 + 3 * kMaxGroups * 4 + 16 + 128 * 4 + kScaleSmemBytes <= kMiscBytes, "smem layout");
 constexpr int kStageOutBytes = 4096;  // 32 rows x 64 bf16 columns
-constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kMiscBytes + 4 * kStageOutBytes;
+constexpr int kPickBytes = 32 * 64;  // per epilogue warp: 32 rows x (8 inv_pos + 8 gate weights), fused combine
+constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kMiscBytes + 4 * kStageOutBytes + 4 * kPickBytes;
 
 // TMA-store epilogue of one 32-row slice (a warp's TMEM lanes) whose rows all lie inside the group:
 // per 64-column chunk the warp converts its accumulator columns to bf16, writes them to its staging
@@ -132,14 +133,6 @@ __device__ __forceinline__ void epilogue_tma(const Params& p, uint32_t taddr, co
   }
 }
 
-// Fused K6 (EPI_COMBINE, the shared MLP's down GEMM; reading R6, same order and roundings as
-// combine.cu): y[t] = bf16(r_t + bf16(acc_t) + Σ_j w_tj·y_perm[inv_pos_tj]) for this warp's 32 token
-// rows x the tile's 256 columns.  Per 64-column chunk the warp first writes o_sh = bf16(acc·scale)
-// of its rows (one TMEM lane = one row per thread) into its 4 KB staging buffer (128-byte swizzle),
-// then switches to 8 lanes per row: 4 rows per warp instruction, every load of y_perm, of the
-// residual and every store of y a full 128-byte line, two row groups' loads in flight before the
-// first FMA.  Each row's picks (inv_pos, w) are loaded once per tile by the thread that owns the
-// row and handed to the 8 lanes working on it with shuffles.
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
   const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
@@ -149,31 +142,44 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
     f[2 * i + 1] = x.y;
   }
 }
+
+// Fused K6 (EPI_COMBINE, the shared MLP's down GEMM; reading R6, same order and roundings as
+// combine.cu): y[t] = bf16(r_t + bf16(acc_t) + Σ_j w_tj·y_perm[inv_pos_tj]) for this warp's 32 token
+// rows x the tile's 256 columns.  Per tile each thread puts its row's picks (inv_pos, w) in the
+// warp's 2 KB pick table; per 64-column chunk the warp writes o_sh = bf16(acc·scale) of its rows
+// (one TMEM lane = one row per thread) into its 4 KB staging buffer (128-byte swizzle), then
+// switches to 8 lanes per row: 4 rows per warp instruction, every load of y_perm and of the residual
+// and every store of y a full 128-byte line, four row groups' loads in flight before the first FMA.
 __device__ __forceinline__ void epilogue_combine(const Params& p, uint32_t taddr, const TileInfo& ti, const float* sc,
-                                                 uint32_t stage, int r_warp, int rows_in_grp) {
+                                                 uint32_t stage, uint32_t picks, int r_warp, int rows_in_grp) {
   const int lane = (int)lane_id();
   const int H = p.N_s;
   const int k = p.k;
-  int pos[8];
-  float wt[8];
   {
     const int t = r_warp + lane;
+    uint32_t pv[8], wv[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
-      pos[jj] = -1;
-      wt[jj] = 0.f;
+      int pos = -1;
+      float wt = 0.f;
       if (t < rows_in_grp && jj < k) {
-        pos[jj] = __ldg(&p.inv_pos[(int64_t)t * k + jj]);
-        wt[jj] = __ldg(&p.topk_w[(int64_t)t * k + jj]);
+        pos = __ldg(&p.inv_pos[(int64_t)t * k + jj]);  // -1: a pick folded by gate re-routing (NEXT-2)
+        wt = __ldg(&p.topk_w[(int64_t)t * k + jj]);
       }
+      pv[jj] = (uint32_t)pos;
+      wv[jj] = __float_as_uint(wt);
     }
+    const uint32_t row = picks + lane * 64;
+    st_shared_v4(row, make_uint4(pv[0], pv[1], pv[2], pv[3]));
+    st_shared_v4(row + 16, make_uint4(pv[4], pv[5], pv[6], pv[7]));
+    st_shared_v4(row + 32, make_uint4(wv[0], wv[1], wv[2], wv[3]));
+    st_shared_v4(row + 48, make_uint4(wv[4], wv[5], wv[6], wv[7]));
   }
   __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(p.out_s);
   const int chunk = lane & 7, sub = lane >> 3;
-  for (int cc = 0; cc < kBN / 64; ++cc) {
-    const int c0 = ti.n * kBN + cc * 64;
-    if (c0 >= H) break;  // warp-uniform (H % 64 == 0)
-    // phase 1: o_sh of this thread's row -> staging row `lane`
+  const int n_chunks = min(kBN / 64, (H - ti.n * kBN) / 64);  // H % 64 == 0
+  // phase 1 of chunk cc: o_sh of this thread's row -> staging row `lane`
+  auto stage_chunk = [&](int cc) {
     float v0[16], v1[16], v2[16], v3[16];
     tmem_ld16(taddr + cc * 64, v0);
     tmem_ld16(taddr + cc * 64 + 16, v1);
@@ -200,39 +206,47 @@ __device__ __forceinline__ void epilogue_combine(const Params& p, uint32_t taddr
     put(v1, 1);
     put(v2, 2);
     put(v3, 3);
-    __syncwarp();
-    // phase 2: 8 lanes per row, rows rr = 4·it + sub, 16-byte column chunk `chunk`; two row groups'
-    // loads are issued before the first FMA (measured: four groups spill at 255 registers and run
-    // 2.5x slower; fetching the picks by shuffle next to each load instead of up front: 2x slower)
+  };
+  // phase 2 per chunk: 8 lanes per row, rows rr = 4·group + sub, 16-byte column chunk `chunk`; four
+  // row groups' loads are issued before the first FMA (measured: 4.1 ms/layer for the fused shared
+  // down + combine; two groups 4.3; two groups software-pipelined across chunks 4.9)
+  __syncwarp();  // the pick table is visible to the whole warp
+  constexpr int kRowsInFlight = 4;
+  for (int cc = 0; cc < n_chunks; ++cc) {
+    const int c0 = ti.n * kBN + cc * 64;
+    stage_chunk(cc);
+    __syncwarp();  // staging rows are visible to the whole warp
 #pragma unroll 1
-    for (int it = 0; it < 8; it += 2) {
-      uint4 rv[2], ov[2][8];
-      int pj[2][8];
-      float wj[2][8];
-      bool ok[2];
+    for (int it = 0; it < 8; it += kRowsInFlight) {
+      uint4 rv[kRowsInFlight], ov[kRowsInFlight][8];
+      uint32_t live[kRowsInFlight];  // bit jj: pick jj has a y_perm row
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kRowsInFlight; ++u) {
         const int rr = 4 * (it + u) + sub;
         const int t = r_warp + rr;
-        ok[u] = t < rows_in_grp;
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          pj[u][jj] = __shfl_sync(0xffffffffu, pos[jj], rr);
-          wj[u][jj] = __shfl_sync(0xffffffffu, wt[jj], rr);
-        }
-        if (ok[u]) {
+        live[u] = 0;
+        if (t < rows_in_grp) {
           rv[u] = __ldg(reinterpret_cast<const uint4*>(p.resid + (int64_t)t * H + c0) + chunk);
+          const uint4 pa = ld_shared_v4(picks + rr * 64), pb = ld_shared_v4(picks + rr * 64 + 16);
+          const int pj[8] = {(int)pa.x, (int)pa.y, (int)pa.z, (int)pa.w, (int)pb.x, (int)pb.y, (int)pb.z, (int)pb.w};
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj)
-            if (jj < k && pj[u][jj] >= 0)  // -1: a pick folded by gate re-routing (NEXT-2)
-              ov[u][jj] = __ldg(reinterpret_cast<const uint4*>(p.y_perm + (int64_t)pj[u][jj] * H + c0) + chunk);
+            if (jj < k && pj[jj] >= 0) {  // -1: a pick folded by gate re-routing (NEXT-2)
+              ov[u][jj] = __ldg(reinterpret_cast<const uint4*>(p.y_perm + (int64_t)pj[jj] * H + c0) + chunk);
+              live[u] |= 1u << jj;
+            }
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!ok[u]) continue;
+      for (int u = 0; u < kRowsInFlight; ++u) {
         const int rr = 4 * (it + u) + sub;
+        const int t = r_warp + rr;
+        if (t >= rows_in_grp) continue;
         const uint4 sv = ld_shared_v4(stage + rr * 128 + ((chunk ^ (rr & 7)) << 4));
+        const uint4 wa = ld_shared_v4(picks + rr * 64 + 32), wb = ld_shared_v4(picks + rr * 64 + 48);
+        const float wj[8] = {__uint_as_float(wa.x), __uint_as_float(wa.y), __uint_as_float(wa.z),
+                             __uint_as_float(wa.w), __uint_as_float(wb.x), __uint_as_float(wb.y),
+                             __uint_as_float(wb.z), __uint_as_float(wb.w)};
         float acc[8], f[8];
         unpack_bf16x8(rv[u], acc);
         unpack_bf16x8(sv, f);
@@ -240,12 +254,11 @@ __device__ __forceinline__ void epilogue_combine(const Params& p, uint32_t taddr
         for (int i = 0; i < 8; ++i) acc[i] += f[i];
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj)
-          if (jj < k && pj[u][jj] >= 0) {
+          if (live[u] & (1u << jj)) {
             unpack_bf16x8(ov[u][jj], f);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = fmaf(wj[u][jj], f[i], acc[i]);
+            for (int i = 0; i < 8; ++i) acc[i] = fmaf(wj[jj], f[i], acc[i]);
           }
-        const int t = r_warp + rr;
         *(reinterpret_cast<uint4*>(y + (int64_t)t * H + c0) + chunk) =
             make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
                        pack_bf16x2(acc[6], acc[7]));
@@ -475,7 +488,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
       const int r_warp = ti.m * kPairM + (int)rank * kHalfM + q * 32;  // this warp's first row in the group
       const int half = pair_tile_cols<EPI>(p, ti) / 2;
       if constexpr (EPI == EPI_COMBINE) {
-        epilogue_combine(p, tmem + acc * kBN + lane_base, ti, sc, stage_out, r_warp, s_rows[ti.g]);
+        epilogue_combine(p, tmem + acc * kBN + lane_base, ti, sc, stage_out,
+                         smem_u32(s_out) + 4 * kStageOutBytes + q * kPickBytes, r_warp, s_rows[ti.g]);
       } else if (r_warp + 32 <= s_rows[ti.g]) {
         epilogue_tma<EPI>(p, tmem + acc * kBN + lane_base, ti, half, sc, ti.g < p.E ? &tm_o_r : &tm_o_s,
                           stage_out, s_row0[ti.g] + r_warp, (p.l2_hints & 1) != 0, pol_store);
