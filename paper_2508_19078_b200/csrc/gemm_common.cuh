@@ -35,6 +35,7 @@ struct Params {
   const __nv_bfloat16* a_src;  // gather source rows (x) and their stride in elements
   int a_ld;
   int l2_hints;                // GemmArgs::l2_hints
+  int32_t* tile_ctr;           // GemmArgs::tile_ctr
 };
 
 struct TileInfo {
@@ -382,6 +383,7 @@ inline Params make_params(const GemmArgs& g) {
   p.a_src = reinterpret_cast<const __nv_bfloat16*>(g.a_src);
   p.a_ld = g.a_ld;
   p.l2_hints = g.l2_hints;
+  p.tile_ctr = g.tile_ctr;
   return p;
 }
 

@@ -42,7 +42,12 @@ constexpr int kMiscBytes = 8192;
 static_assert(256 + 3 * kMaxGroups * 4 + 16 + 128 * 4 + kScaleSmemBytes <= kMiscBytes, "smem layout");
 constexpr int kStageOutBytes = 4096;  // 32 rows x 64 bf16 columns
 constexpr int kPickBytes = 32 * 64;  // per epilogue warp: 32 rows x (8 inv_pos + 8 gate weights), fused combine
-constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kMiscBytes + 4 * kStageOutBytes + 4 * kPickBytes;
+// dynamic tile claiming: a ring of claimed tile ids with full/empty barriers (after the pick tables)
+constexpr int kTileSlots = 8;
+constexpr int kTileRingBytes = 256;
+static_assert(2 * kTileSlots * 8 + kTileSlots * 4 <= kTileRingBytes, "tile ring");
+constexpr int kSmemBytes =
+    1024 + kStages * kStageBytes + kMiscBytes + 4 * kStageOutBytes + 4 * kPickBytes + kTileRingBytes;
 
 // TMA-store epilogue of one 32-row slice (a warp's TMEM lanes) whose rows all lie inside the group:
 // per 64-column chunk the warp converts its accumulator columns to bf16, writes them to its staging
@@ -321,6 +326,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
       reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(s_rows + kMaxGroups) + 15) & ~uintptr_t(15));
   float* s_scales = reinterpret_cast<float*>(s_idx + 128);  // [2][kScaleFloats] (stage_tile_scales)
   uint8_t* s_out = smem + kStages * kStageBytes + kMiscBytes;  // [4 warps][kStageOutBytes]
+  uint64_t* tid_full = reinterpret_cast<uint64_t*>(s_out + 4 * kStageOutBytes + 4 * kPickBytes);  // [kTileSlots]
+  uint64_t* tid_empty = tid_full + kTileSlots;  // [kTileSlots], the leader's are the ones used
+  int32_t* s_tid = reinterpret_cast<int32_t*>(tid_empty + kTileSlots);  // [kTileSlots]
 
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();
@@ -340,6 +348,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
       mbar_init(&empty[s], 1);
       mbar_init(&afull[s], 32 * kGatherParts);
     }
+    // tile-id consumers per slot, both CTAs: warp 0 of CTA 1, the MMA warp of CTA 0, 4 + 4 epilogue
+    // warps, and with the cp.async gather 2 + 2 gather warps and 2 relays
+    for (int s = 0; s < kTileSlots; ++s) {
+      mbar_init(&tid_full[s], 1);
+      mbar_init(&tid_empty[s], 10 + (cpg ? 6 : 0));
+    }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);
@@ -354,6 +368,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
   const int total = s_sched[p.n_groups];
   const int nkb_r = (p.K_r + kBK - 1) / kBK, nkb_s = (p.K_s + kBK - 1) / kBK;
   const int cid = (int)cluster_id_x(), ncl = (int)ncluster_x();
+  // The pair's tile sequence: static round-robin (tile i of this pair = cid + i·ncl), or, with
+  // p.tile_ctr, claimed in global order by the leader's producer warp (atomicAdd) and published to
+  // every role of both CTAs through a ring of tile ids — concurrent pairs then always work on
+  // neighbouring tiles (the n-tiles of one m-tile together), however far their speeds drift.
+  const bool dyn = p.tile_ctr != nullptr;
+  // Publishing: the leader writes the id into its ring and arrives on its tid_full, and st.async's
+  // it into CTA 1's ring, completing 4 transaction bytes on CTA 1's tid_full (no memory barrier on
+  // the publishing warp, which also issues the TMA loads).
+  auto read_tile = [&](int i) -> int {  // one lane: the i-th tile id published to this CTA
+    const int slot = i % kTileSlots;
+    mbar_wait(&tid_full[slot], (i / kTileSlots) & 1);  // CTA 1: completed by the peer's st.async
+    return *reinterpret_cast<volatile int32_t*>(&s_tid[slot]);
+  };
+  // Called once the id read by read_tile(i) has been consumed (so the load has completed): frees the
+  // slot.  A plain arrive (no cluster-scope release: that would be a MEMBAR draining every in-flight
+  // cp.async of the gather warps at each tile boundary).
+  auto release_tile = [&](int i) {
+    const int slot = i % kTileSlots;
+    if (leader)
+      mbar_arrive(&tid_empty[slot]);
+    else
+      mbar_arrive_cluster(mapa(smem_u32(&tid_empty[slot]), 0));
+  };
+  auto next_tile = [&](int i) -> int {  // whole warp; -1 = done
+    if (!dyn) {
+      const int t = cid + i * ncl;
+      return t < total ? t : -1;
+    }
+    int t = 0;
+    if (lane_id() == 0) t = read_tile(i);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (lane_id() == 0) release_tile(i);
+    return t;
+  };
+  // Leader's warp 0 (lane 0) publishes one tile ahead: at iteration i it publishes tile i + 1 (so
+  // CTA 1's producer learns it while both CTAs still load tile i — publishing at the tile boundary
+  // cost ~7%) and claims tile i + 2, whose atomic round trip overlaps this tile's loads.
+  const bool dyn_static = dyn && (p.l2_hints & 64);  // diagnostic: the ring with the static order
+  int n_claims = 0, cur = 0, pending = 0;
+  auto claim = [&]() -> int {
+    const int c = dyn_static ? cid + (n_claims++) * ncl : atomicAdd(p.tile_ctr, 1);
+    return c < total ? c : -1;
+  };
+  auto publish = [&](int i, int t) {
+    const int slot = i % kTileSlots;
+    mbar_wait(&tid_empty[slot], ((i / kTileSlots) & 1) ^ 1);  // every consumer has read slot's last id
+    s_tid[slot] = t;
+    mbar_arrive(&tid_full[slot]);
+    const uint32_t peer_full = mapa(smem_u32(&tid_full[slot]), 1);
+    mbar_arrive_expect_tx_cluster(peer_full, 4);
+    st_async_u32(mapa(smem_u32(&s_tid[slot]), 1), (uint32_t)t, peer_full);
+  };
+  if (dyn && leader && warp == 0 && lane_id() == 0) {
+    cur = claim();
+    publish(0, cur);
+    pending = cur >= 0 ? claim() : -1;
+  }
+  auto claim_tile = [&](int i) -> int {  // whole warp 0 of the leader: the i-th tile of this pair
+    int t = 0;
+    if (lane_id() == 0) {
+      t = cur;
+      if (t >= 0) {
+        publish(i + 1, pending);
+        cur = pending;
+        if (pending >= 0) pending = claim();
+      }
+    }
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
 
   if (warp == 0) {
     // whole warp: it stages gathered row ids; lane 0 issues the TMA
@@ -365,7 +448,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
     }
     const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
     uint32_t it = 0;
-    for (int tile = cid; tile < total; tile += ncl) {
+    for (int i = 0;; ++i) {
+      const int tile = dyn && leader ? claim_tile(i) : next_tile(i);
+      if (tile < 0) break;
       const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
       const bool routed = ti.g < p.E;
       const bool gather = routed && p.gather_idx != nullptr;
@@ -407,7 +492,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
   } else if (warp == 1) {
     if (leader) {
       uint32_t it = 0, tc = 0;
-      for (int tile = cid; tile < total; tile += ncl, ++tc) {
+      for (int i = 0;; ++i, ++tc) {
+        const int tile = next_tile(i);
+        if (tile < 0) break;
         const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
         const int nkb = ti.g < p.E ? nkb_r : nkb_s;
         const int K = ti.g < p.E ? p.K_r : p.K_s;
@@ -441,7 +528,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
     if (cpg) {
       const int part = warp - 2;
       uint32_t it = 0;
-      for (int tile = cid; tile < total; tile += ncl) {
+      for (int i = 0;; ++i) {
+        const int tile = next_tile(i);
+        if (tile < 0) break;
         const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
         const bool gather = ti.g < p.E;
         const int nkb = gather ? nkb_r : nkb_s;
@@ -461,7 +550,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
     if (cpg && lane_id() == 0) {
       const uint32_t full_leader0 = mapa(smem_u32(&full[0]), 0);
       uint32_t it = 0;
-      for (int tile = cid; tile < total; tile += ncl) {
+      for (int i = 0;; ++i) {
+        int tile = cid + i * ncl < total ? cid + i * ncl : -1;
+        if (dyn) {
+          tile = read_tile(i);
+          if (tile >= -1) release_tile(i);  // (always true: makes the release depend on the loaded id)
+        }
+        if (tile < 0) break;
         const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
         const int nkb = ti.g < p.E ? nkb_r : nkb_s;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -479,7 +574,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
     const uint32_t stage_out = smem_u32(s_out) + q * kStageOutBytes;
     const uint64_t pol_store = policy_evict_first();
     uint32_t tc = 0;
-    for (int tile = cid; tile < total; tile += ncl, ++tc) {
+    for (int i = 0;; ++i, ++tc) {
+      const int tile = next_tile(i);
+      if (tile < 0) break;
       const TileInfo ti = decode(tile, s_sched, p.n_groups, p.n_tiles_r, p.n_tiles_s, p.E);
       const uint32_t acc = tc & 1, aph = (tc >> 1) & 1;
       const float* sc = stage_tile_scales<EPI>(p, ti, s_scales, tc, (int)threadIdx.x - 128);

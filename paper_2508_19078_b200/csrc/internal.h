@@ -99,7 +99,7 @@ struct ScheduleArgs {
   int32_t* tile_base;       // [n_tiles][E]
   int32_t* offsets;         // [E+1] internal
   int32_t* user_offsets;    // [E+1] or null
-  int32_t* done_counter;    // 1 int, zeroed by the launcher
+  int32_t* done_counter;    // 4 ints zeroed by the launcher: [0] K2 ticket, [1..3] pair-GEMM tile counters
   int has_shared;
   int n_tiles_gu, n_tiles_gu_sh;  // n-tiles of the gate/up GEMM (routed, shared)
   int n_tiles_dn, n_tiles_dn_sh;  // n-tiles of the down GEMM
@@ -155,6 +155,7 @@ struct GemmArgs {
   int gather_cp;
   const void* a_src;
   int a_ld;
+  int32_t* tile_ctr;  // CTA-pair kernels: zeroed int the pair leaders claim tiles from (null = static)
   int l2_hints;  // L2 cache policies of the CTA-pair pass kernel: bit 0 = evict_first on the output
                  // stores, bit 1 = evict_last on the B loads, bit 2 = evict_first on the A loads
 };

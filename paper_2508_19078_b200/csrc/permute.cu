@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
 }  // namespace
 
 cudaError_t launch_schedule(const ScheduleArgs& a, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(a.done_counter, 0, sizeof(int32_t), st);
+  cudaError_t e = cudaMemsetAsync(a.done_counter, 0, 4 * sizeof(int32_t), st);  // + the GEMM tile counters
   if (e != cudaSuccess) return e;
   schedule_kernel<<<a.E, 256, 0, st>>>(a);
   return cudaGetLastError();

@@ -83,8 +83,10 @@ def test_degenerate_cases_on_every_gemm_path(name, monkeypatch):
     x = synthetic.tokens(cfg, 0, cfg.tokens)
     outs = []
     for env in ({"FLUX_GEMM_FUSED_DEQUANT": "1"}, {"FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GATHER_A": "0"}, {"FLUX_GEMM_1SM": "1"}):
-        for k in ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM", "FLUX_GATHER_A"):
+                {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GATHER_A": "0"}, {"FLUX_GEMM_1SM": "1"},
+                {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GEMM_DYNAMIC": "0"}):
+        for k in ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM", "FLUX_GATHER_A",
+                  "FLUX_GEMM_DYNAMIC"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)

@@ -135,9 +135,14 @@ def test_weight_paths_bit_identical(name, monkeypatch):
                 {"FLUX_GATHER_A": "1", "FLUX_GEMM_FUSED_DEQUANT": "1"},
                 {"FLUX_GATHER_A": "1", "FLUX_GEMM_DEQUANT_PASS": "1"},
                 {"FLUX_GATHER_A": "2", "FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GATHER_A": "0", "FLUX_GEMM_DEQUANT_PASS": "1"}):
+                {"FLUX_GATHER_A": "0", "FLUX_GEMM_DEQUANT_PASS": "1"},
+                {"FLUX_GEMM_DYNAMIC": "1", "FLUX_GEMM_DEQUANT_PASS": "1"},
+                {"FLUX_GEMM_DYNAMIC": "1", "FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_FUSED_COMBINE": "1"},
+                {"FLUX_GEMM_DYNAMIC": "1", "FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GATHER_A": "0"},
+                {"FLUX_GEMM_DYNAMIC": "0", "FLUX_GEMM_DEQUANT_PASS": "1"},
+                {"FLUX_GEMM_DYNAMIC": "0", "FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_FUSED_COMBINE": "1"}):
         for k in ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM", "FLUX_FUSED_COMBINE",
-                  "FLUX_GATHER_A"):
+                  "FLUX_GATHER_A", "FLUX_GEMM_DYNAMIC"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
