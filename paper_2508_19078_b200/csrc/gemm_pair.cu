@@ -20,7 +20,9 @@
 // tfull[a] exist in both CTAs and are signalled by a multicast tcgen05.commit;
 // afull[s] is CTA-local (64 cp.async noinc arrivals of the gather warps);
 // tempty[a] lives in the leader and collects one arrive per epilogue warp of
-// both CTAs.  The tile loop runs per cluster (static round-robin over 74 pairs).
+// both CTAs.  The tile loop runs per cluster: tiles claimed in global order from an atomic counter
+// (tid_full / tid_empty ring of claimed ids, see claim_tile / next_tile) or, with a null counter, the static
+// round-robin over the 74 pairs.
 #include "gemm_common.cuh"
 
 namespace flux {
