@@ -407,10 +407,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
   // Leader's warp 0 (lane 0) publishes one tile ahead: at iteration i it publishes tile i + 1 (so
   // CTA 1's producer learns it while both CTAs still load tile i — publishing at the tile boundary
   // cost ~7%) and claims tile i + 2, whose atomic round trip overlaps this tile's loads.
-  const bool dyn_static = dyn && (p.l2_hints & 64);  // diagnostic: the ring with the static order
-  int n_claims = 0, cur = 0, pending = 0;
+  int cur = 0, pending = 0;
   auto claim = [&]() -> int {
-    const int c = dyn_static ? cid + (n_claims++) * ncl : atomicAdd(p.tile_ctr, 1);
+    const int c = atomicAdd(p.tile_ctr, 1);
     return c < total ? c : -1;
   };
   auto publish = [&](int i, int t) {
