@@ -114,7 +114,20 @@ typedef struct {
   float* router_logits;
 } flux_layer_out;
 
-/* Workspace bytes flux_profile_layer needs for T tokens (host function). */
+/* Workspace bytes flux_profile_layer needs for T tokens (host function).  The size depends on the
+ * GEMM path the library picks (below), so query it under the same environment as the calls.
+ *
+ * Performance policies of flux_profile_layer (environment variables read per call; every choice
+ * produces bit-identical outputs — tests/test_gpu_parity.py::test_weight_paths_bit_identical):
+ *   FLUX_GEMM_FUSED_DEQUANT=1 / FLUX_GEMM_DEQUANT_PASS=1  force the weight path (default: one
+ *       dequantization pass per layer when T·k >= 2048·E, in-GEMM dequantization otherwise)
+ *   FLUX_GEMM_1SM=1         1-CTA GEMMs instead of CTA pairs
+ *   FLUX_GATHER_A=0|1       routed A rows materialised by K2 (0) or gathered with TMA gather4 (1)
+ *                           instead of the default in-GEMM cp.async gather
+ *   FLUX_FUSED_COMBINE=1    the combine fused into the shared MLP's down-GEMM epilogue
+ *   FLUX_GEMM_DYNAMIC=0     static round-robin tile order instead of claimed tiles
+ *   FLUX_L2_HINTS=<bits>    L2 cache policies of the CTA-pair GEMMs (default 1)
+ *   FLUX_DEBUG_SYNC=1       synchronise after every launch (see flux_last_error) */
 size_t flux_profile_layer_workspace(const flux_moe_cfg* cfg, int64_t T);
 
 /* One quantized MoE layer forward over T tokens that also emits the expert
