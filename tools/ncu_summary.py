@@ -69,7 +69,8 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__by
         "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_op_read_hit_rate.pct",
         "l1tex__m_xbar2l1tex_read_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active"]
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
 
 
 def full(path, out, traffic_prefix=None):
