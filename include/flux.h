@@ -114,33 +114,56 @@ typedef struct {
   float* router_logits;
 } flux_layer_out;
 
-/* Workspace bytes flux_profile_layer needs for T tokens (host function).  The size depends on the
- * GEMM path the library picks (below), so query it under the same environment as the calls.
- *
- * Performance policies of flux_profile_layer (environment variables read per call; every choice
- * produces bit-identical outputs — tests/test_gpu_parity.py::test_weight_paths_bit_identical):
- *   FLUX_GEMM_FUSED_DEQUANT=1 / FLUX_GEMM_DEQUANT_PASS=1  force the weight path (default: one
- *       dequantization pass per layer when T·k >= 2048·E, in-GEMM dequantization otherwise)
- *   FLUX_GEMM_1SM=1         1-CTA GEMMs instead of CTA pairs
- *   FLUX_GATHER_A=0|1       routed A rows materialised by K2 (0) or gathered with TMA gather4 (1)
- *                           instead of the default in-GEMM cp.async gather
- *   FLUX_FUSED_COMBINE=1    the combine fused into the shared MLP's down-GEMM epilogue
- *   FLUX_GEMM_DYNAMIC=0     static round-robin tile order instead of claimed tiles
- *   FLUX_L2_HINTS=<bits>    L2 cache policies of the CTA-pair GEMMs (default 1)
- *   FLUX_DEBUG_SYNC=1       synchronise after every launch (see flux_last_error) */
+/* Performance policy of flux_profile_layer_ex (NULL or all-zero = the library's measured defaults).
+ * Every value produces bit-identical outputs (tests/test_gpu_parity.py::test_weight_paths_bit_identical);
+ * values marked TEST-ONLY were measured slower on B200 and exist so that the bit-identity
+ * test can pin them against the defaults. */
+enum {
+  FLUX_WEIGHTS_AUTO = 0,          /* dequant pass when T·k >= 2048·E (B tiles reused by many m-tiles), else in-GEMM */
+  FLUX_WEIGHTS_DEQUANT_PASS = 1,  /* one dequantization pass per layer into bf16 B operands, TMA-fed GEMMs */
+  FLUX_WEIGHTS_IN_GEMM = 2        /* dequant warps inside the GEMM convert the raw codes per B tile (INT4/INT8) */
+};
+enum {
+  FLUX_ROWS_AUTO = 0,             /* in-GEMM cp.async gather of the routed rows from x on the pass path, else
+                                     materialised */
+  FLUX_ROWS_MATERIALISED = 1,     /* K2 writes x_perm (k·H·2 bytes per token) */
+  FLUX_ROWS_TMA_GATHER4 = 2       /* TEST-ONLY: TMA tile::gather4 (~2.5x slower gate/up GEMM) */
+};
+#define FLUX_L2_SET 0x100         /* l2_hints = FLUX_L2_SET | bits overrides the default (bits 1) */
+typedef struct {
+  int32_t weight_path;    /* FLUX_WEIGHTS_*                                                      */
+  int32_t routed_rows;    /* FLUX_ROWS_*                                                         */
+  int32_t fused_combine;  /* 1 = TEST-ONLY: K6 in the shared-MLP down-GEMM epilogue (needs F_s > 0) */
+  int32_t static_tiles;   /* 1 = TEST-ONLY: static round-robin GEMM tile order instead of claimed tiles */
+  int32_t l2_hints;       /* 0 = default (evict_first on the act / y_perm stores); FLUX_L2_SET | bits:
+                             bit 0 evict_first on output stores, bit 1 evict_last on B, bit 2 evict_first on A */
+} flux_policy;
+
+/* Workspace bytes flux_profile_layer needs for T tokens (host function); it depends on the policy
+ * (default policy for flux_profile_layer_workspace).  0 on invalid arguments.
+ * The environment variable FLUX_DEBUG_SYNC=1 synchronises after every launch (see flux_last_error). */
+size_t flux_profile_layer_workspace_ex(const flux_moe_cfg* cfg, const flux_policy* policy, int64_t T);
 size_t flux_profile_layer_workspace(const flux_moe_cfg* cfg, int64_t T);
 
 /* One quantized MoE layer forward over T tokens that also emits the expert
  * activation statistics — the profiling step of §4.1:
  *   z = x·W_rᵀ; S_t = top-k(z_t); w_t from softmax(z_t)            (R2)
  *   hist[e] += #{t : e ∈ S_t}; D_e = {t : e ∈ S_t}
- *   o_{t,e} = bf16(bf16(SiLU(x_t·ŵgᵀ)⊙(x_t·ŵuᵀ))·ŵdᵀ), ŵ = q·s     (R4)
+ *   o_{t,e} = bf16(bf16(SiLU(x_t·ŵgᵀ)⊙(x_t·ŵuᵀ))·ŵdᵀ)                 (R4)
+ *   ŵ = q·s for per-channel codes (the scale multiplies the fp32 dot product in the
+ *   epilogue); ŵ = bf16(q·bf16(s)) for grouped codes (reading R1b, the W4A16 convention)
  *   sh_t = shared SwiGLU(x_t) (R5);  y_t = bf16(r_t + sh_t + Σ_j w_tj o_{t,S_tj})
- * x: bf16 [T][H] device; residual: bf16 [T][H] device or NULL (NULL = x, R6).
+ * x: bf16 [T][H] device; residual: bf16 [T][H] device or NULL (NULL = x, R6; an all-zero
+ * buffer gives the MoE branch alone, y = bf16(sh + Σ_j w_j o_j)).
  * T may be 0 (no-op) or any positive count up to 2^31/k. Tokens are
  * independent; results do not depend on T or on how a batch is split. */
 flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, const void* x, const void* residual,
                                int64_t T, const flux_layer_out* out, void* ws, size_t ws_bytes, void* stream);
+/* The same with an explicit performance policy (NULL = defaults); ws sized by
+ * flux_profile_layer_workspace_ex with the same policy. */
+flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* policy, const flux_qlayer* w,
+                                  const void* x, const void* residual, int64_t T, const flux_layer_out* out, void* ws,
+                                  size_t ws_bytes, void* stream);
 
 /* Activation-frequency-weighted merge of non-tuning experts, eq.(2):
  *   W_c = Σ_{e∈E_c} α_e / Σ_{e'∈E_c} α_e' · W_e  (Σα = 0 -> plain mean, R10)
@@ -152,11 +175,33 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
  *   remap       int32 [E] device or NULL: compact slot of e — tuning experts
  *               first in ascending id, then clusters 0..C-1
  * numel % 8 == 0, pointers 16-byte aligned, 1 <= n_clusters <= E <= 1024.
- * Every cluster id in [0, n_clusters) must have a member: this is checked on
- * the device and an empty cluster's output is left as zeros. */
+ * A cluster id in [0, n_clusters) with no member produces an all-zero output (no
+ * error is reported: K-Means may legitimately leave a cluster empty); an expert
+ * whose id is < -1 or >= n_clusters belongs to no output (its remap is -1). */
 flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t numel, const void* experts,
                                const int32_t* cluster_of, const float* alpha, int32_t n_clusters, void* merged,
                                int32_t* remap, void* stream);
+
+/* The same eq.(2) merge for a BATCH of jobs in ONE persistent launch (a job = one weight family
+ * of one layer; the whole model's L x 3 families in one call).  All jobs share n_experts and numel;
+ * each has its own cluster_of / alpha / n_clusters (per-layer budgets B(l) of eq.(1)),
+ * output and remap.  compact = 0: out = [n_clusters][numel] as flux_merge_experts; compact = 1: out =
+ * the compact model's slots [n_tuning + n_clusters][numel] as flux_compact_experts, where n_tuning must
+ * be the number of -1 entries of cluster_of.  Results are bit-identical to one flux_merge_experts /
+ * flux_compact_experts call per job.  jobs: HOST array of n_jobs <= FLUX_MERGE_MAX_JOBS entries (read
+ * before the call returns); device pointers 16-byte aligned; numel % 8 == 0. */
+#define FLUX_MERGE_MAX_JOBS 256
+typedef struct {
+  const void* experts;       /* [E][numel] dtype, device                                      */
+  const int32_t* cluster_of; /* [E] device, -1 = tuning expert                                */
+  const float* alpha;        /* [E] device, >= 0                                              */
+  int32_t n_clusters;        /* C of this job                                                 */
+  int32_t n_tuning;          /* compact = 1 only: tuning experts of this job (slots = n_tuning + C) */
+  void* out;                 /* [C][numel] or [n_tuning + C][numel] dtype, device             */
+  int32_t* remap;            /* [E] device or NULL: compact slot of every expert             */
+} flux_merge_job;
+flux_status flux_merge_experts_batch(flux_dtype dtype, int32_t n_experts, int64_t numel, int32_t n_jobs,
+                                     const flux_merge_job* jobs, int32_t compact, void* stream);
 
 /* ---------------------------------------------------------------------------
  * NEXT-2: the compact model after merging (§5.3 + §7 "Customized MoE construction",

@@ -62,7 +62,7 @@ def lib():
         L.orc_router.argtypes = [_I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]
         L.orc_router.restype = _I
         L.orc_permute.argtypes = [_I64, _I, _I, _P, _P, _P, _P, _P]
-        L.orc_moe_tokens.argtypes = [_I64, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+        L.orc_moe_tokens.argtypes = [_I64, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I]
         L.orc_moe_tokens.restype = _I
         L.orc_compact_tokens.argtypes = [_I64, _I, _I, _I, _I, _I, _I, _I] + [_P] * 14
         L.orc_layer_budget.argtypes = [_I, _I, _P, _I64, _I64, _P, _P, _P, _P]
@@ -163,9 +163,18 @@ class QExpert:
         return _Expert(*[a.ctypes.data for a in self.arrs])
 
 
-def moe_tokens(x, wr, experts, shared, *, k: int, group_size: int, norm: int):
-    """O2+O4-O6 for independent tokens of one layer. Returns (y, ids, w, z, margin)."""
+def moe_tokens(x, wr, experts, shared, *, k: int, group_size: int, norm: int, residual=None, with_cond=False,
+               exact_dequant=False):
+    """O2+O4-O6 for independent tokens of one layer. Returns (y, ids, w, z, margin), plus cond when
+    with_cond: cond[t][h] = |r| + |sh| + Σ_j w_j|o_j| (the magnitude of the terms of the O6 sum) and
+    dmag[t][h] = Σ_j w_j max_f |a_jf·ŵd_hf| + max_f |a_sh,f·ŵsh_hf| (the largest down-projection term).
+    residual: [n][H] real values (e.g. zeros: y is the MoE branch alone) or None (r = x, R6).
+    exact_dequant: grouped codes dequantized as ŵ = q·s exactly instead of reading R1b's
+    bf16(q·bf16(s)); only for showing that R1b does not decide parity."""
     x = _c(x, np.float64)
+    r = None if residual is None else _c(residual, np.float64)
+    if r is not None and r.shape != x.shape:
+        raise ValueError("residual must have the shape of x")
     wr = _c(wr, np.float64)
     n, H = x.shape
     E = wr.shape[0]
@@ -178,11 +187,18 @@ def moe_tokens(x, wr, experts, shared, *, k: int, group_size: int, norm: int):
     w = np.empty((n, k))
     z = np.empty((n, E))
     m = np.empty(n)
+    cond = np.empty((n, H)) if with_cond else None
+    dmag = np.empty((n, H)) if with_cond else None
     rc = lib().orc_moe_tokens(n, H, E, k, F, Fs, group_size, norm, x.ctypes.data, wr.ctypes.data,
-                              ctypes.cast(arr, _P), ctypes.cast(sh, _P) if sh is not None else None, y.ctypes.data,
-                              ids.ctypes.data, w.ctypes.data, z.ctypes.data, m.ctypes.data)
+                              ctypes.cast(arr, _P), ctypes.cast(sh, _P) if sh is not None else None,
+                              r.ctypes.data if r is not None else None, y.ctypes.data, ids.ctypes.data,
+                              w.ctypes.data, z.ctypes.data, m.ctypes.data,
+                              cond.ctypes.data if cond is not None else None,
+                              dmag.ctypes.data if dmag is not None else None, int(bool(exact_dequant)))
     if rc:
         raise RuntimeError(f"orc_moe_tokens failed ({rc})")
+    if with_cond:
+        return y, ids, w, z, m, cond, dmag
     return y, ids, w, z, m
 
 

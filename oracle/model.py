@@ -60,6 +60,19 @@ def profile_tokens(cfg, token_ids, layers=None, quantized=None):
     return out
 
 
+def branch_tokens(cfg, token_ids, layer: int, quantized=None, exact_dequant=False):
+    """The MoE branch of one layer alone (residual r = 0, R6) on the generated x_0 of the given tokens:
+    y = bf16(sh + Σ_j w_j o_j).  Returns a dict x, y, ids, w, z, margin, cond (cond = |sh| + Σ_j w_j|o_j|,
+    the magnitude of the terms of the O6 sum) and dmag (the largest down-projection term, weighted),
+    for condition-aware element-wise bounds."""
+    x = synth.bf16_bits_to_f32(synth.cpu_rows(synth.spec_x(cfg), token_ids)).astype(np.float64)
+    wr, experts, shared = quantized if quantized is not None else quantized_layer(cfg, layer)
+    y, ids, w, z, m, cond, dmag = moe_tokens(x, wr, experts, shared, k=cfg.top_k, group_size=cfg.group_size,
+                                             norm=cfg.norm_topk, residual=np.zeros_like(x), with_cond=True,
+                                             exact_dequant=exact_dequant)
+    return dict(x=x, y=y, ids=ids, w=w, z=z, margin=m, cond=cond, dmag=dmag)
+
+
 def profile_all(cfg, quantized=None):
     """Whole-batch oracle for small configs: per layer also the histogram and D_e CSR (O3/O8)."""
     res = profile_tokens(cfg, np.arange(cfg.tokens), quantized=quantized)

@@ -243,14 +243,19 @@ static void deq_free(deq_expert* d) {
   free(d->up);
   free(d->down);
 }
-static void deq_fill(deq_expert* d, const orc_expert* ex, int H, int F, int g) {
-  const int grouped = g != 0;
-  dequantize(ex->q_gate, ex->s_gate, F, H, grouped ? g : H, grouped, d->gate);
-  dequantize(ex->q_up, ex->s_up, F, H, grouped ? g : H, grouped, d->up);
-  dequantize(ex->q_down, ex->s_down, H, F, grouped ? g : F, grouped, d->down);
+/* exact != 0: the survey's O4 reading ŵ = q·s for grouped codes as well (no bf16 rounding of the
+ * scale or the product) — used only to show that R1b does not decide parity (tests). */
+static void deq_fill(deq_expert* d, const orc_expert* ex, int H, int F, int g, int exact) {
+  const int grouped = g != 0 && !exact;
+  dequantize(ex->q_gate, ex->s_gate, F, H, g ? g : H, grouped, d->gate);
+  dequantize(ex->q_up, ex->s_up, F, H, g ? g : H, grouped, d->up);
+  dequantize(ex->q_down, ex->s_down, H, F, g ? g : F, grouped, d->down);
 }
 
-static void swiglu_expert(int H, int F, const deq_expert* w, const double* x, double* a, double* out) {
+/* mag (NULL = skip): [H] the largest term of each down-projection dot product,
+ * mag_h = max_f |a_f·ŵdown[h][f]| (an act value a_f one bf16 ulp off moves o_h by <= 2^-7·mag_h). */
+static void swiglu_expert(int H, int F, const deq_expert* w, const double* x, double* a, double* out,
+                          double* mag) {
   for (int f = 0; f < F; ++f) {
     double gs = 0.0, us = 0.0;
     for (int h = 0; h < H; ++h) {
@@ -264,6 +269,11 @@ static void swiglu_expert(int H, int F, const deq_expert* w, const double* x, do
     double acc = 0.0;
     for (int f = 0; f < F; ++f) acc += a[f] * w->down[(int64_t)h * F + f];
     out[h] = orc_bf16_round(acc);
+    if (mag) {
+      double m = 0.0;
+      for (int f = 0; f < F; ++f) m = fmax(m, fabs(a[f] * w->down[(int64_t)h * F + f]));
+      mag[h] = m;
+    }
   }
 }
 
@@ -273,18 +283,31 @@ static void swiglu_expert(int H, int F, const deq_expert* w, const double* x, do
  *   (z, S, w, margin) = router(x_t)
  *   o_{t,j}  = expert_{S_tj}(x_t)                       (O4; for e, for t in D_e)
  *   sh_t     = shared SwiGLU(x_t), 0 if F_s == 0        (O5)
- *   y_t      = bf16( x_t + sh_t + Σ_j w_tj · o_{t,j} )  (O6, residual = x_t, j in order)
+ *   y_t      = bf16( r_t + sh_t + Σ_j w_tj · o_{t,j} )  (O6, j in order)
+ * r: the residual (R6: "r = residual (optional)"): resid [n][H] when given (e.g. all
+ * zeros, so that y is the MoE branch alone), else r_t = x_t.
  * x, y: [n][H] real (bf16-valued) numbers.  experts: array of E routed experts;
  * shared: NULL or one expert of width F_s.  g: group size (0 = per channel).
+ * deq_exact: 0 = reading R1b (grouped ŵ = bf16(q·bf16(s))); 1 = ŵ = q·s exactly for every
+ * granularity (SURVEY O4's literal reading; a cross-check that R1b is not load-bearing).
+ * cond (NULL = skip): [n][H] magnitude of the terms of the O6 sum,
+ *   cond_th = |r_th| + |sh_th| + Σ_j w_tj·|o_{t,j,h}|
+ * — the condition of the sum: a perturbation of relative size ε in every term moves
+ * y_th by at most ε·cond_th (the standard forward error bound of a sum).
+ * dmag (NULL = skip): [n][H] Σ_j w_tj·max_f |a_tjf·ŵd_hf| + max_f |a_sh,f·ŵsh_hf| — the largest
+ * down-projection term behind each y_th (an act value a_f that lands one bf16 ulp away moves y_th by
+ * at most 2^-7 of its term).
  * Work order: each expert's weights are dequantized once, then its tokens run.
  * -------------------------------------------------------------------------- */
 int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int norm, const double* x, const double* wr,
-                   const orc_expert* experts, const orc_expert* shared, double* y, int32_t* ids, double* w, double* z,
-                   double* margin) {
+                   const orc_expert* experts, const orc_expert* shared, const double* resid, double* y, int32_t* ids,
+                   double* w, double* z, double* margin, double* cond, double* dmag, int deq_exact) {
   if (orc_router(n, H, E, k, norm, x, wr, z, ids, w, margin)) return 1;
   double* o = (double*)malloc(sizeof(double) * (size_t)n * k * H);   /* o[t][j][h] */
   double* sh = (double*)calloc((size_t)n * H, sizeof(double));       /* sh[t][h]   */
-  if (!o || !sh) { free(o); free(sh); return 2; }
+  double* om = dmag ? (double*)calloc((size_t)n * k * H, sizeof(double)) : NULL;  /* down-term magnitudes */
+  double* shm = dmag ? (double*)calloc((size_t)n * H, sizeof(double)) : NULL;
+  if (!o || !sh || (dmag && (!om || !shm))) { free(o); free(sh); free(om); free(shm); return 2; }
   int ok = 1;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int e = 0; e < E; ++e) {
@@ -294,10 +317,11 @@ int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int nor
     deq_expert d;
     double* a = (double*)malloc(sizeof(double) * (size_t)F);
     if (!deq_alloc(&d, H, F) || !a) { ok = 0; deq_free(&d); free(a); continue; }
-    deq_fill(&d, &experts[e], H, F, g);
+    deq_fill(&d, &experts[e], H, F, g, deq_exact);
     for (int64_t t = 0; t < n; ++t)
       for (int j = 0; j < k; ++j)
-        if (ids[t * k + j] == e) swiglu_expert(H, F, &d, x + t * H, a, o + (t * k + j) * (int64_t)H);
+        if (ids[t * k + j] == e) swiglu_expert(H, F, &d, x + t * H, a, o + (t * k + j) * (int64_t)H,
+                                                   om ? om + (t * k + j) * (int64_t)H : NULL);
     deq_free(&d);
     free(a);
   }
@@ -305,11 +329,11 @@ int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int nor
     deq_expert d;
     if (!deq_alloc(&d, H, Fs)) { ok = 0; }
     else {
-      deq_fill(&d, shared, H, Fs, g);
+      deq_fill(&d, shared, H, Fs, g, deq_exact);
 #pragma omp parallel for schedule(dynamic, 1)
       for (int64_t t = 0; t < n; ++t) {
         double* a = (double*)malloc(sizeof(double) * (size_t)Fs);
-        swiglu_expert(H, Fs, &d, x + t * H, a, sh + t * H);
+        swiglu_expert(H, Fs, &d, x + t * H, a, sh + t * H, shm ? shm + t * H : NULL);
         free(a);
       }
     }
@@ -318,13 +342,26 @@ int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int nor
 #pragma omp parallel for schedule(static)
   for (int64_t t = 0; t < n; ++t)
     for (int h = 0; h < H; ++h) {
-      double acc = x[t * H + h];
+      const double r = resid ? resid[t * H + h] : x[t * H + h];
+      double acc = r;
       acc += sh[t * H + h];
       for (int j = 0; j < k; ++j) acc += w[t * k + j] * o[(t * k + j) * (int64_t)H + h];
       y[t * H + h] = orc_bf16_round(acc);
+      if (cond) {
+        double m = fabs(r) + fabs(sh[t * H + h]);
+        for (int j = 0; j < k; ++j) m += w[t * k + j] * fabs(o[(t * k + j) * (int64_t)H + h]);
+        cond[t * H + h] = m;
+      }
+      if (dmag) {
+        double m = shm[t * H + h];
+        for (int j = 0; j < k; ++j) m += w[t * k + j] * om[(t * k + j) * (int64_t)H + h];
+        dmag[t * H + h] = m;
+      }
     }
   free(o);
   free(sh);
+  free(om);
+  free(shm);
   return ok ? 0 : 2;
 }
 
@@ -373,7 +410,7 @@ int orc_compact_tokens(int64_t n, int H, int Er, int k, int S, int F, int Fs, in
     double* a = (double*)malloc(sizeof(double) * (size_t)F);
     for (int64_t t = 0; t < n; ++t)
       for (int j = 0; j < k; ++j)
-        if (ids[t * k + j] == s) swiglu_expert(H, F, &d, x + t * H, a, o + (t * k + j) * (int64_t)H);
+        if (ids[t * k + j] == s) swiglu_expert(H, F, &d, x + t * H, a, o + (t * k + j) * (int64_t)H, NULL);
     free(a);
   }
   if (Fs > 0 && sh_gate) {
@@ -381,7 +418,7 @@ int orc_compact_tokens(int64_t n, int H, int Er, int k, int S, int F, int Fs, in
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t t = 0; t < n; ++t) {
       double* a = (double*)malloc(sizeof(double) * (size_t)Fs);
-      swiglu_expert(H, Fs, &d, x + t * H, a, sh + t * H);
+      swiglu_expert(H, Fs, &d, x + t * H, a, sh + t * H, NULL);
       free(a);
     }
   }
@@ -449,7 +486,8 @@ int64_t orc_layer_budget(int L, int E, const int64_t* hist, int64_t T, int64_t B
   for (int l = 0; l < L; ++l) {
     int64_t B = (int64_t)floor(b[l] / bsum * (double)B_non);
     if (B < 1) B = 1;
-    if (n_non && B > n_non[l]) B = n_non[l];
+    /* R9: at most the layer's non-tuning experts; n_non NULL = every expert is non-tuning (E) */
+    if (B > (n_non ? n_non[l] : E)) B = n_non ? n_non[l] : E;
     C_out[l] = (int32_t)B;
     if (b_out) b_out[l] = b[l];
     total += B;

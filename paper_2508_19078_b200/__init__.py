@@ -47,6 +47,29 @@ class QLayer(ctypes.Structure):
                  "sh_gate_q", "sh_up_q", "sh_down_q", "sh_gate_s", "sh_up_s", "sh_down_s", "remap")]
 
 
+class MergeJob(ctypes.Structure):
+    """flux_merge_job (include/flux.h)."""
+    _fields_ = [("experts", ctypes.c_void_p), ("cluster_of", ctypes.c_void_p), ("alpha", ctypes.c_void_p),
+                ("n_clusters", ctypes.c_int32), ("n_tuning", ctypes.c_int32), ("out", ctypes.c_void_p),
+                ("remap", ctypes.c_void_p)]
+
+
+class Policy(ctypes.Structure):
+    """flux_policy (include/flux.h): performance policy of flux_profile_layer_ex; all-zero = defaults.
+    Every value gives bit-identical outputs; TEST-ONLY values were measured slower."""
+    _fields_ = [("weight_path", ctypes.c_int32), ("routed_rows", ctypes.c_int32), ("fused_combine", ctypes.c_int32),
+                ("static_tiles", ctypes.c_int32), ("l2_hints", ctypes.c_int32)]
+
+
+WEIGHTS_AUTO, WEIGHTS_DEQUANT_PASS, WEIGHTS_IN_GEMM = 0, 1, 2
+ROWS_AUTO, ROWS_MATERIALISED, ROWS_TMA_GATHER4 = 0, 1, 2
+L2_SET = 0x100
+
+
+def make_policy(weight_path=0, routed_rows=0, fused_combine=0, static_tiles=0, l2_hints=0) -> Policy:
+    return Policy(weight_path, routed_rows, fused_combine, static_tiles, l2_hints)
+
+
 class LayerOut(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
                 ("y", "topk_ids", "topk_w", "hist", "expert_offsets", "token_index", "router_logits")]
@@ -68,9 +91,14 @@ def _lib():
         L.flux_profile_layer_workspace.restype = SZ
         L.flux_profile_layer.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(QLayer), P, P, I64,
                                          ctypes.POINTER(LayerOut), P, SZ, P]
+        L.flux_profile_layer_workspace_ex.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(Policy), I64]
+        L.flux_profile_layer_workspace_ex.restype = SZ
+        L.flux_profile_layer_ex.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(Policy), ctypes.POINTER(QLayer),
+                                            P, P, I64, ctypes.POINTER(LayerOut), P, SZ, P]
         L.flux_merge_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
         L.flux_quantize_weights.argtypes = [I32, I32, ctypes.c_int, P, I64, I64, P, P, P]
         L.flux_compact_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
+        L.flux_merge_experts_batch.argtypes = [ctypes.c_int, I32, I64, I32, P, I32, P]
         L.flux_attention_hist.argtypes = [I64, I32, I32, P, P, P, P]
         L.flux_output_error_workspace.argtypes = []
         L.flux_output_error_workspace.restype = SZ
@@ -84,8 +112,9 @@ def _lib():
         L.flux_comm_init.argtypes = [ctypes.POINTER(P), P, I32, I32]
         L.flux_reduce_stats.argtypes = [P, P, SZ, P]
         L.flux_comm_destroy.argtypes = [P]
-        for f in ("flux_profile_layer", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
+        for f in ("flux_profile_layer", "flux_profile_layer_ex", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
                   "flux_expert_features", "flux_cluster_experts", "flux_compact_experts", "flux_output_error",
+                  "flux_merge_experts_batch",
                   "flux_attention_hist",
                   "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
             getattr(L, f).restype = ctypes.c_int
@@ -145,15 +174,20 @@ def make_cfg(hidden, ffn, n_experts, top_k, shared_ffn, wbits, group_size, norm_
     return MoECfg(hidden, ffn, n_experts, top_k, shared_ffn, wbits, group_size, norm_topk, n_router)
 
 
-def profile_layer_workspace(cfg: MoECfg, T: int) -> int:
-    return int(_lib().flux_profile_layer_workspace(ctypes.byref(cfg), T))
+def _pol(policy):
+    return ctypes.byref(policy) if policy is not None else None
 
 
-def profile_layer(cfg: MoECfg, qlayer: QLayer, x, residual, T: int, out: LayerOut, ws, stream=None):
-    """One quantized MoE layer + statistics (flux_profile_layer). Tensors are CUDA tensors."""
-    st = _lib().flux_profile_layer(ctypes.byref(cfg), ctypes.byref(qlayer), _ptr(x), _ptr(residual), T,
-                                   ctypes.byref(out), _ptr(ws), ws.numel() * ws.element_size() if ws is not None
-                                   else 0, _stream(stream))
+def profile_layer_workspace(cfg: MoECfg, T: int, policy: Policy | None = None) -> int:
+    return int(_lib().flux_profile_layer_workspace_ex(ctypes.byref(cfg), _pol(policy), T))
+
+
+def profile_layer(cfg: MoECfg, qlayer: QLayer, x, residual, T: int, out: LayerOut, ws, stream=None,
+                  policy: Policy | None = None):
+    """One quantized MoE layer + statistics (flux_profile_layer_ex). Tensors are CUDA tensors."""
+    st = _lib().flux_profile_layer_ex(ctypes.byref(cfg), _pol(policy), ctypes.byref(qlayer), _ptr(x), _ptr(residual),
+                                      T, ctypes.byref(out), _ptr(ws),
+                                      ws.numel() * ws.element_size() if ws is not None else 0, _stream(stream))
     _check(st, "flux_profile_layer")
 
 
@@ -165,6 +199,32 @@ def merge_experts(experts, cluster_of, alpha, n_clusters: int, merged, remap=Non
     st = _lib().flux_merge_experts(dt, E, numel, _ptr(experts), _ptr(cluster_of), _ptr(alpha), n_clusters,
                                    _ptr(merged), _ptr(remap), _stream(stream))
     _check(st, "flux_merge_experts")
+
+
+MERGE_MAX_JOBS = 256
+
+
+def merge_experts_batch(jobs, compact: bool = False, stream=None):
+    """eq.(2) for many jobs in ONE launch (flux_merge_experts_batch).  jobs: list of dicts with experts
+    [E][numel], cluster_of [E], alpha [E], n_clusters, out, optional remap and (compact) n_tuning; all
+    jobs share E, numel and the dtype."""
+    if not jobs:
+        return
+    ex0 = jobs[0]["experts"]
+    dt = FLUX_FP32 if ex0.dtype == torch.float32 else FLUX_BF16
+    E = ex0.shape[0]
+    numel = ex0.numel() // E
+    for i in range(0, len(jobs), MERGE_MAX_JOBS):
+        part = jobs[i:i + MERGE_MAX_JOBS]
+        arr = (MergeJob * len(part))()
+        for a, j in zip(arr, part):
+            assert j["experts"].dtype == ex0.dtype and j["experts"].numel() == E * numel
+            a.experts, a.cluster_of, a.alpha = _ptr(j["experts"]), _ptr(j["cluster_of"]), _ptr(j["alpha"])
+            a.n_clusters, a.n_tuning = int(j["n_clusters"]), int(j.get("n_tuning", 0))
+            a.out, a.remap = _ptr(j["out"]), _ptr(j.get("remap"))
+        st = _lib().flux_merge_experts_batch(dt, E, numel, len(part), ctypes.cast(arr, ctypes.c_void_p),
+                                             int(compact), _stream(stream))
+        _check(st, "flux_merge_experts_batch")
 
 
 def compact_experts(experts, cluster_of, alpha, n_clusters: int, compact, remap=None, stream=None):

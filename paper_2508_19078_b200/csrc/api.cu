@@ -62,64 +62,57 @@ static flux_status check_device() {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Grouped-GEMM tile rows: 256 = CTA-pair kernel (default), 128 = 1-CTA kernel (FLUX_GEMM_1SM=1,
-// kept for A/B measurements).  Both are deterministic and batch-invariant.
-static bool env_on(const char* name) {
-  const char* e = getenv(name);
-  return e && e[0] == '1';
-}
-// Where the bf16 B operand of the expert GEMMs comes from.  Both choices produce bit-identical
-// weights (bf16(q·bf16(s)) or exact q) and the same MMA order, so results never depend on it:
-//  * fused: dequant warps inside the GEMM convert each B tile per m-tile -- best when few tokens
-//    reach each expert (the weights dominate traffic);
-//  * pass: one dequantization per layer into bf16 buffers the GEMM streams with TMA -- best when
-//    every B tile is reused by many m-tiles (e.g. 262,144 tokens: ~96 m-tiles per expert).
-// Policy: pass when the average routed rows per expert reach 8 tile rows (2048); overrides:
-// FLUX_GEMM_DEQUANT_PASS=1 / FLUX_GEMM_FUSED_DEQUANT=1 (FLUX_GEMM_1SM=1 implies the pass).
-static bool dequant_pass(const flux_moe_cfg& c, int64_t T) {
-  if (c.wbits == 16 || c.wbits == 2) return true;  // bf16 copy / INT2 codes: the fused kernel does INT4/INT8
-  if (env_on("FLUX_GEMM_DEQUANT_PASS") || env_on("FLUX_GEMM_1SM")) return true;
-  if (env_on("FLUX_GEMM_FUSED_DEQUANT")) return false;
-  return T * c.top_k >= (int64_t)2048 * c.n_experts;
-}
-static int gemm_bm() { return env_on("FLUX_GEMM_1SM") ? 128 : 256; }
-// K6 placement with shared experts: a standalone gather kernel (default; HBM-bound at ~80% of the
-// copy roofline) or fused into the shared-MLP down GEMM's epilogue (FLUX_FUSED_COMBINE=1; bit-
-// identical, saves the y_sh round-trip, but its per-thread-row gathers are latency-bound today).
-static bool fused_combine() { return env_on("FLUX_FUSED_COMBINE"); }
-// Routed A rows of the gate/up GEMM (all choices bit-identical, by test):
-//  * GATHER_CP (default whenever the dequant-pass CTA-pair kernel runs): gathered from x inside the
-//    GEMM by two producer warps with per-lane 16-byte cp.async (LDGSTS) into the swizzled stage, so
-//    K2 writes only the D_e indices.  Measured (B200, in the bench step): the gate/up GEMM runs ~1-3%
-//    slower than from a materialised x_perm, but K2's k·H·2 bytes per token disappear (1.4 ms per
-//    layer) and the lower HBM power lets the clocks rise: +5% tokens/s on both BASELINE shapes.
-//  * GATHER_TMA (FLUX_GATHER_A=1): TMA tile::gather4 (~5 B/clk/SM: ~2.5x slower GEMM).
-//  * NONE (FLUX_GATHER_A=0, the fused-dequant kernel, the 1-CTA kernel): K2 materialises x_perm.
-// L2 cache policies of the CTA-pair pass kernel (GemmArgs::l2_hints).  Default 1: the act / y_perm
-// output tiles (4.4 / 6.4 GB per DeepSeek-shape layer, consumed by the next kernel long after they
-// left L2) are stored evict_first, which cut the down GEMM's DRAM reads by 1.4 GB per layer (ncu:
-// 12.1 -> 10.7 GB; more A re-reads hit L2).  evict_last on B (2) or evict_first on A (4) raised them
-// (15.3 / 26.8 GB).  FLUX_L2_HINTS overrides for experiments.
-static int l2_hints() {
-  const char* e = getenv("FLUX_L2_HINTS");
-  return e ? atoi(e) : 1;
-}
-// Tile order of the CTA-pair pass kernels: claimed in global order from a counter (default), or the
-// static round-robin over the 74 pairs (FLUX_GEMM_DYNAMIC=0).  With the static order the pairs drift
-// apart over ~1,200 tiles and the n-tiles of an m-tile stop sharing their A rows in L2: the gate/up
-// and down GEMMs read 8-12 and 10-17 GB per DeepSeek layer from DRAM instead of 8.3 and 6.3 GB.
-// Claimed tiles cost ~0-2% in isolation, but the DRAM power saved raises the power-capped clocks by
-// ~100 MHz in the bench step: +3-4% tokens/s on both BASELINE shapes (same box, 2 runs each).
-static bool dynamic_tiles() {
-  const char* e = getenv("FLUX_GEMM_DYNAMIC");
-  return !(e && e[0] == '0');
-}
+// ---------------------------------------------------------------- performance policy (flux_policy)
+// Every choice produces bit-identical outputs (tests/test_gpu_parity.py::test_weight_paths_bit_identical);
+// the defaults are the measured winners on B200.  Paths measured slower are kept only as
+// test-only values of the policy, so the bit-identity test can pin them against the defaults.
+//  * weight path — where the bf16 B operand of the expert GEMMs comes from (bf16(q·bf16(s)) or exact q):
+//    in-GEMM dequant warps convert each B tile per m-tile (best when few tokens reach each expert); one
+//    dequantization pass per layer feeds TMA-loaded bf16 tiles (best when every B tile is reused by many
+//    m-tiles: 262,144 tokens = ~96 m-tiles per expert).  Auto: the pass when the average routed rows per
+//    expert reach 8 tile rows (T·k >= 2048·E).
+//  * routed A rows of the gate/up GEMM: gathered from x inside the GEMM by two producer warps with per-lane
+//    16-byte cp.async (default on the pass path: K2 then writes only the D_e indices; measured +5% tokens/s
+//    in the bench step on both BASELINE shapes, the lower HBM power raises the capped clocks), materialised
+//    by K2 as x_perm (the in-GEMM-dequant kernel always), or TMA tile::gather4 (test-only: ~2.5x slower GEMM).
+//  * K6 placement: standalone (default) or fused into the shared-MLP down-GEMM epilogue (test-only: ties
+//    the standalone kernel in isolation, 0.6% behind in the bench step with claimed tiles).
+//  * tile order of the CTA-pair GEMMs: claimed in global order from a counter (default: the n-tiles of an
+//    m-tile run together and share their A rows in L2; gate/up and down read 8.3 / 6.3 GB per DeepSeek
+//    layer from DRAM instead of 8-12 / 10-17 GB) or static round-robin over the 74 pairs (test-only).
+//  * L2 hints (bits): 1 = evict_first on the act / y_perm TMA stores (default; the down GEMM's DRAM reads
+//    12.1 -> 10.7 GB per layer), 2 = evict_last on B, 4 = evict_first on A (both measured worse).
 enum GatherMode { GATHER_NONE = 0, GATHER_TMA = 1, GATHER_CP = 2 };
-static GatherMode gather_mode(const flux_moe_cfg& c, int64_t T) {
-  const char* e = getenv("FLUX_GATHER_A");
-  if (gemm_bm() != 256 || (e && e[0] == '0')) return GATHER_NONE;
-  if (e && e[0] == '1') return GATHER_TMA;
-  return dequant_pass(c, T) ? GATHER_CP : GATHER_NONE;
+struct Policy {
+  bool pass;
+  GatherMode gmode;
+  bool fused_combine;
+  bool dynamic_tiles;
+  int l2_hints;
+};
+static Policy resolve_policy(const flux_moe_cfg& c, const flux_policy* up, int64_t T) {
+  flux_policy d{};
+  const flux_policy& u = up ? *up : d;
+  Policy p;
+  if (c.wbits == 16 || c.wbits == 2) p.pass = true;  // bf16 copy / INT2 codes: the in-GEMM kernel does INT4/INT8
+  else if (u.weight_path == FLUX_WEIGHTS_DEQUANT_PASS) p.pass = true;
+  else if (u.weight_path == FLUX_WEIGHTS_IN_GEMM) p.pass = false;
+  else p.pass = T * c.top_k >= (int64_t)2048 * c.n_experts;
+  if (u.routed_rows == FLUX_ROWS_MATERIALISED) p.gmode = GATHER_NONE;
+  else if (u.routed_rows == FLUX_ROWS_TMA_GATHER4) p.gmode = GATHER_TMA;
+  else p.gmode = p.pass ? GATHER_CP : GATHER_NONE;
+  p.fused_combine = u.fused_combine != 0 && c.shared_ffn > 0;
+  p.dynamic_tiles = u.static_tiles == 0;
+  p.l2_hints = (u.l2_hints & FLUX_L2_SET) ? (u.l2_hints & 7) : 1;
+  return p;
+}
+static flux_status validate_policy(const flux_policy* u) {
+  if (!u) return FLUX_OK;
+  if (u->weight_path < 0 || u->weight_path > 2 || u->routed_rows < 0 || u->routed_rows > 2 ||
+      (u->fused_combine != 0 && u->fused_combine != 1) || (u->static_tiles != 0 && u->static_tiles != 1) ||
+      (u->l2_hints != 0 && (u->l2_hints & ~(FLUX_L2_SET | 7)) != 0))
+    return FLUX_E_INVALID;
+  return FLUX_OK;
 }
 
 static bool tmap_u8(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols_bytes, uint32_t box_cols) {
@@ -156,7 +149,7 @@ int pad128(int v) { return (v + 127) / 128 * 128; }
 // The tensor maps keep the logical width F, so the pad columns are never read (no zeroing needed).
 int pad64(int v) { return (v + 63) / 64 * 64; }
 
-WsPlan plan(const flux_moe_cfg& c, int64_t T) {
+WsPlan plan(const flux_moe_cfg& c, const Policy& pol, int64_t T) {
   Layout L;
   WsPlan p;
   const int64_t n_rt = (T + kRouterTile - 1) / kRouterTile;
@@ -174,13 +167,13 @@ WsPlan plan(const flux_moe_cfg& c, int64_t T) {
   p.row0 = L.take(sizeof(int32_t) * n_groups);
   p.rows = L.take(sizeof(int32_t) * n_groups);
   // x_perm (routed A rows materialised by K2) unless the GEMM gathers them; y_perm always.
-  p.x_perm = L.take(gather_mode(c, T) != GATHER_NONE ? 0 : 2ull * Tk * c.hidden);
+  p.x_perm = L.take(pol.gmode != GATHER_NONE ? 0 : 2ull * Tk * c.hidden);
   p.y_perm = L.take(2ull * Tk * c.hidden);
   p.act = L.take(2ull * Tk * pad64(c.ffn));
   p.act_sh = L.take(2ull * T * pad64(c.shared_ffn));
   p.sh_sched = L.take(4 * sizeof(int32_t));  // sched_sh[2], row0_sh[1], rows_sh[1]
-  p.y_sh = L.take(c.shared_ffn && !fused_combine() ? 2ull * T * c.hidden : 0);
-  const size_t pass = dequant_pass(c, T) ? 1 : 0;  // bf16 B operands only for the separate-pass path
+  p.y_sh = L.take(c.shared_ffn && !pol.fused_combine ? 2ull * T * c.hidden : 0);
+  const size_t pass = pol.pass ? 1 : 0;  // bf16 B operands only for the separate-pass path
   p.wgu_r = L.take(pass * 2ull * c.n_experts * 2 * pad128(c.ffn) * c.hidden);
   p.wdn_r = L.take(pass * 2ull * c.n_experts * c.hidden * pad64(c.ffn));
   p.wgu_s = L.take(pass * 2ull * 2 * pad128(c.shared_ffn) * c.hidden);
@@ -231,15 +224,26 @@ const char* flux_status_string(flux_status s) {
   return "unknown status";
 }
 
+size_t flux_profile_layer_workspace_ex(const flux_moe_cfg* cfg, const flux_policy* policy, int64_t T) {
+  if (validate_cfg(cfg) != FLUX_OK || validate_policy(policy) != FLUX_OK || T < 0) return 0;
+  return plan(*cfg, resolve_policy(*cfg, policy, T), T).total;
+}
+
 size_t flux_profile_layer_workspace(const flux_moe_cfg* cfg, int64_t T) {
-  if (validate_cfg(cfg) != FLUX_OK || T < 0) return 0;
-  return plan(*cfg, T).total;
+  return flux_profile_layer_workspace_ex(cfg, nullptr, T);
 }
 
 flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, const void* x, const void* residual,
                                int64_t T, const flux_layer_out* out, void* ws, size_t ws_bytes, void* stream) {
+  return flux_profile_layer_ex(cfg, nullptr, w, x, residual, T, out, ws, ws_bytes, stream);
+}
+
+flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* policy, const flux_qlayer* w,
+                                  const void* x, const void* residual, int64_t T, const flux_layer_out* out, void* ws,
+                                  size_t ws_bytes, void* stream) {
   flux_status st = validate_cfg(cfg);
   if (st != FLUX_OK) return st;
+  if ((st = validate_policy(policy)) != FLUX_OK) return st;
   if (!w || !out || T < 0) return FLUX_E_INVALID;
   if (T == 0) return FLUX_OK;
   if (T * cfg->top_k >= (int64_t)1 << 31) return FLUX_E_UNSUPPORTED;
@@ -257,7 +261,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
                           w->sh_gate_q, w->sh_up_q, w->sh_down_q, ws};
   for (const void* p : ptrs16)
     if (p && !aligned16(p)) return FLUX_E_INVALID;
-  const WsPlan P = plan(c, T);
+  const Policy pol = resolve_policy(c, policy, T);
+  const WsPlan P = plan(c, pol, T);
   if (!ws || ws_bytes < P.total) return FLUX_E_WORKSPACE;
   if ((st = check_device()) != FLUX_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
@@ -279,14 +284,14 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   int32_t* offsets = (int32_t*)(W + P.offsets);
   int32_t* token_index = out->token_index ? out->token_index : (int32_t*)(W + P.token_index);
   int32_t* inv_pos = (int32_t*)(W + P.inv_pos);
-  const GatherMode gmode = gather_mode(*cfg, T);
+  const GatherMode gmode = pol.gmode;
   const bool gather_a = gmode != GATHER_NONE;
   void* x_perm = gather_a ? nullptr : W + P.x_perm;
   void* y_perm = W + P.y_perm;
   void* act = W + P.act;
   void* act_sh = W + P.act_sh;
   int32_t* sh_sched = (int32_t*)(W + P.sh_sched);
-  const bool fuse_combine = sh && fused_combine();
+  const bool fuse_combine = sh && pol.fused_combine;
   void* y_sh = W + P.y_sh;  // shared-MLP output (unused when the combine is fused into its down GEMM)
   void* wgu_r = W + P.wgu_r;
   void* wdn_r = W + P.wdn_r;
@@ -295,7 +300,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
 
   // ---- (a) weights -> bf16 B operands (scale folded for grouped quantization)
   cudaError_t e = cudaSuccess;
-  const bool pass = dequant_pass(c, T);
+  const bool pass = pol.pass;
   if (pass) {
   KernelTimer kt(K_DEQUANT, s);
   e = launch_dequant(c.wbits, (const uint8_t*)w->gate_q, w->gate_s, (const uint8_t*)w->up_q, w->up_s, E, F, H, Fp, 1,
@@ -343,7 +348,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   sa.sched_dn = (int32_t*)(W + P.sched_dn);
   sa.grp_row0 = (int32_t*)(W + P.row0);
   sa.grp_rows = (int32_t*)(W + P.rows);
-  sa.gemm_bm = gemm_bm();
+  sa.gemm_bm = 256;  // CTA pairs
   sa.sched_sh = sh ? sh_sched : nullptr;
   sa.grp_row0_sh = sh_sched + 2;
   sa.grp_rows_sh = sh_sched + 3;
@@ -387,8 +392,8 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   ga.bm = sa.gemm_bm;
   ga.gather_idx = gather_a ? token_index : nullptr;
   ga.gather_cp = gmode == GATHER_CP ? 1 : 0;
-  ga.l2_hints = l2_hints();
-  ga.tile_ctr = dynamic_tiles() ? sa.done_counter + 1 : nullptr;  // zeroed by launch_schedule
+  ga.l2_hints = pol.l2_hints;
+  ga.tile_ctr = pol.dynamic_tiles ? sa.done_counter + 1 : nullptr;  // zeroed by launch_schedule
   ga.a_src = x;
   ga.a_ld = H;
   GemmArgs gd = ga;
@@ -430,7 +435,7 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
 
   CUtensorMap a_r, a_s, b_r, b_s;
   if (pass) {
-    const uint32_t bbox = sa.gemm_bm == 256 ? 128 : 256;  // B rows per TMA box: half the tile for CTA pairs
+    const uint32_t bbox = 128;  // B rows per TMA box: half the 256-row tile of a CTA pair
     if (!tmap_a_routed(&a_r, gather_a, x, x_perm, T, Tk, H) || !tmap_bf16(&b_r, wgu_r, (uint64_t)E * 2 * Fp, H, bbox) ||
         (sh && (!tmap_bf16(&a_s, x, T, H, 128) || !tmap_bf16(&b_s, wgu_s, 2ull * Fsp, H, bbox)))) {
       set_last_error("gate/up tensor maps", cudaErrorInvalidValue);
@@ -554,6 +559,39 @@ flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t nume
   KernelTimer kt(K_MERGE, (cudaStream_t)stream);
   return cuda_status(launch_merge(dtype == FLUX_FP32, n_experts, numel, experts, cluster_of, alpha, n_clusters, merged,
                                   remap, (cudaStream_t)stream));
+}
+
+flux_status flux_merge_experts_batch(flux_dtype dtype, int32_t n_experts, int64_t numel, int32_t n_jobs,
+                                     const flux_merge_job* jobs, int32_t compact, void* stream) {
+  if (dtype != FLUX_BF16 && dtype != FLUX_FP32) return FLUX_E_INVALID;
+  if (n_experts < 1 || n_experts > 1024 || numel < 0 || n_jobs < 0 || n_jobs > FLUX_MERGE_MAX_JOBS ||
+      (compact != 0 && compact != 1))
+    return FLUX_E_INVALID;
+  if (numel % 8) return FLUX_E_UNSUPPORTED;
+  if (n_jobs == 0) return FLUX_OK;
+  if (!jobs) return FLUX_E_INVALID;
+  MergeBatch b{};
+  b.n_jobs = n_jobs;
+  b.E = n_experts;
+  b.numel = numel;
+  b.compact = compact;
+  b.contiguous = 1;
+  for (int j = 0; j < n_jobs; ++j) {
+    const flux_merge_job& J = jobs[j];
+    if (!J.experts || !J.cluster_of || !J.alpha || !J.out || !aligned16(J.experts) || !aligned16(J.out))
+      return FLUX_E_INVALID;
+    if (J.n_clusters < (compact ? 0 : 1) || J.n_clusters > n_experts) return FLUX_E_INVALID;
+    if (compact && (J.n_tuning < 0 || J.n_tuning + J.n_clusters > n_experts || J.n_tuning + J.n_clusters < 1))
+      return FLUX_E_INVALID;
+    b.jobs[j] = MergeJob{J.experts, J.cluster_of, J.alpha, J.out, J.remap, J.n_clusters,
+                         compact ? J.n_tuning + J.n_clusters : 0};
+  }
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  KernelTimer kt(K_MERGE, (cudaStream_t)stream);
+  cudaError_t e = launch_merge_batch(dtype == FLUX_FP32, b, (cudaStream_t)stream);
+  if (e != cudaSuccess) set_last_error("merge_batch", e);
+  return cuda_status(e);
 }
 
 /* ---------------------------------------------------------------- NEXT-2: compact model + output error */

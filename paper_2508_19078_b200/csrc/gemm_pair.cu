@@ -608,12 +608,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
 }
 }  // namespace
 
-cudaError_t launch_gemm_1sm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
-                            const CUtensorMap& b_s, const GemmArgs& g, cudaStream_t st);
-
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& g, cudaStream_t st) {
-  if (g.bm == 128) return launch_gemm_1sm(epi, a_r, a_s, b_r, b_s, g, st);
   if (g.bm != 256 || g.n_groups > kMaxGroups - 1) return cudaErrorInvalidValue;
   const Params p = make_params(g);
   // output tensor maps of the TMA-store epilogue: bf16 [rows][N], row stride ld, 32x64 boxes

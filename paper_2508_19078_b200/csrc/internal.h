@@ -47,6 +47,23 @@ const char* last_error();
 cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, int64_t R, int64_t K, void* q, float* s,
                             cudaStream_t st);
 // K7 (merge.cu)
+constexpr int kMergeMaxJobs = 256;
+struct MergeJob {           // one weight family of one layer
+  const void* experts;      // [E][numel]
+  const int32_t* cluster_of;// [E]
+  const float* alpha;       // [E]
+  void* merged;             // [n_out][numel]
+  int32_t* remap;           // [E] or null
+  int n_clusters;
+  int n_slots;              // compact mode: n_tun + n_clusters (0 = unknown, E used as the bound)
+};
+struct MergeBatch {
+  int n_jobs, E, compact, contiguous;
+  int64_t numel;
+  MergeJob jobs[kMergeMaxJobs];
+  int64_t chunk_prefix[kMergeMaxJobs + 1];  // filled by launch_merge_batch
+};
+cudaError_t launch_merge_batch(bool fp32, const MergeBatch& b, cudaStream_t st);
 cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
                          const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st, int compact = 0);
 // output error of a merged model: mean over tokens of 1 - cos(a_t, b_t)
@@ -140,7 +157,7 @@ struct GemmArgs {
   int64_t ld_r, ld_s;
   int64_t rows_r, rows_s;   // rows of out_r / out_s (TMA-store tensor maps of the CTA-pair kernel)
   int grid;
-  int bm;                   // rows per tile: 128 (1-CTA kernel) or 256 (CTA-pair kernel)
+  int bm;                   // rows per tile: 256 (CTA-pair kernel)
   // EPI_COMBINE only (shared-MLP down GEMM whose epilogue writes the layer output)
   const void* resid;        // bf16 [T][H]
   const void* y_perm;       // bf16 [T*k][H] routed expert outputs

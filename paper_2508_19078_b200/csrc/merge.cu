@@ -5,13 +5,26 @@
 // experts first in ascending id, then clusters 0..C-1: exps_config,
 // P:1013-1014).
 //
-// HBM-bound (read Σ|W_e| once, write Σ|W_c| once).  Every CTA builds the
-// member lists and fp32 weights of all clusters in shared memory (members in
-// ascending expert id, Σα accumulated in that order: deterministic); threads
-// then own 2 × 8 elements of one cluster output, load up to 4 members' 16-byte
-// vectors at once, accumulate w_e·W_e in fp32 (FMA chain in member order) and
-// round once.  A singleton cluster has w = α/α = 1 exactly, so its output is
-// the input bit for bit.
+// HBM-bound (read Σ|W_e| once, write Σ|W_c| once).  ONE launch covers a batch
+// of jobs (a job = one weight family of one layer: the bench merges all L x 3
+// families of a model in one persistent launch instead of 3L small ones, whose
+// ramp-up / tail cost ~20% of each short launch).  The work is cut into chunks
+// of 4,096 consecutive output elements (256 threads x 2 x 16-byte vectors);
+// every CTA owns a CONTIGUOUS range of chunks (equal counts: balanced), so it
+// rebuilds its member table only when its range crosses into the next output
+// (cluster or job) — a few times per CTA.
+//
+// Per output: the member list (ascending expert id) and fp32 weights
+// w_e = α_e / Σα (Σα accumulated in ascending id: deterministic) live in shared
+// memory.  Threads load up to 4 members' vectors before the first FMA (bytes in
+// flight per SM to cover HBM latency), accumulate w_e·W_e in fp32 (FMA chain in
+// member order) and round once.  A singleton cluster has w = α/α = 1 exactly,
+// so its output is the input bit for bit.
+//
+// Out-of-range labels: an expert whose cluster id is < -1 or >= n_clusters
+// belongs to no output; an output with no member is written as zeros.
+#include <algorithm>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -19,10 +32,10 @@ namespace flux {
 namespace {
 
 constexpr int kMaxE = 1024;
+constexpr int kThreads = 256;
 constexpr int kVecPerThread = 2;
+constexpr int64_t kChunkVecs = (int64_t)kVecPerThread * kThreads;  // 16-byte vectors per chunk
 
-// One 8-element vector kept raw until its FMA (bf16: one uint4 = 4 registers), so a thread can
-// hold many loads in flight.
 template <bool F32> struct Raw;
 template <> struct Raw<false> { uint4 a; };
 template <> struct Raw<true> { float4 a, b; };
@@ -70,141 +83,182 @@ __device__ __forceinline__ void store_vec(void* base, int64_t elem, const float 
   }
 }
 
-// compact = 0: outputs are the C clusters.  compact = 1 (NEXT-2): outputs are the slots of the
-// compact model in remap order — every tuning expert as its own slot (ascending id; a singleton
-// with weight α/α = 1, so its copy is bit-exact), then the C clusters.
-template <bool F32>
-__global__ void __launch_bounds__(256) merge_kernel(int E, int64_t numel, const void* __restrict__ experts,
-                                                    const int32_t* __restrict__ cluster_of,
-                                                    const float* __restrict__ alpha, int C, void* __restrict__ merged,
-                                                    int32_t* __restrict__ remap, int compact) {
-  __shared__ int s_cl[kMaxE];
-  __shared__ float s_w[kMaxE];       // weight of member slot
-  __shared__ int s_mem[kMaxE];       // member expert ids grouped by cluster
-  __shared__ int s_start[kMaxE + 1]; // cluster -> first member slot
-  __shared__ float s_alpha[kMaxE];
-  __shared__ int s_ntun;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    s_cl[e] = cluster_of[e];
-    s_alpha[e] = alpha[e];
-  }
-  __syncthreads();
-  if (compact) {  // relabel: tuning expert -> its rank among tuning experts, cluster c -> n_tun + c
-    if (threadIdx.x == 0) {
-      int n = 0;
-      for (int e = 0; e < E; ++e) n += s_cl[e] < 0;
-      s_ntun = n;
+struct SmemTable {
+  int lab[kMaxE];    // output index of every expert of the current job (-1: none)
+  int mem[kMaxE];    // members of the current output, ascending expert id
+  float w[kMaxE];    // their weights
+  int n_mem;
+  int n_tun;
+};
+
+// Labels of the experts of job j.  slot(e) = the compact-model slot: tuning experts
+// (cluster_of = -1) take 0..n_tun-1 in ascending id, cluster c takes n_tun + c; an out-of-range id has
+// no slot (-1).  Output index: compact = 1 -> slot(e); compact = 0 -> c for cluster_of = c in [0, C),
+// none (-1) for tuning experts.  remap (if any) = slot(e) in both modes.  Called by all threads.
+__device__ void build_labels(const MergeJob& job, int E, int compact, SmemTable& t) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();  // every thread is done with the previous job's tables
+  if (wid == 0) {
+    int n_tun = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      n_tun += __popc(__ballot_sync(0xffffffffu, e < E && __ldg(&job.cluster_of[e]) == -1));
     }
-    __syncthreads();
-    const int n_tun = s_ntun;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int r = 0;
-      for (int e = 0; e < E; ++e) s_cl[e] = s_cl[e] < 0 ? r++ : n_tun + s_cl[e];
-    }
-    C += n_tun;
-    __syncthreads();
-  }
-  // per cluster: count, Σα (ascending e), then the member slots
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    int cnt = 0;
-    for (int e = 0; e < E; ++e) cnt += s_cl[e] == c;
-    s_start[c + 1] = cnt;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s_start[0] = 0;
-    for (int c = 0; c < C; ++c) s_start[c + 1] += s_start[c];
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float asum = 0.f;
-    int cnt = 0;
-    for (int e = 0; e < E; ++e)
-      if (s_cl[e] == c) {
-        asum += s_alpha[e];
-        s_mem[s_start[c] + cnt++] = e;
+    int rank0 = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int cl = e < E ? __ldg(&job.cluster_of[e]) : -2;
+      const unsigned tun = __ballot_sync(0xffffffffu, cl == -1);
+      const bool in_range = cl >= 0 && cl < job.n_clusters;
+      const int slot = cl == -1 ? rank0 + __popc(tun & ((1u << lane) - 1u)) : in_range ? n_tun + cl : -1;
+      if (e < E) {
+        t.lab[e] = compact ? slot : (in_range ? cl : -1);
+        if (job.remap) job.remap[e] = slot;
       }
-    for (int i = 0; i < cnt; ++i) {
-      const int e = s_mem[s_start[c] + i];
-      s_w[s_start[c] + i] = asum > 0.f ? __fdiv_rn(s_alpha[e], asum) : __fdiv_rn(1.f, (float)cnt);
+      rank0 += __popc(tun);
+    }
+    if (lane == 0) t.n_tun = n_tun;
+  }
+  __syncthreads();
+}
+
+// Members (ascending id) and weights of output o of the current job.  Called by all threads.
+__device__ void build_members(const MergeJob& job, int E, int o, SmemTable& t) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();  // every thread is done with the previous output's members
+  if (wid == 0) {
+    int n = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const bool m = e < E && t.lab[e] == o;
+      const unsigned b = __ballot_sync(0xffffffffu, m);
+      if (m) t.mem[n + __popc(b & ((1u << lane) - 1u))] = e;
+      n += __popc(b);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      float asum = 0.f;
+      for (int i = 0; i < n; ++i) asum += __ldg(&job.alpha[t.mem[i]]);  // ascending id
+      for (int i = 0; i < n; ++i)
+        t.w[i] = asum > 0.f ? __fdiv_rn(__ldg(&job.alpha[t.mem[i]]), asum) : __fdiv_rn(1.f, (float)n);
+      t.n_mem = n;
     }
   }
   __syncthreads();
-  if (remap && blockIdx.x == 0 && threadIdx.x == 0) {
-    if (compact) {
-      for (int e = 0; e < E; ++e) remap[e] = s_cl[e];
-    } else {
-      int slot = 0;
-      for (int e = 0; e < E; ++e)
-        if (s_cl[e] == -1) remap[e] = slot++;
-      for (int e = 0; e < E; ++e)
-        if (s_cl[e] >= 0) remap[e] = slot + s_cl[e];
-    }
-  }
-  // Main loop: a CTA owns chunks of kVecPerThread·blockDim.x consecutive 16-byte vectors of one
-  // output (chunks dealt round-robin, so at any moment the CTAs stream neighbouring addresses);
-  // each thread issues the loads of up to 4 members × kVecPerThread vectors before the first FMA
-  // (bytes in flight per SM to cover HBM latency), then accumulates in member order — the same FMA
-  // chain as one member at a time, so results are unchanged bit for bit.
+}
+
+template <bool F32>
+__device__ __forceinline__ void merge_chunk(const MergeJob& job, int64_t numel, int o, int64_t v0,
+                                            const SmemTable& t) {
   const int64_t nvec = numel / 8;
-  const int64_t per_chunk = (int64_t)kVecPerThread * blockDim.x;
-  const int64_t chunks_per_c = (nvec + per_chunk - 1) / per_chunk;
-  const int64_t chunks = (int64_t)C * chunks_per_c;
-  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
-    const int c = (int)(ch / chunks_per_c);
-    const int64_t v0 = (ch - (int64_t)c * chunks_per_c) * per_chunk + threadIdx.x;
-    float acc[kVecPerThread][8];
+  float acc[kVecPerThread][8];
 #pragma unroll
-    for (int u = 0; u < kVecPerThread; ++u)
+  for (int u = 0; u < kVecPerThread; ++u)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
-    const int m_end = s_start[c + 1];
-    for (int m0 = s_start[c]; m0 < m_end; m0 += 4) {
-      Raw<F32> r[4][kVecPerThread];
+    for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
+  const int m_end = t.n_mem;
+  for (int m0 = 0; m0 < m_end; m0 += 4) {
+    Raw<F32> r[4][kVecPerThread];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (m0 + j < m_end) {
-          const int64_t base = (int64_t)s_mem[m0 + j] * numel;
+    for (int j = 0; j < 4; ++j)
+      if (m0 + j < m_end) {
+        const int64_t base = (int64_t)t.mem[m0 + j] * numel;
 #pragma unroll
-          for (int u = 0; u < kVecPerThread; ++u) {
-            const int64_t v = v0 + (int64_t)u * blockDim.x;
-            if (v < nvec) load_raw<F32>(experts, base + v * 8, r[j][u]);
-          }
+        for (int u = 0; u < kVecPerThread; ++u) {
+          const int64_t v = v0 + (int64_t)u * kThreads;
+          if (v < nvec) load_raw<F32>(job.experts, base + v * 8, r[j][u]);
         }
+      }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (m0 + j < m_end) {
-          const float wm = s_w[m0 + j];
+    for (int j = 0; j < 4; ++j)
+      if (m0 + j < m_end) {
+        const float wm = t.w[m0 + j];
 #pragma unroll
-          for (int u = 0; u < kVecPerThread; ++u) {
-            float f[8];
-            to_f32<F32>(r[j][u], f);
+        for (int u = 0; u < kVecPerThread; ++u) {
+          float f[8];
+          to_f32<F32>(r[j][u], f);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[u][i] = fmaf(wm, f[i], acc[u][i]);
-          }
+          for (int i = 0; i < 8; ++i) acc[u][i] = fmaf(wm, f[i], acc[u][i]);
         }
-    }
+      }
+  }
 #pragma unroll
-    for (int u = 0; u < kVecPerThread; ++u) {
-      const int64_t v = v0 + (int64_t)u * blockDim.x;
-      if (v < nvec) store_vec<F32>(merged, (int64_t)c * numel + v * 8, acc[u]);
+  for (int u = 0; u < kVecPerThread; ++u) {
+    const int64_t v = v0 + (int64_t)u * kThreads;
+    if (v < nvec) store_vec<F32>(job.merged, (int64_t)o * numel + v * 8, acc[u]);
+  }
+}
+
+// chunk_prefix[j] = first chunk of job j (chunks of job j = n_out_j · chunks per output).
+// contiguous = 1: CTA b owns chunks [b·n/G, (b+1)·n/G); 0: chunks dealt round-robin (single-job calls
+// whose output count is only an upper bound, compact mode).
+template <bool F32>
+__global__ void __launch_bounds__(kThreads) merge_batch_kernel(MergeBatch b) {
+  __shared__ SmemTable t;
+  const int64_t nvec = b.numel / 8;
+  const int64_t cpo = (nvec + kChunkVecs - 1) / kChunkVecs;  // chunks per output
+  const int64_t total = b.chunk_prefix[b.n_jobs];
+  int64_t ch0, ch1, step;
+  if (b.contiguous) {
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    ch0 = (int64_t)blockIdx.x * per;
+    ch1 = min(total, ch0 + per);
+    step = 1;
+  } else {
+    ch0 = blockIdx.x;
+    ch1 = total;
+    step = gridDim.x;
+  }
+  int j = 0, cur_job = -1, cur_o = -1;
+  for (int64_t ch = ch0; ch < ch1; ch += step) {
+    while (ch >= b.chunk_prefix[j + 1]) ++j;
+    const int64_t local = ch - b.chunk_prefix[j];
+    const int o = (int)(local / cpo);
+    const int64_t v0 = (local - (int64_t)o * cpo) * kChunkVecs + threadIdx.x;
+    if (j != cur_job) {
+      build_labels(b.jobs[j], b.E, b.compact, t);
+      cur_job = j;
+      cur_o = -1;
     }
+    if (b.compact && o >= t.n_tun + b.jobs[j].n_clusters) continue;  // beyond the job's slots (upper bound)
+    if (o != cur_o) {
+      build_members(b.jobs[j], b.E, o, t);
+      cur_o = o;
+    }
+    merge_chunk<F32>(b.jobs[j], b.numel, o, v0, t);
   }
 }
 }  // namespace
 
+cudaError_t launch_merge_batch(bool fp32, const MergeBatch& b0, cudaStream_t st) {
+  MergeBatch b = b0;
+  const int64_t cpo = (b.numel / 8 + kChunkVecs - 1) / kChunkVecs;
+  b.chunk_prefix[0] = 0;
+  for (int j = 0; j < b.n_jobs; ++j) {
+    const int64_t n_out = b.compact ? (b.jobs[j].n_slots > 0 ? b.jobs[j].n_slots : b.E) : b.jobs[j].n_clusters;
+    b.chunk_prefix[j + 1] = b.chunk_prefix[j] + n_out * cpo;
+  }
+  const int64_t total = b.chunk_prefix[b.n_jobs];
+  if (total == 0) return cudaSuccess;
+  // one resident wave: 3 (bf16) / 2 (fp32) CTAs per SM
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)kNumSMs * (fp32 ? 2 : 3)));
+  if (fp32)
+    merge_batch_kernel<true><<<grid, kThreads, 0, st>>>(b);
+  else
+    merge_batch_kernel<false><<<grid, kThreads, 0, st>>>(b);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
                          const float* alpha, int C, void* merged, int32_t* remap, cudaStream_t st, int compact) {
-  const int64_t per_chunk = (int64_t)kVecPerThread * 256;
-  const int64_t chunks = (int64_t)(compact ? E : C) * ((numel / 8 + per_chunk - 1) / per_chunk);  // upper bound (compact)
-  const unsigned grid = (unsigned)std::max<int64_t>(  // one resident wave: 3 (bf16) / 2 (fp32) CTAs per SM
-      1, std::min<int64_t>(chunks, (int64_t)kNumSMs * (fp32 ? 2 : 3)));
-  if (fp32)
-    merge_kernel<true><<<grid, 256, 0, st>>>(E, numel, experts, cluster_of, alpha, C, merged, remap, compact);
-  else
-    merge_kernel<false><<<grid, 256, 0, st>>>(E, numel, experts, cluster_of, alpha, C, merged, remap, compact);
-  return cudaGetLastError();
+  MergeBatch b{};
+  b.n_jobs = 1;
+  b.E = E;
+  b.numel = numel;
+  b.compact = compact;
+  b.contiguous = compact ? 0 : 1;  // compact: the slot count (n_tun + C) is known only on the device
+  b.jobs[0] = MergeJob{experts, cluster_of, alpha, merged, remap, C, 0};
+  return launch_merge_batch(fp32, b, st);
 }
 
 }  // namespace flux

@@ -5,12 +5,17 @@
 //                   per-tile counts -> tile_base[tile][e]; the last CTA to
 //                   finish (atomic ticket) scans the per-expert totals ->
 //                   offsets[e] and builds the tile prefix of both grouped GEMMs.
-//  scatter_kernel   (one warp per token): pos = offsets[e] + tile_base[tile][e]
-//                   + rank (rank from K1) -> token_index[pos] = t (ascending t
-//                   inside every segment: reading R3), inv_pos[t][j] = pos, and
-//                   the gather x[t] -> x_perm[pos] (16-byte vectors, x read
-//                   once, written k times).
+//  scatter_pick_kernel (one thread per pick (t, j); the default, when the
+//                   gate/up GEMM gathers its A rows from x itself):
+//                   pos = offsets[e] + tile_base[tile][e] + rank (rank from K1)
+//                   -> token_index[pos] = t (ascending t inside every segment:
+//                   reading R3), inv_pos[t][j] = pos.  k·12 bytes per token.
+//  scatter_kernel   (one warp per token; only when x_perm is materialised): the
+//                   same indices plus the gather x[t] -> x_perm[pos] (16-byte
+//                   vectors, x read once, written k times).
 // No atomics decide positions, so D_e is bitwise reproducible.
+#include <algorithm>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -141,7 +146,6 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
     inv_pos[t * k + lane] = p;
     if (p >= 0) token_index[p] = (int32_t)t;
   }
-  if (!x_perm) return;  // the GEMM gathers A rows from x itself (TMA tile::gather4)
   const int nvec = H / 8;  // 16-byte vectors per row
   const uint4* src = x + t * nvec;
   // four 16-byte vectors per lane in flight before the k copies are written
@@ -159,6 +163,26 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
     }
   }
 }
+// One thread per pick: coalesced reads of ids / rank, coalesced inv_pos writes; token_index writes
+// land in the expert segments (consecutive tokens of one expert are adjacent).  The per-tile bases
+// (n_tiles x E int32, <= 1 MB) stay in L2.
+__global__ void __launch_bounds__(256) scatter_pick_kernel(int64_t Tk, int E, int k, const int32_t* __restrict__ ids,
+                                                           const int32_t* __restrict__ rank,
+                                                           const int32_t* __restrict__ tile_base,
+                                                           const int32_t* __restrict__ offsets,
+                                                           int32_t* __restrict__ inv_pos,
+                                                           int32_t* __restrict__ token_index) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Tk; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = __ldcs(&ids[i]);
+    const int64_t t = i / k;
+    int p = -1;
+    if (e >= 0) {  // -1: a pick folded by gate re-routing (NEXT-2) owns no row
+      p = __ldg(&offsets[e]) + __ldg(&tile_base[(t / kRouterTile) * E + e]) + __ldcs(&rank[i]);
+      token_index[p] = (int32_t)t;
+    }
+    inv_pos[i] = p;
+  }
+}
 }  // namespace
 
 cudaError_t launch_schedule(const ScheduleArgs& a, cudaStream_t st) {
@@ -172,6 +196,12 @@ cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const 
                            const int32_t* tile_base, const int32_t* offsets, int32_t* inv_pos, int32_t* token_index,
                            void* x_perm, cudaStream_t st) {
   if (T == 0) return cudaSuccess;
+  if (!x_perm) {  // indices only
+    const int64_t Tk = T * k;
+    const unsigned grid = (unsigned)std::min<int64_t>((Tk + 255) / 256, (int64_t)kNumSMs * 8);
+    scatter_pick_kernel<<<grid, 256, 0, st>>>(Tk, E, k, ids, rank, tile_base, offsets, inv_pos, token_index);
+    return cudaGetLastError();
+  }
   const unsigned grid = (unsigned)((T + 7) / 8);
   scatter_kernel<<<grid, 256, 0, st>>>((const uint4*)x, T, H, E, k, ids, rank, tile_base, offsets, inv_pos,
                                        token_index, (uint4*)x_perm);

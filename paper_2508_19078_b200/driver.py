@@ -17,9 +17,9 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import (FLUX_OK, Comm, LayerOut, QLayer, attention_hist, cluster_experts, compact_experts, expert_features,
-               layer_budget,
-               make_cfg, merge_experts, output_error, profile_layer, profile_layer_workspace, quantize_weights)
+from . import (FLUX_OK, Comm, LayerOut, QLayer, attention_hist, cluster_experts, expert_features, layer_budget,
+               make_cfg, merge_experts_batch, output_error, profile_layer, profile_layer_workspace,
+               quantize_weights)
 
 
 @dataclass
@@ -34,14 +34,20 @@ class ModelShape:
     group_size: int
     norm_topk: int
     n_router: int = 0  # > 0: gate re-routing (NEXT-2): the router scores n_router original experts
+    # per-layer expert (slot) counts of a compact model with adaptive layer sizes (eq.(1)):
+    # layer l uses the first layer_experts[l] of the n_experts (= max) slots; None = n_experts everywhere
+    layer_experts: tuple | None = None
 
     @staticmethod
     def of(cfg) -> "ModelShape":
         return ModelShape(cfg.n_layers, cfg.hidden, cfg.n_experts, cfg.top_k, cfg.ffn, cfg.shared_ffn, cfg.wbits,
                           cfg.group_size, cfg.norm_topk)
 
-    def ccfg(self):
-        return make_cfg(self.hidden, self.ffn, self.n_experts, self.top_k, self.shared_ffn, self.wbits,
+    def experts_of(self, l: int) -> int:
+        return self.n_experts if self.layer_experts is None else int(self.layer_experts[l])
+
+    def ccfg(self, l: int = 0):
+        return make_cfg(self.hidden, self.ffn, self.experts_of(l), self.top_k, self.shared_ffn, self.wbits,
                         self.group_size, self.norm_topk, self.n_router)
 
 
@@ -141,14 +147,22 @@ def dense_model(m: MasterWeights) -> DenseWeights:
     return DenseWeights(shape, m.router, m.gate, m.up, m.down, m.sh_gate, m.sh_up, m.sh_down)
 
 
-def compact_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tensor, n_clusters: int,
-                  n_tuning: int = 0, stream=None, out: DenseWeights | None = None) -> DenseWeights:
+def _per_layer(v, L: int) -> list[int]:
+    return [int(v)] * L if np.isscalar(v) else [int(c) for c in v]
+
+
+def compact_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tensor, n_clusters,
+                  n_tuning=0, stream=None, out: DenseWeights | None = None) -> DenseWeights:
     """NEXT-2: the compact model (§7 "Customized MoE construction" + "Gate re-routing"): per layer the slots
-    [n_tuning tuning experts (ascending id), n_clusters eq.(2) merges] of every weight family
-    (flux_compact_experts) and the remap of the router's picks.  Every layer must keep n_tuning experts."""
+    [n_tuning[l] tuning experts (ascending id), n_clusters[l] eq.(2) merges] of every weight family and the
+    remap of the router's picks — ONE flux_merge_experts_batch launch (compact mode) for all L x 3 families.
+    n_clusters / n_tuning: an int (uniform) or per-layer counts (adaptive layer sizes, eq.(1) P:696-713);
+    n_tuning[l] must equal the number of -1 entries of cluster_of[l]."""
     s = m.shape
     L, E, F, H = s.n_layers, s.n_experts, s.ffn, s.hidden
-    S = n_tuning + n_clusters
+    Cl, Tl = _per_layer(n_clusters, L), _per_layer(n_tuning, L)
+    Sl = [c + t for c, t in zip(Cl, Tl)]
+    S = max(Sl)
     dev = m.gate.device
     if out is not None and out.gate.shape[1] == S:  # reuse the buffers of a previous round
         gate, up, down, remap = out.gate, out.up, out.down, out.remap
@@ -157,25 +171,30 @@ def compact_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tenso
         up = torch.empty_like(gate)
         down = torch.empty(L, S, H, F, dtype=m.gate.dtype, device=dev)
         remap = torch.empty(L, E, dtype=torch.int32, device=dev)
+    jobs = []
     for l in range(L):
-        compact_experts(m.gate[l].view(E, -1), cluster_of[l], alpha[l], n_clusters, gate[l].view(S, -1), remap[l],
-                        stream)
-        compact_experts(m.up[l].view(E, -1), cluster_of[l], alpha[l], n_clusters, up[l].view(S, -1), None, stream)
-        compact_experts(m.down[l].view(E, -1), cluster_of[l], alpha[l], n_clusters, down[l].view(S, -1), None,
-                        stream)
-    shape = ModelShape(L, H, S, s.top_k, F, s.shared_ffn, 16, 0, s.norm_topk, n_router=E)
+        for src, dst, rm in ((m.gate, gate, remap[l]), (m.up, up, None), (m.down, down, None)):
+            jobs.append(dict(experts=src[l].view(E, -1), cluster_of=cluster_of[l], alpha=alpha[l], n_clusters=Cl[l],
+                             n_tuning=Tl[l], out=dst[l].view(S, -1), remap=rm))
+    merge_experts_batch(jobs, compact=True, stream=stream)
+    shape = ModelShape(L, H, S, s.top_k, F, s.shared_ffn, 16, 0, s.norm_topk, n_router=E,
+                       layer_experts=None if len(set(Sl)) == 1 else tuple(Sl))
     return DenseWeights(shape, m.router, gate, up, down, m.sh_gate, m.sh_up, m.sh_down, remap)
 
 
 class Profiler:
     """Buffers for profiling T tokens through all layers (a1-a6) on one GPU."""
 
-    def __init__(self, shape: ModelShape, T: int, device="cuda", with_de: bool = True, with_logits: bool = False):
+    def __init__(self, shape: ModelShape, T: int, device="cuda", with_de: bool = True, with_logits: bool = False,
+                 policy=None):
         s = self.shape = shape
         self.T = T
+        self.policy = policy  # flux_policy (None = the library's measured defaults)
         L, E, H, k = s.n_layers, s.n_experts, s.hidden, s.top_k
-        self.cfg = s.ccfg()
-        self.ws = torch.empty(max(profile_layer_workspace(self.cfg, T), 1), dtype=torch.uint8, device=device)
+        self.cfgs = [s.ccfg(l) for l in range(L)]  # per-layer expert counts (adaptive layer sizes)
+        self.cfg = self.cfgs[0]
+        ws = max(profile_layer_workspace(c, T, policy) for c in self.cfgs)
+        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=device)
         self.y = torch.empty(2, T, H, dtype=torch.bfloat16, device=device)
         self.ids = torch.empty(L, T, k, dtype=torch.int32, device=device)
         self.w = torch.empty(L, T, k, dtype=torch.float32, device=device)
@@ -191,6 +210,12 @@ class Profiler:
         return LayerOut(self.y[l % 2].data_ptr(), p(self.ids), p(self.w), p(self.hist), p(self.offsets),
                         p(self.token_index), p(self.logits))
 
+    def run_layer(self, qm, l: int, x: torch.Tensor, residual: torch.Tensor | None = None, stream=None):
+        """One flux_profile_layer call with layer l's weights on x (no chaining); residual None = x (R6),
+        e.g. a zero buffer so that y is the MoE branch alone.  Accumulates into hist[l]; returns y."""
+        profile_layer(self.cfgs[l], qm.qlayer(l), x, residual, self.T, self.out(l), self.ws, stream, self.policy)
+        return self.y[l % 2]
+
     def run(self, qm: QuantizedModel, x: torch.Tensor, stream=None, on_layer=None, zero_hist: bool = True,
             attn: torch.Tensor | None = None):
         """Profile x [T][H] (bf16, device) through every layer; returns the last layer's y.
@@ -205,7 +230,7 @@ class Profiler:
                 self.ahist.zero_()
         cur = x
         for l in range(self.shape.n_layers):
-            profile_layer(self.cfg, qm.qlayer(l), cur, None, self.T, self.out(l), self.ws, stream)
+            profile_layer(self.cfgs[l], qm.qlayer(l), cur, None, self.T, self.out(l), self.ws, stream, self.policy)
             if attn is not None:
                 attention_hist(self.ids[l], attn[l], self.shape.n_experts, self.ahist[l], stream)
             cur = self.y[l % 2]
@@ -230,28 +255,34 @@ def frequencies(hist_host: np.ndarray, T_total: int) -> np.ndarray:
 
 @dataclass
 class MergedModel:
-    gate: torch.Tensor
+    gate: torch.Tensor   # [L][C_max][F][H]; layer l uses its first n_clusters[l] rows
     up: torch.Tensor
-    down: torch.Tensor
-    remap: torch.Tensor
+    down: torch.Tensor   # [L][C_max][H][F]
+    remap: torch.Tensor  # [L][E]
+    n_clusters: tuple = ()
 
 
-def merge_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tensor, n_clusters: int,
+def merge_model(m: MasterWeights, alpha: torch.Tensor, cluster_of: torch.Tensor, n_clusters,
                 out: MergedModel | None = None, stream=None) -> MergedModel:
-    """a8: eq.(2) for every layer and weight family. alpha fp32 [L][E], cluster_of int32 [L][E] (device)."""
+    """a8: eq.(2) for every layer and weight family in ONE flux_merge_experts_batch launch.
+    alpha fp32 [L][E], cluster_of int32 [L][E] (device); n_clusters an int or per-layer budgets B(l)."""
     s = m.shape
-    L, E, F, H, C = s.n_layers, s.n_experts, s.ffn, s.hidden, n_clusters
-    if out is None:
+    L, E, F, H = s.n_layers, s.n_experts, s.ffn, s.hidden
+    Cl = _per_layer(n_clusters, L)
+    C = max(Cl)
+    if out is None or out.gate.shape[1] != C:
         dev = m.gate.device
         out = MergedModel(torch.empty(L, C, F, H, dtype=m.gate.dtype, device=dev),
                           torch.empty(L, C, F, H, dtype=m.gate.dtype, device=dev),
                           torch.empty(L, C, H, F, dtype=m.gate.dtype, device=dev),
                           torch.empty(L, E, dtype=torch.int32, device=dev))
+    out.n_clusters = tuple(Cl)
+    jobs = []
     for l in range(L):
-        merge_experts(m.gate[l].view(E, -1), cluster_of[l], alpha[l], C, out.gate[l].view(C, -1), out.remap[l],
-                      stream)
-        merge_experts(m.up[l].view(E, -1), cluster_of[l], alpha[l], C, out.up[l].view(C, -1), None, stream)
-        merge_experts(m.down[l].view(E, -1), cluster_of[l], alpha[l], C, out.down[l].view(C, -1), None, stream)
+        for src, dst, rm in ((m.gate, out.gate, out.remap[l]), (m.up, out.up, None), (m.down, out.down, None)):
+            jobs.append(dict(experts=src[l].view(E, -1), cluster_of=cluster_of[l], alpha=alpha[l],
+                             n_clusters=Cl[l], out=dst[l].view(C, -1), remap=rm))
+    merge_experts_batch(jobs, stream=stream)
     return out
 
 

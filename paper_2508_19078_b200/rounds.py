@@ -16,10 +16,19 @@ Here a round is:
   stale  (Fig. 7b): foreground stream (high priority): merge(f^{r-1}) -> fine-tune;
                     background stream (low priority): profile -> f^r for the next round.
 Both are measured with CUDA events on their streams: the fine-tuning start latency (round start ->
-merged model ready) and the round makespan.  Buffers and sequencing only; all arithmetic is in
-libflux.
+merged model ready) and the GPU span of the round.
+
+Round makespan with the server's aggregation (Fig. 7: "the latency of model aggregation on
+the server ... the participant is idle"): after fine-tuning, the participant uploads its update and waits
+for the aggregated model; that wait W is modelled (agg_wait_s, an input — the paper gives no number) as
+an idle period on the host.  Serial: profile -> merge -> fine-tune -> wait W.  Stale: merge(f^{r-1}) ->
+fine-tune -> wait W on the foreground while the background profile of w_r runs on the GPU, so the
+profile hides inside the wait.  The makespan is host wall-clock from the round start until both the
+wait and every GPU stream are done.  Buffers and sequencing only; all arithmetic is in libflux.
 """
 from __future__ import annotations
+
+import time
 
 import numpy as np
 import torch
@@ -30,7 +39,8 @@ from .driver import (MasterWeights, ModelShape, Profiler, QuantizedModel, cluste
 
 class Participant:
     def __init__(self, masters: MasterWeights, x_prof: torch.Tensor, x_ft: torch.Tensor, comm, n_clusters: int,
-                 T_total: int, clustering: str = "pca", seeded_cluster_of: torch.Tensor | None = None):
+                 T_total: int, clustering: str = "pca", seeded_cluster_of: torch.Tensor | None = None,
+                 agg_wait_s: float = 0.0):
         s = masters.shape
         self.m = masters
         self.shape = s
@@ -38,6 +48,7 @@ class Participant:
         self.C = n_clusters
         self.T_total = T_total
         self.clustering = clustering
+        self.agg_wait_s = agg_wait_s  # modelled server-aggregation wait after fine-tuning
         self.x_prof, self.x_ft = x_prof, x_ft
         self.qm = QuantizedModel(s)
         self.prof = Profiler(s, x_prof.shape[0], with_de=True)
@@ -90,31 +101,43 @@ class Participant:
 
     # ------------------------------------------------------------------ rounds
     def round_serial(self):
-        """Fig. 7a: profile w_r, then merge with f^r, then fine-tune (one stream)."""
+        """Fig. 7a: profile w_r, then merge with f^r, then fine-tune (one stream), then wait for aggregation."""
         st = self.fg
         e0, em, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        torch.cuda.synchronize()
+        h0 = time.perf_counter()
         e0.record(st)
         self.profile(st)
         self.absorb_statistics()  # host waits: the merge needs f^r
         self.merge_and_finetune(st, em)
         e1.record(st)
         e1.synchronize()
-        return {"ft_start_ms": e0.elapsed_time(em), "round_ms": e0.elapsed_time(e1)}
+        time.sleep(self.agg_wait_s)  # upload + server aggregation + download: the participant idles
+        makespan = time.perf_counter() - h0
+        return {"ft_start_ms": e0.elapsed_time(em), "round_ms": e0.elapsed_time(e1), "makespan_ms": 1e3 * makespan}
 
     def round_stale(self):
-        """Fig. 7b: merge with the stale f^{r-1} and fine-tune at once; profile w_r in the background."""
+        """Fig. 7b: merge with the stale f^{r-1} and fine-tune at once; profile w_r in the background, hidden
+        behind the aggregation wait."""
         e0, em, efg, ebg = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+        torch.cuda.synchronize()
+        h0 = time.perf_counter()
         e0.record(self.fg)
         self.merge_and_finetune(self.fg, em)  # foreground first: uses f^{r-1} (self.alpha, self.cluster_of)
         efg.record(self.fg)
         self.bg.wait_event(e0)
         self.profile(self.bg)                 # background: f^r for the next round
         ebg.record(self.bg)
+        efg.synchronize()                     # fine-tuning done: upload, wait for the aggregated model
+        time.sleep(self.agg_wait_s)
+        ebg.synchronize()
+        makespan = time.perf_counter() - h0
         self.fg.wait_event(ebg)
         e_end = torch.cuda.Event(enable_timing=True)
         e_end.record(self.fg)
         e_end.synchronize()
         out = {"ft_start_ms": e0.elapsed_time(em), "round_ms": e0.elapsed_time(e_end),
-               "finetune_done_ms": e0.elapsed_time(efg), "profile_done_ms": e0.elapsed_time(ebg)}
+               "finetune_done_ms": e0.elapsed_time(efg), "profile_done_ms": e0.elapsed_time(ebg),
+               "makespan_ms": 1e3 * makespan}
         self.absorb_statistics()  # f^r becomes the next round's stale statistics
         return out

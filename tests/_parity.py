@@ -108,3 +108,82 @@ def check_hist_and_de(ids_gpu, hist_gpu, offsets_gpu, token_index_gpu, E):
     order = order[flat[order] >= 0]
     want = (order // k).astype(np.int32)
     assert np.array_equal(token_index_gpu[:len(want)], want)
+
+
+# ---------------------------------------------------------------------------------------------
+# MoE-branch parity (residual r = 0, so y = bf16(sh + Σ_j w_j o_j) is the expert branch alone)
+# ---------------------------------------------------------------------------------------------
+# Element-wise, condition-aware bounds.  From the oracle, per output element:
+#   cond = |sh| + Σ_j w_j|o_j|                 magnitude of the terms of the O6 sum
+#   dmax = max_f|a_sh,f ŵ_hf| + Σ_j w_j max_f|a_jf ŵ_hf|   largest down-projection term behind it
+# Two correct implementations of R4/R6 differ only where a bf16 storage point rounds to the other
+# neighbour: an o_j or sh (<= one bf16 ulp <= 2^-7 of it), an act value a_f (moves its down term by
+# <= 2^-7 of it; a few per expert row at most), and y itself (one ulp).  So
+#   arithmetic bound:   |Δy| <= ulp(y) + 2^-7·(cond + 2·dmax)      (allows two act flips per element)
+#   north star (2e-2):  |Δy| <= ulp(y) + 2e-2·(cond + dmax)
+# Where the terms do not cancel and no single down term dominates, cond + dmax ≈ |y| and the north
+# star's bound reads |Δy| <= 2e-2·|y| + 1 ulp.
+BRANCH_TOL = 2e-2
+BRANCH_TIGHT = 2.0 ** -7
+
+
+def bf16_ulp(v):
+    """ulp of the bf16 format (8 significant bits) at |v|; the smallest subnormal at 0."""
+    m = np.abs(np.asarray(v, np.float64))
+    e = np.floor(np.log2(np.where(m > 0, m, 1.0)))
+    return np.where(m > 0, 2.0 ** (e - 7), 2.0 ** -133)
+
+
+def branch_bound(y_gpu, y_ref, cond, dmax, tight):
+    u = bf16_ulp(np.maximum(np.abs(y_gpu), np.abs(y_ref)))
+    return u + (BRANCH_TIGHT * (cond + 2 * dmax) if tight else BRANCH_TOL * (cond + dmax))
+
+
+def branch_violations(y_gpu, y_ref, cond, dmax, tight):
+    """Boolean mask of elements outside the bound (tight = the arithmetic bound, else the north star's)."""
+    d = np.abs(np.asarray(y_gpu, np.float64) - y_ref)
+    return d > branch_bound(y_gpu, y_ref, cond, dmax, tight)
+
+
+def compare_branch(ref, gpu, tight=True, stats=None):
+    """ref: oracle.model.branch_tokens() dict; gpu: logits, ids, w, y for the same tokens (layer input =
+    the generated x_0, identical on both sides, so no input term).  Asserts the router contract and the
+    element-wise bounds on every token with the oracle's routing; returns (n_compared, n_near_tie, worst
+    ratio |Δ| / north-star bound).  stats (dict, optional) collects ratio arrays for reports."""
+    z_ref, k = ref["z"], ref["ids"].shape[1]
+    n_cmp = n_tie = 0
+    worst = 0.0
+    for t in range(z_ref.shape[0]):
+        zr = z_ref[t]
+        assert np.all(np.abs(gpu["logits"][t] - zr) <= LOGIT_TOL * max(np.max(np.abs(zr)), 1e-30)), t
+        s_ref, s_gpu = set(ref["ids"][t].tolist()), set(gpu["ids"][t].tolist())
+        if ref["margin"][t] <= MARGIN:
+            n_tie += 1
+            chosen = [zr[e] for e in s_gpu]
+            unchosen = [zr[e] for e in range(len(zr)) if e not in s_gpu]
+            if unchosen:
+                assert min(chosen) >= max(unchosen) - MARGIN, t
+            if s_gpu != s_ref:
+                continue  # a valid near-tie routing: a different (correct) output
+        else:
+            assert s_gpu == s_ref, (t, s_gpu, s_ref)
+        assert len(s_gpu) == k
+        yg, yr, c, dm = gpu["y"][t], ref["y"][t], ref["cond"][t], ref["dmag"][t]
+        d = np.abs(yg - yr)
+        r_ns = d / branch_bound(yg, yr, c, dm, False)
+        r_t = d / branch_bound(yg, yr, c, dm, True)
+        if stats is not None:
+            stats.setdefault("ns", []).append(r_ns)
+            stats.setdefault("tight", []).append(r_t)
+            stats.setdefault("literal", []).append(d / (BRANCH_TOL * np.abs(yr) + bf16_ulp(yr)))
+            stats.setdefault("exact", []).append(d == 0)
+        else:
+            bad = r_ns > 1
+            assert not bad.any(), ("2e-2", t, np.nonzero(bad)[0][:8], yg[bad][:8], yr[bad][:8])
+            bad = r_t > 1
+            if tight:
+                assert not bad.any(), ("tight", t, np.nonzero(bad)[0][:8], yg[bad][:8], yr[bad][:8], c[bad][:8],
+                                       dm[bad][:8])
+        worst = max(worst, float(r_ns.max()))
+        n_cmp += 1
+    return n_cmp, n_tie, worst

@@ -79,7 +79,7 @@ def test_budget_host_matches_oracle(F):
         T = int(rng.integers(100, 10**6))
         hist = rng.integers(0, T, size=(L, E)).astype(np.int64)
         B_non = int(rng.integers(0, 2000))
-        n_non = rng.integers(0, E + 1, size=L).astype(np.int32)
+        n_non = rng.integers(0, E + 1, size=L).astype(np.int32) if rng.random() < 0.5 else None
         C, over = F.layer_budget(hist, T, B_non, n_non)
         Cr, _, _, over_r = oracle.layer_budget(hist, T, B_non, n_non)
         assert np.array_equal(C, Cr) and over == over_r

@@ -53,3 +53,17 @@ def test_product_arm_line():
     assert line["gpu_launches"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"] or {"sm_mhz": 0, "sm_max_mhz": 0, "reasons": []})
+
+
+def test_launcher_spawns_the_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks (gloo self-test on CPU): rank 0
+    sees the world of 2, both ranks join the all-reduce, and the shards start at 0 and 1000."""
+    line = _run(["--gpus", "2", "--selftest-launcher"], 300)
+    assert line == {"n_gpus": 2, "ranks_seen": 2, "shard_starts_sum": 1000, "gpus_arg": 2}
+
+
+def test_launcher_rejects_a_world_mismatch():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--selftest-launcher"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=120, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE=1" in out.stdout

@@ -70,7 +70,7 @@ def test_degenerate_case_parity(name):
 
 
 @pytest.mark.parametrize("name", list(EDGE))
-def test_degenerate_cases_on_every_gemm_path(name, monkeypatch):
+def test_degenerate_cases_on_every_gemm_path(name):
     """Small batches take the fused-dequant GEMM with materialised x_perm by policy; the same degenerate
     inputs through the dequant-pass CTA-pair GEMM (routed rows gathered in-kernel with cp.async, or
     materialised) must give bit-identical outputs, ids and histograms."""
@@ -82,15 +82,9 @@ def test_degenerate_cases_on_every_gemm_path(name, monkeypatch):
     qm.quantize_from(synthetic.master_weights(cfg))
     x = synthetic.tokens(cfg, 0, cfg.tokens)
     outs = []
-    for env in ({"FLUX_GEMM_FUSED_DEQUANT": "1"}, {"FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GATHER_A": "0"}, {"FLUX_GEMM_1SM": "1"},
-                {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GEMM_DYNAMIC": "0"}):
-        for k in ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM", "FLUX_GATHER_A",
-                  "FLUX_GEMM_DYNAMIC"):
-            monkeypatch.delenv(k, raising=False)
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        prof = Profiler(shape, cfg.tokens)
+    import paper_2508_19078_b200 as F
+    for pol in ((2, 0, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (1, 0, 0, 1), (0, 0, 0, 0)):
+        prof = Profiler(shape, cfg.tokens, policy=F.make_policy(*pol))
         prof.run(qm, x)
         torch.cuda.synchronize()
         outs.append((prof.y[(cfg.n_layers - 1) % 2].clone(), prof.ids.clone(), prof.hist.clone()))

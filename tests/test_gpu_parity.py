@@ -116,11 +116,20 @@ def test_chunk_and_run_invariance():
     assert torch.equal(torch.cat([ya, yb]), y_full)
 
 
+# every flux_policy combination the bit-identity test pins (weight path, routed rows, fused combine, static tiles)
+POLICIES = [(2, 0, 0, 0), (1, 0, 0, 0), (2, 1, 0, 0), (2, 0, 1, 0), (1, 0, 1, 0), (2, 2, 0, 0), (1, 2, 0, 0),
+            (1, 1, 0, 0), (1, 0, 0, 1), (1, 0, 1, 1), (1, 1, 0, 1), (0, 0, 0, 0), (1, 0, 0, 0, 0x100 | 7),
+            (1, 0, 0, 0, 0x100 | 0)]
+
+
 @pytest.mark.parametrize("name", ["int4_shared", "int8_ragged", "int4_e64", "pass_tails", "pass_tails_g64"])
-def test_weight_paths_bit_identical(name, monkeypatch):
-    """Fused in-GEMM dequantization, the separate dequant pass (CTA-pair GEMM) and the 1-CTA GEMM, with
-    the routed A rows materialised (x_perm) or gathered inside the GEMM (cp.async: the pass-path
-    default; TMA gather4), all produce bit-identical layers: the choice is a pure performance policy."""
+def test_weight_paths_bit_identical(name):
+    """Every flux_policy value — in-GEMM dequantization or the separate dequant pass, the routed A rows
+    materialised (x_perm), gathered inside the GEMM with cp.async (the pass-path default) or with TMA
+    gather4 (test-only), the combine standalone or fused into the shared down GEMM (test-only), claimed or
+    static tile order (test-only), every L2-hint combination — produces bit-identical layers: the choice is
+    a pure performance policy."""
+    import paper_2508_19078_b200 as F
     from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
     from paper_2508_19078_b200 import synthetic
     cfg = SMALL[name]
@@ -129,24 +138,8 @@ def test_weight_paths_bit_identical(name, monkeypatch):
     qm.quantize_from(synthetic.master_weights(cfg))
     x = synthetic.tokens(cfg, 0, cfg.tokens)
     outs = []
-    for env in ({"FLUX_GEMM_FUSED_DEQUANT": "1"}, {"FLUX_GEMM_DEQUANT_PASS": "1"}, {"FLUX_GEMM_1SM": "1"},
-                {"FLUX_FUSED_COMBINE": "1", "FLUX_GEMM_FUSED_DEQUANT": "1"},
-                {"FLUX_FUSED_COMBINE": "1", "FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GATHER_A": "1", "FLUX_GEMM_FUSED_DEQUANT": "1"},
-                {"FLUX_GATHER_A": "1", "FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GATHER_A": "2", "FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GATHER_A": "0", "FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GEMM_DYNAMIC": "1", "FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GEMM_DYNAMIC": "1", "FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_FUSED_COMBINE": "1"},
-                {"FLUX_GEMM_DYNAMIC": "1", "FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GATHER_A": "0"},
-                {"FLUX_GEMM_DYNAMIC": "0", "FLUX_GEMM_DEQUANT_PASS": "1"},
-                {"FLUX_GEMM_DYNAMIC": "0", "FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_FUSED_COMBINE": "1"}):
-        for k in ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM", "FLUX_FUSED_COMBINE",
-                  "FLUX_GATHER_A", "FLUX_GEMM_DYNAMIC"):
-            monkeypatch.delenv(k, raising=False)
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        prof = Profiler(shape, cfg.tokens)
+    for pol in POLICIES:
+        prof = Profiler(shape, cfg.tokens, policy=F.make_policy(*pol))
         prof.run(qm, x)
         torch.cuda.synchronize()
         outs.append((prof.y[(cfg.n_layers - 1) % 2].clone(), prof.ids.clone(), prof.hist.clone()))

@@ -54,6 +54,9 @@ def test_budget_clamps():
     assert list(C) == [1, 1, 1]  # never zero experts in a layer
     C, *_ = oracle.layer_budget(hist, T, 3000, n_non=np.array([5, 5, 5]))
     assert list(C) == [5, 5, 5]  # never more than the layer's non-tuning experts
+    E = hist.shape[1]
+    C, *_ = oracle.layer_budget(hist, T, 10 * E)
+    assert list(C) == [E, E, E]  # no n_non: every expert is non-tuning, so at most E (R9)
 
 
 # ---------------------------------------------------------------- eq.(2)

@@ -127,3 +127,115 @@ def test_zero_down_row_keeps_bias_feature():
     x[:, 0] = 1.0
     y, *_ = oracle.moe_tokens(x, rng.standard_normal((E, H)), experts, None, k=2, group_size=0, norm=1)
     assert np.all(y[:, 0] == 1.0)
+
+
+def _dense_equivalent(x, z, experts, k, norm, grouped, shared=None):
+    """Independent numpy/torch formulation of O4-O6 without the residual: every expert on every token
+    (weights dequantized per R1b with torch's bf16 conversions), masked by the top-k set; returns
+    (branch sum Σ_j w_j o_j + sh [n][H] unrounded, magnitude Σ_j w_j|o_j| + |sh| [n][H])."""
+    n = x.shape[0]
+    E = len(experts)
+    X = torch.from_numpy(x)
+
+    def run(ex, want_mag=False):
+        qg, qu, qd, sg, su, sd = ex.arrs
+        Wg, Wu, Wd = (torch.from_numpy(_deq(a, b, grouped)) for a, b in ((qg, sg), (qu, su), (qd, sd)))
+        a = _bf16_torch(torch.nn.functional.silu(X @ Wg.T) * (X @ Wu.T))
+        if want_mag:  # max_f |a_f·ŵd_hf|
+            return (a.abs()[:, None, :] * Wd.abs()[None, :, :]).amax(-1).numpy()
+        return _bf16_torch(a @ Wd.T).numpy()
+
+    outs = np.stack([run(ex) for ex in experts], 1)  # [n][E][H]
+    dots = np.stack([run(ex, True) for ex in experts], 1)
+    p = np.exp(z - z.max(1, keepdims=True))
+    p /= p.sum(1, keepdims=True)
+    mask = np.zeros((n, E))
+    for t in range(n):
+        sel = np.argsort(-z[t], kind="stable")[:k]
+        mask[t, sel] = p[t, sel] / (p[t, sel].sum() if norm else 1.0)
+    branch = np.einsum("te,teh->th", mask, outs)
+    mag = np.einsum("te,teh->th", mask, np.abs(outs))
+    dmag = np.einsum("te,teh->th", mask, dots)
+    if shared is not None:
+        o_sh = run(shared)
+        branch = branch + o_sh
+        mag = mag + np.abs(o_sh)
+        dmag = dmag + run(shared, True)
+    _dense_equivalent.dmag = dmag
+    return branch, mag
+
+
+@pytest.mark.parametrize("wbits,g,norm,with_shared", [(8, 0, 1, False), (4, 16, 0, True), (4, 32, 1, True)])
+def test_zero_residual_is_the_moe_branch(wbits, g, norm, with_shared):
+    """R6 with r = 0: y = bf16(sh + Σ_j w_j o_j) — the MoE branch alone, checked against the
+    dense-equivalent formulation; cond = |sh| + Σ_j w_j|o_j| exactly (up to summation order)."""
+    rng = np.random.default_rng(31 + wbits + g)
+    H, F, Fs, E, k, n = 64, 64, 96, 6, 2, 40
+    experts = [_rand_expert(rng, H, F, wbits, g) for _ in range(E)]
+    sh = _rand_expert(rng, H, Fs, wbits, g) if with_shared else None
+    x = _bf16_x(rng, n, H)
+    wr = rng.standard_normal((E, H))
+    y, ids, w, z, _, cond, dmag = oracle.moe_tokens(x, wr, experts, sh, k=k, group_size=g, norm=norm,
+                                                    residual=np.zeros_like(x), with_cond=True)
+    branch, mag = _dense_equivalent(x, z, experts, k, norm, g != 0, sh)
+    ref = oracle.bf16_round(branch)
+    assert np.all(_ulps_close(y, ref)) and np.mean(y == ref) > 0.98
+    assert np.allclose(cond, mag, rtol=1e-12, atol=1e-300)
+    assert np.allclose(dmag, _dense_equivalent.dmag, rtol=1e-12, atol=1e-300)
+    assert np.all(cond <= dmag * 64 * (1 + 2.0 ** -8) + 1e-300)  # |o_h| <= F·max_f |a_f w_hf| (F = 64)
+    # the zero-residual output is NOT the residual output minus x: the residual changes the rounding
+    y_r, *_ = oracle.moe_tokens(x, wr, experts, sh, k=k, group_size=g, norm=norm)
+    assert np.all(_ulps_close(y_r, oracle.bf16_round(x + branch)))
+    assert np.abs(y).max() < np.abs(y_r).max()  # the branch alone is small next to the residual stream
+
+
+def test_residual_array_and_cond_bound():
+    """An explicit residual r replaces x in O6 (R6); cond = |r| + |sh| + Σ w|o| bounds |y| (up to the
+    final rounding) and equals |y| exactly when every term of the sum is non-negative."""
+    rng = np.random.default_rng(41)
+    H, F, E, k, n = 32, 48, 5, 3, 25
+    experts = [_rand_expert(rng, H, F, 8, 0) for _ in range(E)]
+    x = _bf16_x(rng, n, H)
+    r = _bf16_x(rng, n, H)
+    wr = rng.standard_normal((E, H))
+    y, ids, w, z, _, cond, dmag = oracle.moe_tokens(x, wr, experts, None, k=k, group_size=0, norm=0, residual=r,
+                                                    with_cond=True)
+    branch, mag = _dense_equivalent(x, z, experts, k, 0, False)
+    assert np.all(_ulps_close(y, oracle.bf16_round(r + branch)))
+    assert np.allclose(cond, np.abs(r) + mag, rtol=1e-12)
+    assert np.all(np.abs(y) <= cond * (1 + 2.0 ** -8) + 1e-300)
+    # all terms non-negative: zero routed weights (E experts, q_down = 0) and r >= 0 -> cond == |r| == |y|
+    for ex in experts:
+        ex.arrs[2][:] = 0
+    y0, *_, cond0, _ = oracle.moe_tokens(x, wr, experts, None, k=k, group_size=0, norm=0, residual=np.abs(r),
+                                      with_cond=True)
+    assert np.array_equal(cond0, np.abs(r)) and np.array_equal(y0, np.abs(r))
+
+
+def test_exact_dequant_variant():
+    """SURVEY O4's literal reading ŵ = q·s (kept only to show that R1b is not load-bearing): identical to
+    R1b for per-channel codes; for grouped codes it equals a dense layer with the exact q·s weights."""
+    rng = np.random.default_rng(43)
+    H, F, E, k, n = 64, 64, 4, 2, 20
+    x = _bf16_x(rng, n, H)
+    wr = rng.standard_normal((E, H))
+    pc = [_rand_expert(rng, H, F, 8, 0) for _ in range(E)]
+    a = oracle.moe_tokens(x, wr, pc, None, k=k, group_size=0, norm=1)[0]
+    b = oracle.moe_tokens(x, wr, pc, None, k=k, group_size=0, norm=1, exact_dequant=True)[0]
+    assert np.array_equal(a, b)
+    gr = [_rand_expert(rng, H, F, 4, 16) for _ in range(E)]
+    y, ids, w, z, _ = oracle.moe_tokens(x, wr, gr, None, k=k, group_size=16, norm=1, exact_dequant=True,
+                                        residual=np.zeros_like(x))
+    X = torch.from_numpy(x)
+    outs = []
+    for ex in gr:
+        qg, qu, qd, sg, su, sd = ex.arrs
+        Wg, Wu, Wd = (torch.from_numpy(q.astype(np.float64) * np.repeat(s, 16, axis=1).astype(np.float64))
+                      for q, s in ((qg, sg), (qu, su), (qd, sd)))
+        act = _bf16_torch(torch.nn.functional.silu(X @ Wg.T) * (X @ Wu.T))
+        outs.append(_bf16_torch(act @ Wd.T).numpy())
+    outs = np.stack(outs, 1)
+    ref = oracle.bf16_round(np.stack([sum(w[t, j] * outs[t, ids[t, j]] for j in range(k)) for t in range(n)]))
+    assert np.all(_ulps_close(y, ref))
+    y_r1b = oracle.moe_tokens(x, wr, gr, None, k=k, group_size=16, norm=1, residual=np.zeros_like(x))[0]
+    assert not np.array_equal(y, y_r1b)  # the two readings differ (by bf16 rounding of the weights)

@@ -1,7 +1,7 @@
 """Small workload that calls every libflux entry point once (run under compute-sanitizer by
-tools/sanitize.sh): quantize (INT8/INT4/INT2), the profile pass on every GEMM path (fused-dequant,
-dequant pass with the in-GEMM cp.async gather, materialised x_perm, TMA gather4, fused combine,
-1-CTA), features + K-Means, merge, compact model forward with gate re-routing, attention histogram,
+tools/sanitize.sh): quantize (INT8/INT4/INT2), the profile pass on every GEMM path (flux_policy: in-GEMM
+dequant, dequant pass with the in-GEMM cp.async gather, materialised x_perm, TMA gather4, fused combine,
+static tiles), features + K-Means, merge, compact model forward with gate re-routing, attention histogram,
 output error.  Sizes are tiny: the sanitizers replay every memory access."""
 import os
 import sys
@@ -18,19 +18,8 @@ from paper_2508_19078_b200 import synthetic  # noqa: E402
 from paper_2508_19078_b200.driver import (ModelShape, Profiler, QuantizedModel, cluster_model,  # noqa: E402
                                           compact_model, dense_model, expert_features_model, merge_model)
 
-ENV = ("FLUX_GEMM_FUSED_DEQUANT", "FLUX_GEMM_DEQUANT_PASS", "FLUX_GEMM_1SM", "FLUX_GATHER_A", "FLUX_FUSED_COMBINE")
-PATHS = [{"FLUX_GEMM_FUSED_DEQUANT": "1"}, {"FLUX_GEMM_DEQUANT_PASS": "1"},
-         {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GATHER_A": "0"}, {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_GATHER_A": "1"},
-         {"FLUX_GEMM_DEQUANT_PASS": "1", "FLUX_FUSED_COMBINE": "1"}, {"FLUX_GEMM_1SM": "1"}]
-
-
-# SAN_PATHS=1sm: every GEMM (also the compact / dense forwards) on the 1-CTA kernel, whose epilogue
-# writes with per-thread global stores — initcheck does not see TMA tensor stores as initialising
-# memory, so on the CTA-pair paths it reports every read of a TMA-stored buffer (act, y_perm, y_sh)
-if os.environ.get("SAN_PATHS") == "1sm":
-    ENV = ()
-    PATHS = [{"FLUX_GEMM_1SM": "1"}]
-    os.environ["FLUX_GEMM_1SM"] = "1"
+# flux_policy (weight_path, routed_rows, fused_combine, static_tiles)
+PATHS = [(2, 0, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (1, 2, 0, 0), (1, 0, 1, 0), (1, 0, 0, 1)]
 
 
 def run(cfg, paths):
@@ -39,15 +28,10 @@ def run(cfg, paths):
     qm = QuantizedModel(shape)
     qm.quantize_from(masters)
     x = synthetic.tokens(cfg, 0, cfg.tokens)
-    for env in paths:
-        for k in ENV:
-            os.environ.pop(k, None)
-        os.environ.update(env)
-        prof = Profiler(shape, cfg.tokens, with_de=True, with_logits=True)
+    for pol in paths:
+        prof = Profiler(shape, cfg.tokens, with_de=True, with_logits=True, policy=F.make_policy(*pol))
         prof.run(qm, x)
         torch.cuda.synchronize()
-    for k in ENV:
-        os.environ.pop(k, None)
     return masters, prof
 
 
