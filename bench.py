@@ -236,7 +236,7 @@ def kernel_bytes(cfg, T, C, n_chunks_T):
     sc = 4.0 / g if g else 0.0                                  # scale bytes per weight (grouped)
     return {
         "router": L * T * (2 * H + 12 * k),                     # read x, write ids / w / rank
-        "scatter": L * T * 16 * k,                               # read ids + rank, write inv_pos + token_index
+        "permute": L * T * 16 * k,                               # K2: read ids + rank, write inv_pos + token_index
         "combine": L * T * (k * H * 2 + 8 * k + H * 2 * (3 if Fs else 2)),
         "dequant": L * n_w * (per_w_q + sc + 2.0),              # read codes (+ scales), write bf16
         "quantize": L * n_w * (2.0 + per_w_q + sc),             # read bf16 masters, write codes + scales

@@ -322,7 +322,7 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
   CUtensorMap tm_x, tm_wr;
   if (!tmap_bf16(&tm_x, x, T, H, kRouterTile) || !tmap_bf16(&tm_wr, w->router_w, E_r, H, npad)) { set_last_error("router tensor map", cudaErrorInvalidValue); return FLUX_E_CUDA; }
   RouterArgs ra{T, H, E_r, k, c.norm_topk, out->topk_ids, out->topk_w, out->router_logits, out->hist, tile_counts, rank,
-                E, c.n_router > 0 ? w->remap : nullptr};
+                E, c.n_router > 0 ? w->remap : nullptr, (int32_t*)(W + P.counter)};
   {
     KernelTimer kt(K_ROUTER, s);
     if ((e = launch_router(tm_x, tm_wr, npad, ra, s)) != cudaSuccess) { set_last_error("router", e); return FLUX_E_CUDA; }
@@ -352,15 +352,14 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
   sa.sched_sh = sh ? sh_sched : nullptr;
   sa.grp_row0_sh = sh_sched + 2;
   sa.grp_rows_sh = sh_sched + 3;
-  {
-    KernelTimer kt(K_SCHEDULE, s);
-    if ((e = launch_schedule(sa, s)) != cudaSuccess) { set_last_error("schedule", e); return FLUX_E_CUDA; }
+  {  // indices in one kernel; the routed rows are copied to x_perm only when the GEMM does not gather them
+    KernelTimer kt(K_PERMUTE, s);
+    if ((e = launch_permute(sa, out->topk_ids, rank, inv_pos, token_index, s)) != cudaSuccess) { set_last_error("permute", e); return FLUX_E_CUDA; }
   }
-  {
+  if (x_perm) {
     KernelTimer kt(K_SCATTER, s);
-    if (launch_scatter(x, T, H, E, k, out->topk_ids, rank, tile_base, offsets, inv_pos, token_index, x_perm, s) !=
-        cudaSuccess)
-      return FLUX_E_CUDA;
+    if ((e = launch_scatter(x, T, H, E, k, out->topk_ids, rank, tile_base, offsets, inv_pos, token_index, x_perm,
+                            s)) != cudaSuccess) { set_last_error("scatter", e); return FLUX_E_CUDA; }
   }
 
   // ---- (d) K3 + K5: gate/up grouped GEMM with SwiGLU epilogue (routed + shared in one launch)
@@ -393,7 +392,7 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
   ga.gather_idx = gather_a ? token_index : nullptr;
   ga.gather_cp = gmode == GATHER_CP ? 1 : 0;
   ga.l2_hints = pol.l2_hints;
-  ga.tile_ctr = pol.dynamic_tiles ? sa.done_counter + 1 : nullptr;  // zeroed by launch_schedule
+  ga.tile_ctr = pol.dynamic_tiles ? sa.done_counter + 1 : nullptr;  // zeroed by K1
   ga.a_src = x;
   ga.a_ld = H;
   GemmArgs gd = ga;
@@ -575,7 +574,6 @@ flux_status flux_merge_experts_batch(flux_dtype dtype, int32_t n_experts, int64_
   b.E = n_experts;
   b.numel = numel;
   b.compact = compact;
-  b.contiguous = 1;
   for (int j = 0; j < n_jobs; ++j) {
     const flux_merge_job& J = jobs[j];
     if (!J.experts || !J.cluster_of || !J.alpha || !J.out || !aligned16(J.experts) || !aligned16(J.out))

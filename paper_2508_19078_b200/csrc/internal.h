@@ -22,7 +22,7 @@ inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_O
 
 // ---------------------------------------------------------------- per-kernel timing (timing.cpp)
 enum KernelKind {
-  K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_SCHEDULE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
+  K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_PERMUTE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
   K_GEMM_DN_SH_COMBINE, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, K_COSINE, K_ATTN_HIST, FLUX_NUM_KERNELS
 };
 // RAII: counts one launch; when timing is enabled records CUDA events around it on `st`.
@@ -58,7 +58,7 @@ struct MergeJob {           // one weight family of one layer
   int n_slots;              // compact mode: n_tun + n_clusters (0 = unknown, E used as the bound)
 };
 struct MergeBatch {
-  int n_jobs, E, compact, contiguous;
+  int n_jobs, E, compact;
   int64_t numel;
   MergeJob jobs[kMergeMaxJobs];
   int64_t chunk_prefix[kMergeMaxJobs + 1];  // filled by launch_merge_batch
@@ -103,6 +103,7 @@ struct RouterArgs {
   int32_t* rank;        // [T][k] rank of t inside its router tile among tokens choosing the same expert
   int E_slots;           // experts of the weights (hist, tile counts); == E unless re-routing
   const int32_t* remap;  // [E] pick -> slot (NEXT-2 gate re-routing) or null
+  int32_t* zero4;        // 4 ints zeroed by the router (the K2 grid barrier + the pair-GEMM tile counters)
 };
 cudaError_t launch_router(const CUtensorMap& tmap_x, const CUtensorMap& tmap_wr, int npad, const RouterArgs& a,
                           cudaStream_t st);
@@ -116,7 +117,7 @@ struct ScheduleArgs {
   int32_t* tile_base;       // [n_tiles][E]
   int32_t* offsets;         // [E+1] internal
   int32_t* user_offsets;    // [E+1] or null
-  int32_t* done_counter;    // 4 ints zeroed by the launcher: [0] K2 ticket, [1..3] pair-GEMM tile counters
+  int32_t* done_counter;    // 4 ints: [0] K2 ticket / grid barrier, [1..3] pair-GEMM tile counters
   int has_shared;
   int n_tiles_gu, n_tiles_gu_sh;  // n-tiles of the gate/up GEMM (routed, shared)
   int n_tiles_dn, n_tiles_dn_sh;  // n-tiles of the down GEMM
@@ -129,7 +130,10 @@ struct ScheduleArgs {
   int32_t* grp_row0_sh;     // [1] = 0
   int32_t* grp_rows_sh;     // [1] = T
 };
-cudaError_t launch_schedule(const ScheduleArgs& a, cudaStream_t st);
+// K2 as ONE kernel (schedule + index scatter; the counters are zeroed by the router): ids, rank from K1
+// -> tile_base, offsets, GEMM schedules, inv_pos [T][k], token_index [T*k]
+cudaError_t launch_permute(const ScheduleArgs& a, const int32_t* ids, const int32_t* rank, int32_t* inv_pos,
+                           int32_t* token_index, cudaStream_t st);
 cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const int32_t* ids, const int32_t* rank,
                            const int32_t* tile_base, const int32_t* offsets, int32_t* inv_pos, int32_t* token_index,
                            void* x_perm, cudaStream_t st);

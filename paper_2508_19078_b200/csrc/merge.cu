@@ -5,21 +5,17 @@
 // experts first in ascending id, then clusters 0..C-1: exps_config,
 // P:1013-1014).
 //
-// HBM-bound (read Σ|W_e| once, write Σ|W_c| once).  ONE launch covers a batch
-// of jobs (a job = one weight family of one layer: the bench merges all L x 3
-// families of a model in one persistent launch instead of 3L small ones, whose
-// ramp-up / tail cost ~20% of each short launch).  The work is cut into chunks
-// of 4,096 consecutive output elements (256 threads x 2 x 16-byte vectors);
-// every CTA owns a CONTIGUOUS range of chunks (equal counts: balanced), so it
-// rebuilds its member table only when its range crosses into the next output
-// (cluster or job) — a few times per CTA.
+// HBM-bound (read Σ|W_e| once, write Σ|W_c| once).  ONE persistent launch
+// covers a batch of jobs (a job = one weight family of one layer: the bench
+// merges all L x 3 families of a model in one launch instead of 3L small ones).
+// The work is cut into chunks of 8 KB of consecutive output elements, dealt
+// round-robin over one CTA per SM, and streamed with TMA bulk copies through a
+// 6-stage shared-memory ring (192 KB of reads in flight per SM; see the kernel).
 //
 // Per output: the member list (ascending expert id) and fp32 weights
-// w_e = α_e / Σα (Σα accumulated in ascending id: deterministic) live in shared
-// memory.  Threads load up to 4 members' vectors before the first FMA (bytes in
-// flight per SM to cover HBM latency), accumulate w_e·W_e in fp32 (FMA chain in
-// member order) and round once.  A singleton cluster has w = α/α = 1 exactly,
-// so its output is the input bit for bit.
+// w_e = α_e / Σα (Σα accumulated in ascending id: deterministic); the FMA chain
+// runs in member order in fp32 and rounds once.  A singleton cluster has
+// w = α/α = 1 exactly, so its output is the input bit for bit.
 //
 // Out-of-range labels: an expert whose cluster id is < -1 or >= n_clusters
 // belongs to no output; an output with no member is written as zeros.
@@ -32,207 +28,234 @@ namespace flux {
 namespace {
 
 constexpr int kMaxE = 1024;
-constexpr int kThreads = 256;
-constexpr int kVecPerThread = 2;
-constexpr int64_t kChunkVecs = (int64_t)kVecPerThread * kThreads;  // 16-byte vectors per chunk
+// ------------------------------------------------------------------ TMA-bulk pipelined batch kernel
+// Warp 0 (producer, one elected lane) walks this CTA's chunks (dealt round-robin over the grid, so at any
+// moment the CTAs stream neighbouring addresses), and per chunk issues one 1D bulk copy (cp.async.bulk)
+// per member into a ring of kStages stages of 4 member slices each (8 KB per slice); a chunk of a
+// cluster with m members takes ceil(m / 4) stages.  The stage header carries the members' weights and
+// the output address.  Warps 1..8 (consumers) accumulate w_e·W_e in fp32 registers from shared memory
+// (FMA chain in member order, as the per-job kernel), and after the chunk's last stage round once and
+// store 16-byte vectors.  The producer keeps the job's member table (all outputs: members in ascending
+// id, weights α_e / Σα with Σα in ascending id) in shared memory, rebuilt when the job changes.
+constexpr int kSlice = 8192;                  // bytes of one member slice (one chunk of one expert)
+constexpr int kSlicesPerStage = 4;
+constexpr int kStages = 6;                    // 6 x 32 KB = 192 KB of HBM reads in flight per SM
+constexpr int kConsumers = 256;
+constexpr int kBThreads = 32 + kConsumers;
 
-template <bool F32> struct Raw;
-template <> struct Raw<false> { uint4 a; };
-template <> struct Raw<true> { float4 a, b; };
-
-template <bool F32>
-__device__ __forceinline__ void load_raw(const void* base, int64_t elem, Raw<F32>& r) {
-  if constexpr (F32) {
-    const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + elem);
-    r.a = __ldcs(p);
-    r.b = __ldcs(p + 1);
-  } else {
-    r.a = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + elem));
-  }
-}
-
-template <bool F32>
-__device__ __forceinline__ void to_f32(const Raw<F32>& r, float (&f)[8]) {
-  if constexpr (F32) {
-    f[0] = r.a.x; f[1] = r.a.y; f[2] = r.a.z; f[3] = r.a.w;
-    f[4] = r.b.x; f[5] = r.b.y; f[6] = r.b.z; f[7] = r.b.w;
-  } else {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r.a);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 p = __bfloat1622float2(h[i]);
-      f[2 * i] = p.x;
-      f[2 * i + 1] = p.y;
-    }
-  }
-}
-
-template <bool F32>
-__device__ __forceinline__ void store_vec(void* base, int64_t elem, const float (&f)[8]) {
-  if constexpr (F32) {
-    float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + elem);
-    __stcs(p, make_float4(f[0], f[1], f[2], f[3]));
-    __stcs(p + 1, make_float4(f[4], f[5], f[6], f[7]));
-  } else {
-    uint4 o;
-    o.x = pack_bf16x2(f[0], f[1]);
-    o.y = pack_bf16x2(f[2], f[3]);
-    o.z = pack_bf16x2(f[4], f[5]);
-    o.w = pack_bf16x2(f[6], f[7]);
-    __stcs(reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(base) + elem), o);
-  }
-}
-
-struct SmemTable {
-  int lab[kMaxE];    // output index of every expert of the current job (-1: none)
-  int mem[kMaxE];    // members of the current output, ascending expert id
-  float w[kMaxE];    // their weights
-  int n_mem;
-  int n_tun;
+struct StageHdr {
+  float w[kSlicesPerStage];
+  void* out;       // output vector base of this chunk (null when the stage is not the chunk's last)
+  int n;           // member slices in this stage
+  int nvec;        // 16-byte vectors in this chunk
+  int first;       // 1: the chunk's first stage (reset the accumulators)
+  int pad;
 };
 
-// Labels of the experts of job j.  slot(e) = the compact-model slot: tuning experts
-// (cluster_of = -1) take 0..n_tun-1 in ascending id, cluster c takes n_tun + c; an out-of-range id has
-// no slot (-1).  Output index: compact = 1 -> slot(e); compact = 0 -> c for cluster_of = c in [0, C),
-// none (-1) for tuning experts.  remap (if any) = slot(e) in both modes.  Called by all threads.
-__device__ void build_labels(const MergeJob& job, int E, int compact, SmemTable& t) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();  // every thread is done with the previous job's tables
-  if (wid == 0) {
-    int n_tun = 0;
-    for (int e0 = 0; e0 < E; e0 += 32) {
-      const int e = e0 + lane;
-      n_tun += __popc(__ballot_sync(0xffffffffu, e < E && __ldg(&job.cluster_of[e]) == -1));
-    }
-    int rank0 = 0;
-    for (int e0 = 0; e0 < E; e0 += 32) {
-      const int e = e0 + lane;
-      const int cl = e < E ? __ldg(&job.cluster_of[e]) : -2;
-      const unsigned tun = __ballot_sync(0xffffffffu, cl == -1);
-      const bool in_range = cl >= 0 && cl < job.n_clusters;
-      const int slot = cl == -1 ? rank0 + __popc(tun & ((1u << lane) - 1u)) : in_range ? n_tun + cl : -1;
-      if (e < E) {
-        t.lab[e] = compact ? slot : (in_range ? cl : -1);
-        if (job.remap) job.remap[e] = slot;
-      }
-      rank0 += __popc(tun);
-    }
-    if (lane == 0) t.n_tun = n_tun;
-  }
-  __syncthreads();
-}
+struct BatchSmem {
+  uint8_t data[kStages][kSlicesPerStage][kSlice];
+  StageHdr hdr[kStages];
+  uint64_t full[kStages], empty[kStages];
+  int lab[kMaxE];       // output index of every expert of the current job (-1: none)
+  int start[kMaxE + 2]; // output -> first member slot
+  int mem[kMaxE];       // members grouped by output, ascending id
+  float w[kMaxE];
+  int fill[kMaxE + 1];
+};
 
-// Members (ascending id) and weights of output o of the current job.  Called by all threads.
-__device__ void build_members(const MergeJob& job, int E, int o, SmemTable& t) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();  // every thread is done with the previous output's members
-  if (wid == 0) {
-    int n = 0;
-    for (int e0 = 0; e0 < E; e0 += 32) {
-      const int e = e0 + lane;
-      const bool m = e < E && t.lab[e] == o;
-      const unsigned b = __ballot_sync(0xffffffffu, m);
-      if (m) t.mem[n + __popc(b & ((1u << lane) - 1u))] = e;
-      n += __popc(b);
+// Producer-warp helpers (all 32 lanes).
+__device__ int build_job_table(const MergeJob& job, int E, int compact, bool write_remap, BatchSmem& t) {
+  const int lane = threadIdx.x & 31;
+  int n_tun = 0;
+  for (int e0 = 0; e0 < E; e0 += 32) {
+    const int e = e0 + lane;
+    n_tun += __popc(__ballot_sync(0xffffffffu, e < E && __ldg(&job.cluster_of[e]) == -1));
+  }
+  const int n_out = compact ? n_tun + job.n_clusters : job.n_clusters;
+  for (int o = lane; o <= n_out; o += 32) {
+    t.start[o] = 0;
+    t.fill[o] = 0;
+  }
+  __syncwarp();
+  int rank0 = 0;
+  for (int e0 = 0; e0 < E; e0 += 32) {
+    const int e = e0 + lane;
+    const int cl = e < E ? __ldg(&job.cluster_of[e]) : -2;
+    const unsigned tun = __ballot_sync(0xffffffffu, cl == -1);
+    const bool in_range = cl >= 0 && cl < job.n_clusters;
+    const int slot = cl == -1 ? rank0 + __popc(tun & ((1u << lane) - 1u)) : in_range ? n_tun + cl : -1;
+    if (e < E) {
+      const int lab = compact ? slot : (in_range ? cl : -1);
+      t.lab[e] = lab;
+      if (write_remap && job.remap) job.remap[e] = slot;
+      if (lab >= 0) atomicAdd(&t.start[lab + 1], 1);
+    }
+    rank0 += __popc(tun);
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int o = 0; o < n_out; ++o) t.start[o + 1] += t.start[o];
+  __syncwarp();
+  for (int e0 = 0; e0 < E; e0 += 32) {  // members in ascending id within every output
+    const int e = e0 + lane;
+    const int lab = e < E ? t.lab[e] : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, lab);
+    if (lab >= 0) {
+      const int r = __popc(same & ((1u << lane) - 1u));
+      t.mem[t.start[lab] + t.fill[lab] + r] = e;
     }
     __syncwarp();
-    if (lane == 0) {
-      float asum = 0.f;
-      for (int i = 0; i < n; ++i) asum += __ldg(&job.alpha[t.mem[i]]);  // ascending id
-      for (int i = 0; i < n; ++i)
-        t.w[i] = asum > 0.f ? __fdiv_rn(__ldg(&job.alpha[t.mem[i]]), asum) : __fdiv_rn(1.f, (float)n);
-      t.n_mem = n;
+    if (lab >= 0 && __ffs(same) - 1 == lane) t.fill[lab] += __popc(same);
+    __syncwarp();
+  }
+  for (int o = lane; o < n_out; o += 32) {  // Σα in ascending id, then α_e / Σα (or 1/|E_c|)
+    const int b = t.start[o], n = t.start[o + 1] - b;
+    float asum = 0.f;
+    for (int i = 0; i < n; ++i) asum += __ldg(&job.alpha[t.mem[b + i]]);
+    for (int i = 0; i < n; ++i)
+      t.w[b + i] = asum > 0.f ? __fdiv_rn(__ldg(&job.alpha[t.mem[b + i]]), asum) : __fdiv_rn(1.f, (float)n);
+  }
+  __syncwarp();
+  return n_out;
+}
+
+template <bool F32>
+__global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_constant__ MergeBatch b) {
+  extern __shared__ uint8_t smem_raw[];
+  BatchSmem& t = *reinterpret_cast<BatchSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  constexpr int kEsz = F32 ? 4 : 2;
+  constexpr int kChunkElems = kSlice / kEsz;
+  const int64_t cpo = (b.numel + kChunkElems - 1) / kChunkElems;  // chunks per output
+  const int64_t total = b.chunk_prefix[b.n_jobs];
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&t.full[s], 1);
+      mbar_init(&t.empty[s], kConsumers / 32);
     }
+    fence_barrier_init();
   }
   __syncthreads();
-}
-
-template <bool F32>
-__device__ __forceinline__ void merge_chunk(const MergeJob& job, int64_t numel, int o, int64_t v0,
-                                            const SmemTable& t) {
-  const int64_t nvec = numel / 8;
-  float acc[kVecPerThread][8];
-#pragma unroll
-  for (int u = 0; u < kVecPerThread; ++u)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
-  const int m_end = t.n_mem;
-  for (int m0 = 0; m0 < m_end; m0 += 4) {
-    Raw<F32> r[4][kVecPerThread];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (m0 + j < m_end) {
-        const int64_t base = (int64_t)t.mem[m0 + j] * numel;
-#pragma unroll
-        for (int u = 0; u < kVecPerThread; ++u) {
-          const int64_t v = v0 + (int64_t)u * kThreads;
-          if (v < nvec) load_raw<F32>(job.experts, base + v * 8, r[j][u]);
-        }
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer
+    const uint64_t pol = policy_evict_first();
+    int j = 0, cur_job = -1, n_out = 0, g = 0;
+    for (int64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
+      while (ch >= b.chunk_prefix[j + 1]) ++j;
+      const int64_t local = ch - b.chunk_prefix[j];
+      const int o = (int)(local / cpo);
+      const int64_t c_in = local - (int64_t)o * cpo;
+      const MergeJob& job = b.jobs[j];
+      if (j != cur_job) {
+        n_out = build_job_table(job, b.E, b.compact, b.chunk_prefix[j] % gridDim.x == blockIdx.x, t);
+        cur_job = j;
       }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (m0 + j < m_end) {
-        const float wm = t.w[m0 + j];
-#pragma unroll
-        for (int u = 0; u < kVecPerThread; ++u) {
-          float f[8];
-          to_f32<F32>(r[j][u], f);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[u][i] = fmaf(wm, f[i], acc[u][i]);
+      if (o >= n_out) continue;  // compact single-job calls: the slot count was an upper bound
+      const int64_t e0 = c_in * kChunkElems;
+      const int n_elems = (int)(b.numel - e0 < kChunkElems ? b.numel - e0 : kChunkElems);
+      const uint32_t bytes = (uint32_t)n_elems * kEsz;
+      const int m0 = t.start[o], m1 = t.start[o + 1];
+      int m = m0;
+      do {  // one stage per group of up to 4 members (an output with no member still takes one stage)
+        const int s = g % kStages;
+        mbar_wait(&t.empty[s], ((g / kStages) & 1) ^ 1);
+        const int n = min(kSlicesPerStage, m1 - m);
+        if ((threadIdx.x & 31) == 0) {
+          StageHdr& h = t.hdr[s];
+          for (int i = 0; i < kSlicesPerStage; ++i) h.w[i] = i < n ? t.w[m + i] : 0.f;
+          h.n = n;
+          h.nvec = (int)(bytes / 16);
+          h.first = m == m0;
+          h.out = m + n >= m1 ? (void*)((uint8_t*)job.merged + ((int64_t)o * b.numel + e0) * kEsz) : nullptr;
+          mbar_arrive_expect_tx(&t.full[s], (uint32_t)n * bytes);
+          for (int i = 0; i < n; ++i)
+            bulk_load_1d(t.data[s][i], (const uint8_t*)job.experts + ((int64_t)t.mem[m + i] * b.numel + e0) * kEsz,
+                         bytes, &t.full[s], pol);
         }
-      }
-  }
-#pragma unroll
-  for (int u = 0; u < kVecPerThread; ++u) {
-    const int64_t v = v0 + (int64_t)u * kThreads;
-    if (v < nvec) store_vec<F32>(job.merged, (int64_t)o * numel + v * 8, acc[u]);
-  }
-}
-
-// chunk_prefix[j] = first chunk of job j (chunks of job j = n_out_j · chunks per output).
-// contiguous = 1: CTA b owns chunks [b·n/G, (b+1)·n/G); 0: chunks dealt round-robin (single-job calls
-// whose output count is only an upper bound, compact mode).
-template <bool F32>
-__global__ void __launch_bounds__(kThreads) merge_batch_kernel(MergeBatch b) {
-  __shared__ SmemTable t;
-  const int64_t nvec = b.numel / 8;
-  const int64_t cpo = (nvec + kChunkVecs - 1) / kChunkVecs;  // chunks per output
-  const int64_t total = b.chunk_prefix[b.n_jobs];
-  int64_t ch0, ch1, step;
-  if (b.contiguous) {
-    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
-    ch0 = (int64_t)blockIdx.x * per;
-    ch1 = min(total, ch0 + per);
-    step = 1;
+        __syncwarp();
+        m += n;
+        ++g;
+      } while (m < m1);
+    }
+    // end marker: one stage with n = -1
+    const int s = g % kStages;
+    mbar_wait(&t.empty[s], ((g / kStages) & 1) ^ 1);
+    if ((threadIdx.x & 31) == 0) {
+      t.hdr[s].n = -1;
+      mbar_arrive(&t.full[s]);
+    }
+    __syncwarp();
   } else {
-    ch0 = blockIdx.x;
-    ch1 = total;
-    step = gridDim.x;
-  }
-  int j = 0, cur_job = -1, cur_o = -1;
-  for (int64_t ch = ch0; ch < ch1; ch += step) {
-    while (ch >= b.chunk_prefix[j + 1]) ++j;
-    const int64_t local = ch - b.chunk_prefix[j];
-    const int o = (int)(local / cpo);
-    const int64_t v0 = (local - (int64_t)o * cpo) * kChunkVecs + threadIdx.x;
-    if (j != cur_job) {
-      build_labels(b.jobs[j], b.E, b.compact, t);
-      cur_job = j;
-      cur_o = -1;
+    // ---------------------------------------------------------------- consumers
+    const int tid = threadIdx.x - 32;
+    constexpr int kPerVec = 16 / kEsz;  // elements per 16-byte vector
+    float acc[2][kPerVec];
+    int g = 0;
+    for (;; ++g) {
+      const int s = g % kStages;
+      // the producer signals the end with a stage whose n is -1 (below)
+      mbar_wait(&t.full[s], (g / kStages) & 1);
+      const StageHdr h = t.hdr[s];
+      if (h.n < 0) break;
+      if (h.first) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int i = 0; i < kPerVec; ++i) acc[u][i] = 0.f;
+      }
+      for (int mi = 0; mi < h.n; ++mi) {
+        const float wm = h.w[mi];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int v = tid + u * kConsumers;
+          if (v < h.nvec) {
+            const uint4 r = *reinterpret_cast<const uint4*>(t.data[s][mi] + v * 16);
+            if constexpr (F32) {
+              const float* f = reinterpret_cast<const float*>(&r);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[u][i] = fmaf(wm, f[i], acc[u][i]);
+            } else {
+              const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 p = __bfloat1622float2(hh[i]);
+                acc[u][2 * i] = fmaf(wm, p.x, acc[u][2 * i]);
+                acc[u][2 * i + 1] = fmaf(wm, p.y, acc[u][2 * i + 1]);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&t.empty[s]);
+      if (h.out) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int v = tid + u * kConsumers;
+          if (v < h.nvec) {
+            uint4 o;
+            if constexpr (F32) {
+              o = make_uint4(__float_as_uint(acc[u][0]), __float_as_uint(acc[u][1]), __float_as_uint(acc[u][2]),
+                             __float_as_uint(acc[u][3]));
+            } else {
+              o.x = pack_bf16x2(acc[u][0], acc[u][1]);
+              o.y = pack_bf16x2(acc[u][2], acc[u][3]);
+              o.z = pack_bf16x2(acc[u][4], acc[u][5]);
+              o.w = pack_bf16x2(acc[u][6], acc[u][7]);
+            }
+            __stcs(reinterpret_cast<uint4*>(h.out) + v, o);
+          }
+        }
+      }
     }
-    if (b.compact && o >= t.n_tun + b.jobs[j].n_clusters) continue;  // beyond the job's slots (upper bound)
-    if (o != cur_o) {
-      build_members(b.jobs[j], b.E, o, t);
-      cur_o = o;
-    }
-    merge_chunk<F32>(b.jobs[j], b.numel, o, v0, t);
   }
 }
 }  // namespace
 
 cudaError_t launch_merge_batch(bool fp32, const MergeBatch& b0, cudaStream_t st) {
   MergeBatch b = b0;
-  const int64_t cpo = (b.numel / 8 + kChunkVecs - 1) / kChunkVecs;
+  const int64_t chunk = kSlice / (fp32 ? 4 : 2);
+  const int64_t cpo = (b.numel + chunk - 1) / chunk;
   b.chunk_prefix[0] = 0;
   for (int j = 0; j < b.n_jobs; ++j) {
     const int64_t n_out = b.compact ? (b.jobs[j].n_slots > 0 ? b.jobs[j].n_slots : b.E) : b.jobs[j].n_clusters;
@@ -240,13 +263,17 @@ cudaError_t launch_merge_batch(bool fp32, const MergeBatch& b0, cudaStream_t st)
   }
   const int64_t total = b.chunk_prefix[b.n_jobs];
   if (total == 0) return cudaSuccess;
-  // one resident wave: 3 (bf16) / 2 (fp32) CTAs per SM
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)kNumSMs * (fp32 ? 2 : 3)));
-  if (fp32)
-    merge_batch_kernel<true><<<grid, kThreads, 0, st>>>(b);
-  else
-    merge_batch_kernel<false><<<grid, kThreads, 0, st>>>(b);
-  return cudaGetLastError();
+  const int smem = (int)sizeof(BatchSmem) + 128;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)kNumSMs));
+  cudaError_t e;
+  if (fp32) {
+    e = cudaFuncSetAttribute(merge_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) merge_tma_kernel<true><<<grid, kBThreads, smem, st>>>(b);
+  } else {
+    e = cudaFuncSetAttribute(merge_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) merge_tma_kernel<false><<<grid, kBThreads, smem, st>>>(b);
+  }
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, const int32_t* cluster_of,
@@ -256,7 +283,6 @@ cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, c
   b.E = E;
   b.numel = numel;
   b.compact = compact;
-  b.contiguous = compact ? 0 : 1;  // compact: the slot count (n_tun + C) is known only on the device
   b.jobs[0] = MergeJob{experts, cluster_of, alpha, merged, remap, C, 0};
   return launch_merge_batch(fp32, b, st);
 }

@@ -1,18 +1,17 @@
 // permute.cu — K2: D_e (the tokens routed to each expert) as a
 // deterministic, stable permutation, plus the grouped-GEMM tile schedule.
 //
-//  schedule_kernel  (one CTA per expert): exclusive scan over the router's
-//                   per-tile counts -> tile_base[tile][e]; the last CTA to
-//                   finish (atomic ticket) scans the per-expert totals ->
-//                   offsets[e] and builds the tile prefix of both grouped GEMMs.
-//  scatter_pick_kernel (one thread per pick (t, j); the default, when the
-//                   gate/up GEMM gathers its A rows from x itself):
+//  permute_kernel   ONE cooperative launch: per-expert exclusive scans over the
+//                   router's per-tile counts -> tile_base[tile][e]; a grid
+//                   barrier; every CTA scans the per-expert totals -> offsets
+//                   (CTA 0 publishes them with the tile prefix of both grouped
+//                   GEMMs); then one thread per pick (t, j):
 //                   pos = offsets[e] + tile_base[tile][e] + rank (rank from K1)
 //                   -> token_index[pos] = t (ascending t inside every segment:
-//                   reading R3), inv_pos[t][j] = pos.  k·12 bytes per token.
+//                   reading R3), inv_pos[t][j] = pos.  k·16 bytes per token.
 //  scatter_kernel   (one warp per token; only when x_perm is materialised): the
-//                   same indices plus the gather x[t] -> x_perm[pos] (16-byte
-//                   vectors, x read once, written k times).
+//                   gather x[t] -> x_perm[pos] (16-byte vectors, x read once,
+//                   written k times), rewriting the same indices.
 // No atomics decide positions, so D_e is bitwise reproducible.
 #include <algorithm>
 
@@ -49,74 +48,6 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* sh, int& total) 
   total = sh[7];
   __syncthreads();
   return warp_prefix + x - v;
-}
-
-__global__ void __launch_bounds__(256) schedule_kernel(ScheduleArgs a) {
-  __shared__ int sh[8];
-  __shared__ int is_last;
-  const int e = blockIdx.x;
-  // ---- per-expert scan over router tiles (chunks of 256 tiles)
-  int carry = 0;
-  for (int base = 0; base < a.n_tiles; base += 256) {
-    const int tile = base + threadIdx.x;
-    const int v = tile < a.n_tiles ? a.tile_counts[(int64_t)tile * a.E + e] : 0;
-    int tot;
-    const int ex = block_exclusive_scan(v, sh, tot);
-    if (tile < a.n_tiles) a.tile_base[(int64_t)tile * a.E + e] = carry + ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) {
-    a.offsets[e + 1] = carry;  // temporarily the count of expert e
-    __threadfence();
-    const int ticket = atomicAdd(a.done_counter, 1);
-    is_last = ticket == a.E - 1;
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  // ---- last CTA: offsets (exclusive scan of counts) and GEMM tile schedules
-  const int n_groups = a.E + (a.has_shared ? 1 : 0);
-  int carry_rows = 0, carry_gu = 0, carry_dn = 0;
-  for (int base = 0; base < n_groups; base += 256) {
-    const int g = base + threadIdx.x;
-    int rows = 0, row0 = 0;
-    if (g < a.E) rows = __ldcg(&a.offsets[g + 1]);
-    else if (g < n_groups) rows = (int)a.T;
-    int tot_rows;
-    const int ex_rows = block_exclusive_scan(g < a.E ? rows : 0, sh, tot_rows);
-    row0 = g < a.E ? carry_rows + ex_rows : 0;
-    const int mt = (rows + a.gemm_bm - 1) / a.gemm_bm;
-    const int ngu = mt * (g < a.E ? a.n_tiles_gu : a.n_tiles_gu_sh);
-    const int ndn = mt * (g < a.E ? a.n_tiles_dn : a.n_tiles_dn_sh);
-    int tot_gu, tot_dn;
-    const int ex_gu = block_exclusive_scan(g < n_groups ? ngu : 0, sh, tot_gu);
-    const int ex_dn = block_exclusive_scan(g < n_groups ? ndn : 0, sh, tot_dn);
-    if (g < n_groups) {
-      a.grp_row0[g] = row0;
-      a.grp_rows[g] = rows;
-      a.sched_gu[g] = carry_gu + ex_gu;
-      a.sched_dn[g] = carry_dn + ex_dn;
-    }
-    carry_rows += tot_rows;
-    carry_gu += tot_gu;
-    carry_dn += tot_dn;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    a.sched_gu[n_groups] = carry_gu;
-    a.sched_dn[n_groups] = carry_dn;
-    if (a.sched_sh) {  // the shared MLP alone (down GEMM with the fused combine epilogue)
-      a.sched_sh[0] = 0;
-      a.sched_sh[1] = (int)((a.T + a.gemm_bm - 1) / a.gemm_bm) * a.n_tiles_dn_sh;
-      a.grp_row0_sh[0] = 0;
-      a.grp_rows_sh[0] = (int)a.T;
-    }
-  }
-  for (int g = threadIdx.x; g <= a.E; g += 256) {
-    const int off = g < a.E ? a.grp_row0[g] : carry_rows;
-    a.offsets[g] = off;
-    if (a.user_offsets) a.user_offsets[g] = off;
-  }
 }
 
 __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ x, int64_t T, int H, int E, int k,
@@ -163,21 +94,99 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
     }
   }
 }
-// One thread per pick: coalesced reads of ids / rank, coalesced inv_pos writes; token_index writes
-// land in the expert segments (consecutive tokens of one expert are adjacent).  The per-tile bases
-// (n_tiles x E int32, <= 1 MB) stay in L2.
-__global__ void __launch_bounds__(256) scatter_pick_kernel(int64_t Tk, int E, int k, const int32_t* __restrict__ ids,
-                                                           const int32_t* __restrict__ rank,
-                                                           const int32_t* __restrict__ tile_base,
-                                                           const int32_t* __restrict__ offsets,
-                                                           int32_t* __restrict__ inv_pos,
-                                                           int32_t* __restrict__ token_index) {
+// K2 in one launch.  Phase 1: CTA e (strided) scans expert e's per-tile counts -> tile_base[tile][e]
+// and grp_rows[e] = its row count.  Grid barrier (counter zeroed by K1; the launch is cooperative, so
+// every CTA is resident).  Phase 2: every CTA scans the E counts into its own shared offsets table; CTA 0
+// also publishes offsets, the user's D_e bounds and both GEMM tile schedules.  Phase 3: one thread per
+// pick (t, j): pos = offsets[e] + tile_base[tile][e] + rank -> token_index[pos] = t, inv_pos = pos.
+constexpr int kMaxE2 = 1024;
+__global__ void __launch_bounds__(256) permute_kernel(ScheduleArgs a, const int32_t* __restrict__ ids,
+                                                      const int32_t* __restrict__ rank, int32_t* __restrict__ inv_pos,
+                                                      int32_t* __restrict__ token_index) {
+  __shared__ int sh[8];
+  __shared__ int s_off[kMaxE2 + 1];
+  const int E = a.E;
+  // ---- phase 1: per-expert scans
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    int carry = 0;
+    for (int base = 0; base < a.n_tiles; base += 256) {
+      const int tile = base + threadIdx.x;
+      const int v = tile < a.n_tiles ? __ldcg(&a.tile_counts[(int64_t)tile * E + e]) : 0;
+      int tot;
+      const int ex = block_exclusive_scan(v, sh, tot);
+      if (tile < a.n_tiles) a.tile_base[(int64_t)tile * E + e] = carry + ex;
+      carry += tot;
+    }
+    if (threadIdx.x == 0) a.grp_rows[e] = carry;
+  }
+  // ---- grid barrier
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(a.done_counter, 1);
+    int seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(a.done_counter) : "memory");
+    } while (seen < (int)gridDim.x);
+  }
+  __syncthreads();
+  // ---- phase 2: offsets (every CTA, in shared memory); CTA 0 publishes offsets + GEMM schedules
+  const int n_groups = E + (a.has_shared ? 1 : 0);
+  int carry_rows = 0, carry_gu = 0, carry_dn = 0;
+  for (int base = 0; base < n_groups; base += 256) {
+    const int g = base + threadIdx.x;
+    int rows = 0;
+    if (g < E) rows = __ldcg(&a.grp_rows[g]);
+    else if (g < n_groups) rows = (int)a.T;
+    int tot_rows;
+    const int ex_rows = block_exclusive_scan(g < E ? rows : 0, sh, tot_rows);
+    const int row0 = g < E ? carry_rows + ex_rows : 0;
+    if (g < E) s_off[g] = row0;
+    if (blockIdx.x == 0) {
+      const int mt = (rows + a.gemm_bm - 1) / a.gemm_bm;
+      const int ngu = mt * (g < E ? a.n_tiles_gu : a.n_tiles_gu_sh);
+      const int ndn = mt * (g < E ? a.n_tiles_dn : a.n_tiles_dn_sh);
+      int tot_gu, tot_dn;
+      const int ex_gu = block_exclusive_scan(g < n_groups ? ngu : 0, sh, tot_gu);
+      const int ex_dn = block_exclusive_scan(g < n_groups ? ndn : 0, sh, tot_dn);
+      if (g < n_groups) {
+        a.grp_row0[g] = row0;
+        if (g >= E) a.grp_rows[g] = rows;
+        a.sched_gu[g] = carry_gu + ex_gu;
+        a.sched_dn[g] = carry_dn + ex_dn;
+      }
+      carry_gu += tot_gu;
+      carry_dn += tot_dn;
+    }
+    carry_rows += tot_rows;
+  }
+  if (threadIdx.x == 0) s_off[E] = carry_rows;
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      a.sched_gu[n_groups] = carry_gu;
+      a.sched_dn[n_groups] = carry_dn;
+      if (a.sched_sh) {  // the shared MLP alone (down GEMM with the fused combine epilogue)
+        a.sched_sh[0] = 0;
+        a.sched_sh[1] = (int)((a.T + a.gemm_bm - 1) / a.gemm_bm) * a.n_tiles_dn_sh;
+        a.grp_row0_sh[0] = 0;
+        a.grp_rows_sh[0] = (int)a.T;
+      }
+    }
+    for (int g = threadIdx.x; g <= E; g += 256) {
+      a.offsets[g] = s_off[g];
+      if (a.user_offsets) a.user_offsets[g] = s_off[g];
+    }
+  }
+  // ---- phase 3: one thread per pick
+  const int64_t Tk = a.T * a.k;
+  const int k = a.k;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Tk; i += (int64_t)gridDim.x * blockDim.x) {
     const int e = __ldcs(&ids[i]);
     const int64_t t = i / k;
     int p = -1;
     if (e >= 0) {  // -1: a pick folded by gate re-routing (NEXT-2) owns no row
-      p = __ldg(&offsets[e]) + __ldg(&tile_base[(t / kRouterTile) * E + e]) + __ldcs(&rank[i]);
+      p = s_off[e] + __ldcg(&a.tile_base[(t / kRouterTile) * E + e]) + __ldcs(&rank[i]);
       token_index[p] = (int32_t)t;
     }
     inv_pos[i] = p;
@@ -185,23 +194,27 @@ __global__ void __launch_bounds__(256) scatter_pick_kernel(int64_t Tk, int E, in
 }
 }  // namespace
 
-cudaError_t launch_schedule(const ScheduleArgs& a, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(a.done_counter, 0, 4 * sizeof(int32_t), st);  // + the GEMM tile counters
-  if (e != cudaSuccess) return e;
-  schedule_kernel<<<a.E, 256, 0, st>>>(a);
-  return cudaGetLastError();
+cudaError_t launch_permute(const ScheduleArgs& a0, const int32_t* ids, const int32_t* rank, int32_t* inv_pos,
+                           int32_t* token_index, cudaStream_t st) {
+  if (a0.E > kMaxE2) return cudaErrorInvalidValue;
+  static int max_blocks = -1;  // co-resident CTAs per SM (cooperative launch bound)
+  if (max_blocks < 0) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, permute_kernel, 256, 0) != cudaSuccess) return cudaErrorUnknown;
+    max_blocks = n;
+  }
+  const int64_t Tk = a0.T * a0.k;
+  const int64_t want = std::max<int64_t>((int64_t)a0.E, (Tk + 255) / 256);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * std::min(max_blocks, 4)));
+  ScheduleArgs a = a0;
+  void* args[] = {&a, &ids, &rank, &inv_pos, &token_index};
+  return cudaLaunchCooperativeKernel((const void*)permute_kernel, dim3(grid), dim3(256), args, 0, st);
 }
 
 cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const int32_t* ids, const int32_t* rank,
                            const int32_t* tile_base, const int32_t* offsets, int32_t* inv_pos, int32_t* token_index,
                            void* x_perm, cudaStream_t st) {
-  if (T == 0) return cudaSuccess;
-  if (!x_perm) {  // indices only
-    const int64_t Tk = T * k;
-    const unsigned grid = (unsigned)std::min<int64_t>((Tk + 255) / 256, (int64_t)kNumSMs * 8);
-    scatter_pick_kernel<<<grid, 256, 0, st>>>(Tk, E, k, ids, rank, tile_base, offsets, inv_pos, token_index);
-    return cudaGetLastError();
-  }
+  if (T == 0 || !x_perm) return cudaSuccess;
   const unsigned grid = (unsigned)((T + 7) / 8);
   scatter_kernel<<<grid, 256, 0, st>>>((const uint4*)x, T, H, E, k, ids, rank, tile_base, offsets, inv_pos,
                                        token_index, (uint4*)x_perm);

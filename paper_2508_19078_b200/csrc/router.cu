@@ -13,10 +13,12 @@
 // K=16) into a TMEM accumulator, and 4 epilogue warps read one token row each
 // with tcgen05.ld.  The epilogue keeps the row in registers: max, softmax
 // denominator, k argmax passes, weights.  The histogram is CTA-aggregated:
-// each token sets its bit in a per-expert 128-bit mask in shared memory; one
-// popcount per expert gives this tile's count (one global atomic per expert
-// per CTA) and the stable within-tile rank of every (token, expert) pair that
-// the permutation (K2) needs.  NEXT-2 gate re-routing (§7, R14): with a remap table
+// every epilogue warp builds, with one ballot per expert, the 32-bit mask of
+// its 32 tokens that picked that expert (a 256-bit mask per expert per tile in
+// shared memory, each word written by exactly one warp: no shared atomics);
+// popcounts give this tile's count (one global atomic per expert per CTA) and
+// the stable within-tile rank of every (token, expert) pair that the
+// permutation (K2) needs.  NEXT-2 gate re-routing (§7, R14): with a remap table
 // the picks are sent to the compact model's slots in the same epilogue, repeated slots folded.
 #include <algorithm>
 
@@ -56,7 +58,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = empty + kStages;  // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  uint32_t* masks = reinterpret_cast<uint32_t*>(smem + kStages * S::kStage + 256);  // [NPAD][8]
+  uint32_t* masks = reinterpret_cast<uint32_t*>(smem + kStages * S::kStage + 256);  // [8 row groups][NPAD]
 
   // two buffers x two 128-row halves x NPAD columns
   constexpr uint32_t kTmemCols = NPAD <= 16 ? 64 : (NPAD <= 32 ? 128 : (NPAD <= 64 ? 256 : 512));
@@ -80,6 +82,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (a.zero4 && blockIdx.x == 0 && threadIdx.x < 4) a.zero4[threadIdx.x] = 0;  // for K2 and the GEMMs
 
   if (warp == 0) {
     if (elect_one()) {
@@ -137,9 +140,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = i & 1;
       const int64_t t = (int64_t)tile * kBM + row;
       const bool valid = t < a.T;
-      named_bar_sync(1, 32 * kEpiWarps);  // the previous tile's mask readers are done
-      for (int m = et; m < NPAD * 8; m += 32 * kEpiWarps) masks[m] = 0;
-
       mbar_wait(&acc_full[b], (i >> 1) & 1);
       tc_fence_after();
       float z[NPAD];
@@ -219,12 +219,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
 
-      named_bar_sync(1, 32 * kEpiWarps);  // masks zeroed
-      if (valid) {
+      // per-expert token masks of this warp's 32 rows: one ballot per expert column (no shared-memory
+      // atomics: every mask word has exactly one writer), masks[wr][e] with wr = row >> 5
+      uint32_t pk[(NPAD + 31) / 32];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < k && ids[j] >= 0) atomicOr(&masks[ids[j] * 8 + (row >> 5)], 1u << (row & 31));
+      for (int w = 0; w < (NPAD + 31) / 32; ++w) pk[w] = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (valid && j < k && ids[j] >= 0) {
+#pragma unroll
+          for (int w = 0; w < (NPAD + 31) / 32; ++w)
+            if ((ids[j] >> 5) == w) pk[w] |= 1u << (ids[j] & 31);
+        }
+      uint32_t word[(NPAD + 31) / 32] = {};
+#pragma unroll
+      for (int e = 0; e < NPAD; ++e) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (pk[e >> 5] >> (e & 31)) & 1u);
+        if ((e & 31) == lane_id()) word[e >> 5] = bal;
       }
+      named_bar_sync(1, 32 * kEpiWarps);  // the previous tile's mask readers are done
+#pragma unroll
+      for (int w = 0; w < (NPAD + 31) / 32; ++w)
+        if (w * 32 + lane_id() < NPAD) masks[(row >> 5) * NPAD + w * 32 + lane_id()] = word[w];
       named_bar_sync(1, 32 * kEpiWarps);
 
       if (valid) {
@@ -237,9 +253,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (j >= k) continue;
           int r = 0;
           if (ids[j] >= 0) {
-            const uint32_t* m = &masks[ids[j] * 8];
-            r = __popc(m[row >> 5] & below);
-            for (int wd = 0; wd < (row >> 5); ++wd) r += __popc(m[wd]);
+            const uint32_t* m = &masks[ids[j]];
+            r = __popc(m[(row >> 5) * NPAD] & below);
+            for (int wd = 0; wd < (row >> 5); ++wd) r += __popc(m[wd * NPAD]);
           }
           gid[j] = ids[j];
           gw[j] = wt[j];
@@ -253,10 +269,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (et < a.E_slots) {
-        const uint32_t* m = &masks[et * 8];
+        const uint32_t* m = &masks[et];
         int cnt = 0;
 #pragma unroll
-        for (int wd = 0; wd < 8; ++wd) cnt += __popc(m[wd]);
+        for (int wd = 0; wd < 8; ++wd) cnt += __popc(m[wd * NPAD]);
         a.tile_counts[(int64_t)tile * a.E_slots + et] = cnt;
         if (cnt) atomicAdd(reinterpret_cast<unsigned long long*>(a.hist + et), (unsigned long long)cnt);
       }

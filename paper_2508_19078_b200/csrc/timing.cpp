@@ -12,7 +12,7 @@
 
 namespace flux {
 static const char* kernel_name(int kind) {
-  static const char* names[FLUX_NUM_KERNELS] = {"quantize", "dequant", "router", "schedule", "scatter",
+  static const char* names[FLUX_NUM_KERNELS] = {"quantize", "dequant", "router", "permute", "scatter",
                                                 "gemm_gate_up", "gemm_down", "combine", "merge",
                                                 "gemm_down_shared_combine", "gram", "gram_reduce", "eig",
                                                 "kmeans", "cosine_distance", "attention_hist"};
