@@ -536,7 +536,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=0, help="tokens per flux_profile_layer call (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-tokens", type=int, default=128)  # oracle sample (~20-30 s of host CPU work)
-    ap.add_argument("--ref-layers", type=int, default=1)
+    ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--clusters", type=int, default=0)
     ap.add_argument("--budget", default="uniform", choices=["uniform", "adaptive"],
                     help="uniform: C clusters in every layer (BASELINE configs[3]); adaptive: eq.(1) B(l)")

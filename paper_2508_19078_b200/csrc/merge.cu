@@ -29,31 +29,32 @@ namespace {
 
 constexpr int kMaxE = 1024;
 // ------------------------------------------------------------------ TMA-bulk pipelined batch kernel
-// Warp 0 (producer, one elected lane) walks this CTA's chunks (dealt round-robin over the grid, so at any
-// moment the CTAs stream neighbouring addresses), and per chunk issues one 1D bulk copy (cp.async.bulk)
-// per member into a ring of kStages stages of 4 member slices each (8 KB per slice); a chunk of a
-// cluster with m members takes ceil(m / 4) stages.  The stage header carries the members' weights and
-// the output address.  Warps 1..8 (consumers) accumulate w_e·W_e in fp32 registers from shared memory
-// (FMA chain in member order, as the per-job kernel), and after the chunk's last stage round once and
-// store 16-byte vectors.  The producer keeps the job's member table (all outputs: members in ascending
-// id, weights α_e / Σα with Σα in ascending id) in shared memory, rebuilt when the job changes.
+// Warp 0 (producer, one elected lane) walks this CTA's chunks (dealt round-robin over one CTA per SM, so
+// at any moment the CTAs stream neighbouring addresses) and per chunk issues one 1D bulk copy
+// (cp.async.bulk, evict_first) per member into a ring of kStages stages of up to 4 member slices (8 KB
+// each); a chunk of a cluster with m members takes ceil(m / 4) stages.  The stage header carries the
+// members' weights, whether the stage starts the chunk, and (on its last stage) the output address.
+// Warps 1..16 (consumers, one 16-byte vector of the chunk per thread) accumulate w_e·W_e in fp32
+// (packed FFMA2, bit-identical per lane to fmaf; member order), and after the chunk's last stage round
+// once and store.  The producer keeps the job's member table (every output: members in ascending id,
+// weights α_e / Σα with Σα in ascending id) in shared memory, rebuilt per job.
 constexpr int kSlice = 8192;                  // bytes of one member slice (one chunk of one expert)
-constexpr int kSlicesPerStage = 4;
+constexpr int kPerStage = 4;                  // member slices per stage
 constexpr int kStages = 6;                    // 6 x 32 KB = 192 KB of HBM reads in flight per SM
-constexpr int kConsumers = 256;
+constexpr int kConsumers = kSlice / 16;       // one 16-byte vector per consumer thread
 constexpr int kBThreads = 32 + kConsumers;
 
 struct StageHdr {
-  float w[kSlicesPerStage];
-  void* out;       // output vector base of this chunk (null when the stage is not the chunk's last)
-  int n;           // member slices in this stage
+  float w[kPerStage];
+  void* out;       // output vectors of this chunk when the stage holds its last members, else null
+  int n;           // member slices in this stage (0: an output without members -> zeros; -1: end)
   int nvec;        // 16-byte vectors in this chunk
-  int first;       // 1: the chunk's first stage (reset the accumulators)
+  int first;       // the chunk's first stage: reset the accumulators
   int pad;
 };
 
 struct BatchSmem {
-  uint8_t data[kStages][kSlicesPerStage][kSlice];
+  uint8_t data[kStages][kPerStage][kSlice];
   StageHdr hdr[kStages];
   uint64_t full[kStages], empty[kStages];
   int lab[kMaxE];       // output index of every expert of the current job (-1: none)
@@ -63,7 +64,7 @@ struct BatchSmem {
   int fill[kMaxE + 1];
 };
 
-// Producer-warp helpers (all 32 lanes).
+// Producer-warp helper (all 32 lanes): the job's member table; returns its output count.
 __device__ int build_job_table(const MergeJob& job, int E, int compact, bool write_remap, BatchSmem& t) {
   const int lane = threadIdx.x & 31;
   int n_tun = 0;
@@ -100,10 +101,7 @@ __device__ int build_job_table(const MergeJob& job, int E, int compact, bool wri
     const int e = e0 + lane;
     const int lab = e < E ? t.lab[e] : -1;
     const unsigned same = __match_any_sync(0xffffffffu, lab);
-    if (lab >= 0) {
-      const int r = __popc(same & ((1u << lane) - 1u));
-      t.mem[t.start[lab] + t.fill[lab] + r] = e;
-    }
+    if (lab >= 0) t.mem[t.start[lab] + t.fill[lab] + __popc(same & ((1u << lane) - 1u))] = e;
     __syncwarp();
     if (lab >= 0 && __ffs(same) - 1 == lane) t.fill[lab] += __popc(same);
     __syncwarp();
@@ -139,34 +137,49 @@ __global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_co
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
     const uint64_t pol = policy_evict_first();
-    int j = 0, cur_job = -1, n_out = 0, g = 0;
+    const bool leader = (threadIdx.x & 31) == 0;
+    int j = -1, n_out = 0, g = 0;
+    int64_t local = 0, c_in = 0;  // chunk index inside job j, inside output o
+    int o = 0;
+    auto next_stage = [&]() {
+      const int s = g % kStages;
+      mbar_wait(&t.empty[s], ((g / kStages) & 1) ^ 1);
+      ++g;
+      return s;
+    };
     for (int64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
-      while (ch >= b.chunk_prefix[j + 1]) ++j;
-      const int64_t local = ch - b.chunk_prefix[j];
-      const int o = (int)(local / cpo);
-      const int64_t c_in = local - (int64_t)o * cpo;
-      const MergeJob& job = b.jobs[j];
-      if (j != cur_job) {
-        n_out = build_job_table(job, b.E, b.compact, b.chunk_prefix[j] % gridDim.x == blockIdx.x, t);
-        cur_job = j;
+      if (j < 0 || ch >= b.chunk_prefix[j + 1]) {  // entering a new job: rebuild the table
+        do ++j; while (ch >= b.chunk_prefix[j + 1]);
+        local = ch - b.chunk_prefix[j];
+        o = (int)(local / cpo);
+        c_in = local - (int64_t)o * cpo;
+        n_out = build_job_table(b.jobs[j], b.E, b.compact, b.chunk_prefix[j] % gridDim.x == blockIdx.x, t);
+      } else {  // the next chunk of this CTA in the same job: advance without a 64-bit division
+        c_in += gridDim.x;
+        while (c_in >= cpo) {
+          c_in -= cpo;
+          ++o;
+        }
       }
       if (o >= n_out) continue;  // compact single-job calls: the slot count was an upper bound
+      const MergeJob& job = b.jobs[j];
       const int64_t e0 = c_in * kChunkElems;
       const int n_elems = (int)(b.numel - e0 < kChunkElems ? b.numel - e0 : kChunkElems);
       const uint32_t bytes = (uint32_t)n_elems * kEsz;
+      void* out = (uint8_t*)job.merged + ((int64_t)o * b.numel + e0) * kEsz;
       const int m0 = t.start[o], m1 = t.start[o + 1];
       int m = m0;
       do {  // one stage per group of up to 4 members (an output with no member still takes one stage)
-        const int s = g % kStages;
-        mbar_wait(&t.empty[s], ((g / kStages) & 1) ^ 1);
-        const int n = min(kSlicesPerStage, m1 - m);
-        if ((threadIdx.x & 31) == 0) {
+        const int s = next_stage();
+        const int n = min(kPerStage, m1 - m);
+        if (leader) {
           StageHdr& h = t.hdr[s];
-          for (int i = 0; i < kSlicesPerStage; ++i) h.w[i] = i < n ? t.w[m + i] : 0.f;
+#pragma unroll
+          for (int i = 0; i < kPerStage; ++i) h.w[i] = i < n ? t.w[m + i] : 0.f;
+          h.out = m + n >= m1 ? out : nullptr;
           h.n = n;
           h.nvec = (int)(bytes / 16);
           h.first = m == m0;
-          h.out = m + n >= m1 ? (void*)((uint8_t*)job.merged + ((int64_t)o * b.numel + e0) * kEsz) : nullptr;
           mbar_arrive_expect_tx(&t.full[s], (uint32_t)n * bytes);
           for (int i = 0; i < n; ++i)
             bulk_load_1d(t.data[s][i], (const uint8_t*)job.experts + ((int64_t)t.mem[m + i] * b.numel + e0) * kEsz,
@@ -174,78 +187,66 @@ __global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_co
         }
         __syncwarp();
         m += n;
-        ++g;
       } while (m < m1);
     }
-    // end marker: one stage with n = -1
-    const int s = g % kStages;
-    mbar_wait(&t.empty[s], ((g / kStages) & 1) ^ 1);
-    if ((threadIdx.x & 31) == 0) {
+    const int s = next_stage();  // end marker
+    if (leader) {
       t.hdr[s].n = -1;
       mbar_arrive(&t.full[s]);
     }
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- consumers
-    const int tid = threadIdx.x - 32;
-    constexpr int kPerVec = 16 / kEsz;  // elements per 16-byte vector
-    float acc[2][kPerVec];
-    int g = 0;
-    for (;; ++g) {
+    const int v = threadIdx.x - 32;  // this thread's 16-byte vector of every chunk
+    constexpr int kPairs = 16 / kEsz / 2;
+    float2 acc[kPairs];
+    for (int g = 0;; ++g) {
       const int s = g % kStages;
-      // the producer signals the end with a stage whose n is -1 (below)
       mbar_wait(&t.full[s], (g / kStages) & 1);
-      const StageHdr h = t.hdr[s];
-      if (h.n < 0) break;
-      if (h.first) {
+      const int n = t.hdr[s].n;
+      if (n < 0) break;
+      const int nvec = t.hdr[s].nvec;
+      void* out = t.hdr[s].out;
+      if (t.hdr[s].first) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int i = 0; i < kPerVec; ++i) acc[u][i] = 0.f;
+        for (int i = 0; i < kPairs; ++i) acc[i] = make_float2(0.f, 0.f);
       }
-      for (int mi = 0; mi < h.n; ++mi) {
-        const float wm = h.w[mi];
+      if (v < nvec) {
+        uint4 r[kPerStage];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int v = tid + u * kConsumers;
-          if (v < h.nvec) {
-            const uint4 r = *reinterpret_cast<const uint4*>(t.data[s][mi] + v * 16);
-            if constexpr (F32) {
-              const float* f = reinterpret_cast<const float*>(&r);
+        for (int mi = 0; mi < kPerStage; ++mi)
+          if (mi < n) r[mi] = *reinterpret_cast<const uint4*>(t.data[s][mi] + v * 16);
 #pragma unroll
-              for (int i = 0; i < 4; ++i) acc[u][i] = fmaf(wm, f[i], acc[u][i]);
-            } else {
-              const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&r);
+        for (int mi = 0; mi < kPerStage; ++mi) {
+          if (mi >= n) break;
+          const float w = t.hdr[s].w[mi];
+          const float2 w2 = make_float2(w, w);
+          if constexpr (F32) {
+            acc[0] = fma2_rn(w2, make_float2(__uint_as_float(r[mi].x), __uint_as_float(r[mi].y)), acc[0]);
+            acc[1] = fma2_rn(w2, make_float2(__uint_as_float(r[mi].z), __uint_as_float(r[mi].w)), acc[1]);
+          } else {
+            const uint32_t u[4] = {r[mi].x, r[mi].y, r[mi].z, r[mi].w};
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float2 p = __bfloat1622float2(hh[i]);
-                acc[u][2 * i] = fmaf(wm, p.x, acc[u][2 * i]);
-                acc[u][2 * i + 1] = fmaf(wm, p.y, acc[u][2 * i + 1]);
-              }
-            }
+            for (int i = 0; i < 4; ++i)  // bf16 -> fp32 is exact: the pair's bits shifted into place
+              acc[i] = fma2_rn(w2, make_float2(__uint_as_float(u[i] << 16), __uint_as_float(u[i] & 0xffff0000u)),
+                               acc[i]);
           }
         }
       }
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&t.empty[s]);
-      if (h.out) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int v = tid + u * kConsumers;
-          if (v < h.nvec) {
-            uint4 o;
-            if constexpr (F32) {
-              o = make_uint4(__float_as_uint(acc[u][0]), __float_as_uint(acc[u][1]), __float_as_uint(acc[u][2]),
-                             __float_as_uint(acc[u][3]));
-            } else {
-              o.x = pack_bf16x2(acc[u][0], acc[u][1]);
-              o.y = pack_bf16x2(acc[u][2], acc[u][3]);
-              o.z = pack_bf16x2(acc[u][4], acc[u][5]);
-              o.w = pack_bf16x2(acc[u][6], acc[u][7]);
-            }
-            __stcs(reinterpret_cast<uint4*>(h.out) + v, o);
-          }
+      if (out && v < nvec) {
+        uint4 ov;
+        if constexpr (F32) {
+          ov = make_uint4(__float_as_uint(acc[0].x), __float_as_uint(acc[0].y), __float_as_uint(acc[1].x),
+                          __float_as_uint(acc[1].y));
+        } else {
+          ov.x = pack_bf16x2(acc[0].x, acc[0].y);
+          ov.y = pack_bf16x2(acc[1].x, acc[1].y);
+          ov.z = pack_bf16x2(acc[2].x, acc[2].y);
+          ov.w = pack_bf16x2(acc[3].x, acc[3].y);
         }
+        __stcs(reinterpret_cast<uint4*>(out) + v, ov);
       }
     }
   }

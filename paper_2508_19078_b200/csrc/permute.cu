@@ -23,29 +23,30 @@ namespace flux {
 namespace {
 
 
+// Exclusive scan over the CTA (NW warps); sh: NW ints of shared memory.
+template <int NW>
 __device__ __forceinline__ int block_exclusive_scan(int v, int* sh, int& total) {
-  // 256 threads
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) sh[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    int s = lane < 8 ? sh[lane] : 0;
+    int s = lane < NW ? sh[lane] : 0;
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, s, o);
+    for (int o = 1; o < NW; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
-    if (lane < 8) sh[lane] = s;
+    if (lane < NW) sh[lane] = s;
   }
   __syncthreads();
   const int warp_prefix = wid ? sh[wid - 1] : 0;
-  total = sh[7];
+  total = sh[NW - 1];
   __syncthreads();
   return warp_prefix + x - v;
 }
@@ -100,20 +101,20 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
 // also publishes offsets, the user's D_e bounds and both GEMM tile schedules.  Phase 3: one thread per
 // pick (t, j): pos = offsets[e] + tile_base[tile][e] + rank -> token_index[pos] = t, inv_pos = pos.
 constexpr int kMaxE2 = 1024;
-__global__ void __launch_bounds__(256) permute_kernel(ScheduleArgs a, const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(512) permute_kernel(ScheduleArgs a, const int32_t* __restrict__ ids,
                                                       const int32_t* __restrict__ rank, int32_t* __restrict__ inv_pos,
                                                       int32_t* __restrict__ token_index) {
-  __shared__ int sh[8];
+  __shared__ int sh[16];
   __shared__ int s_off[kMaxE2 + 1];
   const int E = a.E;
   // ---- phase 1: per-expert scans
   for (int e = blockIdx.x; e < E; e += gridDim.x) {
     int carry = 0;
-    for (int base = 0; base < a.n_tiles; base += 256) {
+    for (int base = 0; base < a.n_tiles; base += 512) {
       const int tile = base + threadIdx.x;
       const int v = tile < a.n_tiles ? __ldcg(&a.tile_counts[(int64_t)tile * E + e]) : 0;
       int tot;
-      const int ex = block_exclusive_scan(v, sh, tot);
+      const int ex = block_exclusive_scan<16>(v, sh, tot);
       if (tile < a.n_tiles) a.tile_base[(int64_t)tile * E + e] = carry + ex;
       carry += tot;
     }
@@ -125,21 +126,23 @@ __global__ void __launch_bounds__(256) permute_kernel(ScheduleArgs a, const int3
     __threadfence();
     atomicAdd(a.done_counter, 1);
     int seen;
-    do {
+    for (;;) {  // back off between polls: ~300 CTAs polling one line slow the arrivals down
       asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(a.done_counter) : "memory");
-    } while (seen < (int)gridDim.x);
+      if (seen >= (int)gridDim.x) break;
+      __nanosleep(64);
+    }
   }
   __syncthreads();
   // ---- phase 2: offsets (every CTA, in shared memory); CTA 0 publishes offsets + GEMM schedules
   const int n_groups = E + (a.has_shared ? 1 : 0);
   int carry_rows = 0, carry_gu = 0, carry_dn = 0;
-  for (int base = 0; base < n_groups; base += 256) {
+  for (int base = 0; base < n_groups; base += 512) {
     const int g = base + threadIdx.x;
     int rows = 0;
     if (g < E) rows = __ldcg(&a.grp_rows[g]);
     else if (g < n_groups) rows = (int)a.T;
     int tot_rows;
-    const int ex_rows = block_exclusive_scan(g < E ? rows : 0, sh, tot_rows);
+    const int ex_rows = block_exclusive_scan<16>(g < E ? rows : 0, sh, tot_rows);
     const int row0 = g < E ? carry_rows + ex_rows : 0;
     if (g < E) s_off[g] = row0;
     if (blockIdx.x == 0) {
@@ -147,8 +150,8 @@ __global__ void __launch_bounds__(256) permute_kernel(ScheduleArgs a, const int3
       const int ngu = mt * (g < E ? a.n_tiles_gu : a.n_tiles_gu_sh);
       const int ndn = mt * (g < E ? a.n_tiles_dn : a.n_tiles_dn_sh);
       int tot_gu, tot_dn;
-      const int ex_gu = block_exclusive_scan(g < n_groups ? ngu : 0, sh, tot_gu);
-      const int ex_dn = block_exclusive_scan(g < n_groups ? ndn : 0, sh, tot_dn);
+      const int ex_gu = block_exclusive_scan<16>(g < n_groups ? ngu : 0, sh, tot_gu);
+      const int ex_dn = block_exclusive_scan<16>(g < n_groups ? ndn : 0, sh, tot_dn);
       if (g < n_groups) {
         a.grp_row0[g] = row0;
         if (g >= E) a.grp_rows[g] = rows;
@@ -173,23 +176,40 @@ __global__ void __launch_bounds__(256) permute_kernel(ScheduleArgs a, const int3
         a.grp_rows_sh[0] = (int)a.T;
       }
     }
-    for (int g = threadIdx.x; g <= E; g += 256) {
+    for (int g = threadIdx.x; g <= E; g += 512) {
       a.offsets[g] = s_off[g];
       if (a.user_offsets) a.user_offsets[g] = s_off[g];
     }
   }
-  // ---- phase 3: one thread per pick
+  // ---- phase 3: one thread per pick; four independent picks per thread in flight (their ids / rank /
+  // tile_base loads are issued before the first store)
   const int64_t Tk = a.T * a.k;
   const int k = a.k;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Tk; i += (int64_t)gridDim.x * blockDim.x) {
-    const int e = __ldcs(&ids[i]);
-    const int64_t t = i / k;
-    int p = -1;
-    if (e >= 0) {  // -1: a pick folded by gate re-routing (NEXT-2) owns no row
-      p = s_off[e] + __ldcg(&a.tile_base[(t / kRouterTile) * E + e]) + __ldcs(&rank[i]);
-      token_index[p] = (int32_t)t;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < Tk; i0 += 4 * stride) {
+    int e[4], r[4], tb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      e[u] = i < Tk ? __ldcs(&ids[i]) : -2;
+      r[u] = i < Tk ? __ldcs(&rank[i]) : 0;
     }
-    inv_pos[i] = p;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      tb[u] = e[u] >= 0 ? __ldcg(&a.tile_base[((i / k) / kRouterTile) * E + e[u]]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (e[u] == -2) continue;
+      int p = -1;
+      if (e[u] >= 0) {  // -1: a pick folded by gate re-routing (NEXT-2) owns no row
+        p = s_off[e[u]] + tb[u] + r[u];
+        token_index[p] = (int32_t)(i / k);
+      }
+      inv_pos[i] = p;
+    }
   }
 }
 }  // namespace
@@ -200,15 +220,15 @@ cudaError_t launch_permute(const ScheduleArgs& a0, const int32_t* ids, const int
   static int max_blocks = -1;  // co-resident CTAs per SM (cooperative launch bound)
   if (max_blocks < 0) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, permute_kernel, 256, 0) != cudaSuccess) return cudaErrorUnknown;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, permute_kernel, 512, 0) != cudaSuccess) return cudaErrorUnknown;
     max_blocks = n;
   }
   const int64_t Tk = a0.T * a0.k;
-  const int64_t want = std::max<int64_t>((int64_t)a0.E, (Tk + 255) / 256);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * std::min(max_blocks, 4)));
+  const int64_t want = std::max<int64_t>((int64_t)a0.E, (Tk + 2047) / 2048);  // 4 picks per thread
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * std::min(max_blocks, 2)));
   ScheduleArgs a = a0;
   void* args[] = {&a, &ids, &rank, &inv_pos, &token_index};
-  return cudaLaunchCooperativeKernel((const void*)permute_kernel, dim3(grid), dim3(256), args, 0, st);
+  return cudaLaunchCooperativeKernel((const void*)permute_kernel, dim3(grid), dim3(512), args, 0, st);
 }
 
 cudaError_t launch_scatter(const void* x, int64_t T, int H, int E, int k, const int32_t* ids, const int32_t* rank,

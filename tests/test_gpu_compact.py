@@ -164,3 +164,55 @@ def test_merge_error_falls_with_more_clusters():
         _, prof_c, _ = _gpu_compact(cfg, co, _alpha(cfg), cfg.tokens, with_logits=False)
         errs.append(float(F.output_error(prof_c.y[last], prof_d.y[last]).item()))
     assert abs(errs[2]) < 1e-12 and errs[0] > errs[1] > 1e-6, errs
+
+
+def test_adaptive_layer_sizes_end_to_end():
+    """Per-layer budgets (eq.(1)) through the whole merge path: layer l keeps n_tun[l] tuning
+    experts and B(l) merged slots (different per layer), the compact model's forward uses per-layer
+    expert counts, and every layer equals the oracle's compact layer (O10/O11).  The budgets come from
+    the ORACLE's eq.(1) on the oracle's own routing counts of a token sample."""
+    import oracle
+    cfg = CASES["shared_e16"][0]
+    L, E = cfg.n_layers, cfg.n_experts
+    res = om.profile_tokens(cfg, np.arange(256))
+    hist = np.stack([np.bincount(r["ids"].ravel(), minlength=E) for r in res]).astype(np.int64)
+    n_tun = np.array([2, 0])
+    Cl, *_ = oracle.layer_budget(hist, 256, 10, n_non=E - n_tun)
+    Cl = np.array([max(2, Cl[0]), min(E - n_tun[1], Cl[1] + 5)])  # make the two layers clearly differ
+    co = np.stack([synth.cluster_assignment(cfg, int(Cl[l]), n_tuning=int(n_tun[l]))[l] for l in range(L)])
+    alpha = _alpha(cfg, seed=11)
+    from paper_2508_19078_b200 import synthetic
+    from paper_2508_19078_b200.driver import Profiler, compact_model, merge_model
+    masters = synthetic.master_weights(cfg)
+    model = compact_model(masters, torch.from_numpy(alpha).cuda(), torch.from_numpy(co).cuda(), Cl.tolist(),
+                          n_tun.tolist())
+    S = n_tun + Cl
+    assert model.shape.layer_experts == tuple(int(s) for s in S)
+    T = cfg.tokens
+    prof = Profiler(model.shape, T, with_logits=True)
+    ys = []
+    prof.run(model, synthetic.tokens(cfg, 0, T), on_layer=lambda l, y: ys.append(y.float().cpu().numpy()))
+    torch.cuda.synchronize()
+    toks = np.linspace(0, T - 1, 96).astype(np.int64)
+    layers = [om.compact_layer(om.dense_layer(cfg, l), co[l], alpha[l].astype(np.float64)) for l in range(L)]
+    ref = om.compact_forward(cfg, toks, layers)
+    alive = np.ones(len(toks), bool)
+    x_prev = None
+    for l in range(L):
+        assert np.array_equal(model.remap[l].cpu().numpy(), layers[l][5])
+        ids = prof.ids[l].cpu().numpy()
+        check_hist_and_de(ids, prof.hist[l].cpu().numpy()[:S[l]], prof.offsets[l].cpu().numpy()[:S[l] + 1],
+                          prof.token_index[l].cpu().numpy(), int(S[l]))
+        assert ids.max() < S[l]
+        dz = input_bound(x_prev, ref[l]["x"], layers[l][0])
+        _compare(l, ref[l], prof.logits[l].cpu().numpy()[toks], ids[toks], prof.w[l].cpu().numpy()[toks],
+                 ys[l][toks], alive, dz)
+        x_prev = ys[l][toks]
+    assert alive.mean() > 0.8
+    # the plain merge with the same per-layer budgets (no tuning experts in layer 1): its slots are the
+    # compact model's cluster slots
+    merged = merge_model(masters, torch.from_numpy(alpha).cuda(), torch.from_numpy(co).cuda(), Cl.tolist())
+    for l in range(L):
+        for fam, W in (("gate", model.gate), ("up", model.up), ("down", model.down)):
+            got = getattr(merged, fam)[l][:Cl[l]]
+            assert torch.equal(got, W[l][n_tun[l]:S[l]]), (l, fam)

@@ -14,14 +14,14 @@ import sys
 
 NAMES = [("grouped_gemm_pair_kernel<0>", "K3/K5 gate/up GEMM (pair)"), ("grouped_gemm_pair_kernel<1>", "K4/K5 down GEMM (pair)"),
          ("grouped_gemm_kernel<0>", "K3/K5 gate/up GEMM (1-CTA)"), ("grouped_gemm_kernel<1>", "K4/K5 down GEMM (1-CTA)"),
-         ("router_kernel", "K1 router"), ("schedule_kernel", "K2 schedule"), ("scatter_kernel", "K2 scatter"),
+         ("router_kernel", "K1 router"), ("permute_kernel", "K2 permute (one kernel)"), ("scatter_kernel", "K2 x_perm copy"),
          ("grouped_gemm_pair_kernel<(int)0>", "K3/K5 gate/up GEMM (pair)"),
          ("grouped_gemm_pair_kernel<(int)1>", "K4/K5 down GEMM (pair)"),
          ("grouped_gemm_pair_q_kernel<(int)0", "K3/K5 gate/up GEMM (fused dequant)"),
          ("grouped_gemm_pair_q_kernel<(int)1", "K4/K5 down GEMM (fused dequant)"),
          ("grouped_gemm_kernel<(int)0>", "K3/K5 gate/up GEMM (1-CTA)"), ("grouped_gemm_kernel<(int)1>", "K4/K5 down GEMM (1-CTA)"),
          ("combine_kernel", "K6 combine"), ("quantize_kernel", "K0 quantize"), ("dequant_kernel", "K3/K4 dequant pass"),
-         ("merge_kernel", "K7 merge"), ("gram_reduce_kernel", "K8b Gram reduce"), ("gram_kernel", "K8 Gram (PCA)"),
+         ("merge_tma_kernel", "K7 merge (batched, TMA)"), ("merge_kernel", "K7 merge"), ("gram_reduce_kernel", "K8b Gram reduce"), ("gram_kernel", "K8 Gram (PCA)"),
          ("eig_kernel", "K8c Jacobi eigen"), ("kmeans_kernel", "K9 K-Means"), ("cosine_distance_kernel", "output error")]
 
 
