@@ -209,7 +209,9 @@ flux_status flux_merge_experts_batch(flux_dtype dtype, int32_t n_experts, int64_
  * ------------------------------------------------------------------------- */
 /* eq.(2) as flux_merge_experts, but the output holds every slot of the compact model in
  * remap order: compact[remap[e]] for all e — each tuning expert copied bit for bit (a
- * singleton with weight α/α = 1), then the C merged clusters.  compact: [n_tun + C][numel].
+ * singleton with weight α/α = 1), then the C merged clusters.  compact: [n_tun + C][numel]
+ * (n_tun = the number of -1 entries; slots at index >= n_experts are never written, which
+ * only concerns n_tun + C > E, where some clusters are necessarily empty).
  * Feed the slots to flux_profile_layer with wbits = 16, n_experts = n_tun + C,
  * n_router = E and flux_qlayer.remap = remap (the gate keeps scoring the original experts). */
 flux_status flux_compact_experts(flux_dtype dtype, int32_t n_experts, int64_t numel, const void* experts,

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(192, 1)
   using C = GramCfg<NPAD, INFL>;
   constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still a shared-space pointer
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kTile + C::kPad);
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;    // [2]

@@ -64,7 +64,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr int kRawStages = Cfg<WB>::kRawStages;
   constexpr int kStageBytes = Cfg<WB>::kStageBytes;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still a shared-space pointer
   uint8_t* raw_ring = smem + kStages * kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(raw_ring + kRawStages * kRawTx);  // leader: A bytes + dequant arrivals
   uint64_t* empty = full + kStages;                                             // both: MMA done with A/B stage

@@ -72,7 +72,8 @@ __device__ int build_job_table(const MergeJob& job, int E, int compact, bool wri
     const int e = e0 + lane;
     n_tun += __popc(__ballot_sync(0xffffffffu, e < E && __ldg(&job.cluster_of[e]) == -1));
   }
-  const int n_out = compact ? n_tun + job.n_clusters : job.n_clusters;
+  // outputs: at most E (the table's bound); n_tun + C > E leaves clusters without members anyway
+  const int n_out = min(compact ? n_tun + job.n_clusters : job.n_clusters, E);
   for (int o = lane; o <= n_out; o += 32) {
     t.start[o] = 0;
     t.fill[o] = 0;
@@ -84,7 +85,8 @@ __device__ int build_job_table(const MergeJob& job, int E, int compact, bool wri
     const int cl = e < E ? __ldg(&job.cluster_of[e]) : -2;
     const unsigned tun = __ballot_sync(0xffffffffu, cl == -1);
     const bool in_range = cl >= 0 && cl < job.n_clusters;
-    const int slot = cl == -1 ? rank0 + __popc(tun & ((1u << lane) - 1u)) : in_range ? n_tun + cl : -1;
+    int slot = cl == -1 ? rank0 + __popc(tun & ((1u << lane) - 1u)) : in_range ? n_tun + cl : -1;
+    if (slot >= n_out && compact) slot = -1;  // beyond the table (only with n_tun + C > E)
     if (e < E) {
       const int lab = compact ? slot : (in_range ? cl : -1);
       t.lab[e] = lab;
@@ -120,7 +122,7 @@ __device__ int build_job_table(const MergeJob& job, int E, int compact, bool wri
 template <bool F32>
 __global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_constant__ MergeBatch b) {
   extern __shared__ uint8_t smem_raw[];
-  BatchSmem& t = *reinterpret_cast<BatchSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  BatchSmem& t = *reinterpret_cast<BatchSmem*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   constexpr int kEsz = F32 ? 4 : 2;
   constexpr int kChunkElems = kSlice / kEsz;
   const int64_t cpo = (b.numel + kChunkElems - 1) / kChunkElems;  // chunks per output

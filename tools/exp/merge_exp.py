@@ -65,7 +65,7 @@ def timed(fn, hot):
     return e0.elapsed_time(e1), clk()
 
 
-for v, bps in ((0, 1), (1, 3), (1, 4), (2, 3), (2, 2), (4, 1), (4, 2)):
+for v, bps in ((0, 1),):
     run_variant(v, bps)
     torch.cuda.synchronize()
     if v:
