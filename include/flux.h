@@ -130,6 +130,13 @@ enum {
   FLUX_ROWS_TMA_GATHER4 = 2       /* TEST-ONLY: TMA tile::gather4 (~2.5x slower gate/up GEMM) */
 };
 #define FLUX_L2_SET 0x100         /* l2_hints = FLUX_L2_SET | bits overrides the default (bits 1) */
+enum {
+  FLUX_CHAIN_AUTO = 0,            /* the measured default                          */
+  FLUX_CHAIN_OFF = 1,             /* gate/up and down GEMMs as two launches (act round-trips through HBM) */
+  FLUX_CHAIN_ON = 2               /* one persistent launch: each m-tile's down tiles follow its gate/up
+                                     tiles, act read back from L2 (dequant-pass path with the in-GEMM
+                                     gather, claimed tiles, standalone combine; ignored otherwise)       */
+};
 typedef struct {
   int32_t weight_path;    /* FLUX_WEIGHTS_*                                                      */
   int32_t routed_rows;    /* FLUX_ROWS_*                                                         */
@@ -137,6 +144,7 @@ typedef struct {
   int32_t static_tiles;   /* 1 = TEST-ONLY: static round-robin GEMM tile order instead of claimed tiles */
   int32_t l2_hints;       /* 0 = default (evict_first on the act / y_perm stores); FLUX_L2_SET | bits:
                              bit 0 evict_first on output stores, bit 1 evict_last on B, bit 2 evict_first on A */
+  int32_t gemm_chain;     /* FLUX_CHAIN_*                                                        */
 } flux_policy;
 
 /* Workspace bytes flux_profile_layer needs for T tokens (host function); it depends on the policy

@@ -58,16 +58,17 @@ class Policy(ctypes.Structure):
     """flux_policy (include/flux.h): performance policy of flux_profile_layer_ex; all-zero = defaults.
     Every value gives bit-identical outputs; TEST-ONLY values were measured slower."""
     _fields_ = [("weight_path", ctypes.c_int32), ("routed_rows", ctypes.c_int32), ("fused_combine", ctypes.c_int32),
-                ("static_tiles", ctypes.c_int32), ("l2_hints", ctypes.c_int32)]
+                ("static_tiles", ctypes.c_int32), ("l2_hints", ctypes.c_int32), ("gemm_chain", ctypes.c_int32)]
 
 
 WEIGHTS_AUTO, WEIGHTS_DEQUANT_PASS, WEIGHTS_IN_GEMM = 0, 1, 2
 ROWS_AUTO, ROWS_MATERIALISED, ROWS_TMA_GATHER4 = 0, 1, 2
 L2_SET = 0x100
+CHAIN_AUTO, CHAIN_OFF, CHAIN_ON = 0, 1, 2
 
 
-def make_policy(weight_path=0, routed_rows=0, fused_combine=0, static_tiles=0, l2_hints=0) -> Policy:
-    return Policy(weight_path, routed_rows, fused_combine, static_tiles, l2_hints)
+def make_policy(weight_path=0, routed_rows=0, fused_combine=0, static_tiles=0, l2_hints=0, gemm_chain=0) -> Policy:
+    return Policy(weight_path, routed_rows, fused_combine, static_tiles, l2_hints, gemm_chain)
 
 
 class LayerOut(ctypes.Structure):

@@ -89,6 +89,7 @@ struct Policy {
   bool fused_combine;
   bool dynamic_tiles;
   int l2_hints;
+  bool chain;  // gate/up + down in one launch (gemm_chain.cu)
 };
 static Policy resolve_policy(const flux_moe_cfg& c, const flux_policy* up, int64_t T) {
   flux_policy d{};
@@ -104,13 +105,17 @@ static Policy resolve_policy(const flux_moe_cfg& c, const flux_policy* up, int64
   p.fused_combine = u.fused_combine != 0 && c.shared_ffn > 0;
   p.dynamic_tiles = u.static_tiles == 0;
   p.l2_hints = (u.l2_hints & FLUX_L2_SET) ? (u.l2_hints & 7) : 1;
+  // chained GEMMs need the dequant-pass kernels with the cp.async gather, claimed tiles and the standalone
+  // combine, and at most 128 routed groups (+ the shared MLP); auto = off until measured faster
+  p.chain = u.gemm_chain == FLUX_CHAIN_ON && p.pass && p.gmode == GATHER_CP && p.dynamic_tiles && !p.fused_combine &&
+            c.n_experts <= 128;
   return p;
 }
 static flux_status validate_policy(const flux_policy* u) {
   if (!u) return FLUX_OK;
   if (u->weight_path < 0 || u->weight_path > 2 || u->routed_rows < 0 || u->routed_rows > 2 ||
       (u->fused_combine != 0 && u->fused_combine != 1) || (u->static_tiles != 0 && u->static_tiles != 1) ||
-      (u->l2_hints != 0 && (u->l2_hints & ~(FLUX_L2_SET | 7)) != 0))
+      (u->l2_hints != 0 && (u->l2_hints & ~(FLUX_L2_SET | 7)) != 0) || u->gemm_chain < 0 || u->gemm_chain > 2)
     return FLUX_E_INVALID;
   return FLUX_OK;
 }
@@ -139,7 +144,7 @@ struct Layout {
 };
 struct WsPlan {
   size_t tile_counts, tile_base, rank, offsets, token_index, inv_pos, counter, sched_gu, sched_dn, row0, rows;
-  size_t x_perm, y_perm, act, act_sh, sh_sched, y_sh, wgu_r, wdn_r, wgu_s, wdn_s;
+  size_t x_perm, y_perm, act, act_sh, sh_sched, y_sh, wgu_r, wdn_r, wgu_s, wdn_s, sched_c, mt_base, ready;
   size_t total;
 };
 int pad128(int v) { return (v + 127) / 128 * 128; }
@@ -178,6 +183,10 @@ WsPlan plan(const flux_moe_cfg& c, const Policy& pol, int64_t T) {
   p.wdn_r = L.take(pass * 2ull * c.n_experts * c.hidden * pad64(c.ffn));
   p.wgu_s = L.take(pass * 2ull * 2 * pad128(c.shared_ffn) * c.hidden);
   p.wdn_s = L.take(pass * 2ull * c.hidden * pad64(c.shared_ffn));
+  const size_t ch = pol.chain ? 1 : 0;  // chained GEMMs: tile / m-tile prefixes and the act ready flags
+  p.sched_c = L.take(ch * sizeof(int32_t) * (n_groups + 1));
+  p.mt_base = L.take(ch * sizeof(int32_t) * n_groups);
+  p.ready = L.take(ch * sizeof(int32_t) * (Tk / 256 + T / 256 + n_groups + 2));
   p.total = L.off;
   return p;
 }
@@ -350,6 +359,9 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
   sa.grp_rows = (int32_t*)(W + P.rows);
   sa.gemm_bm = 256;  // CTA pairs
   sa.sched_sh = sh ? sh_sched : nullptr;
+  sa.sched_c = pol.chain ? (int32_t*)(W + P.sched_c) : nullptr;
+  sa.mt_base = pol.chain ? (int32_t*)(W + P.mt_base) : nullptr;
+  sa.ready = pol.chain ? (int32_t*)(W + P.ready) : nullptr;
   sa.grp_row0_sh = sh_sched + 2;
   sa.grp_rows_sh = sh_sched + 3;
   {  // indices in one kernel; the routed rows are copied to x_perm only when the GEMM does not gather them
@@ -441,6 +453,21 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
       return FLUX_E_CUDA;
     }
     if (!sh) { a_s = a_r; b_s = b_r; }
+    if (pol.chain) {  // K3 + K4 in one persistent launch
+      CUtensorMap a_r1, a_s1, b_r1, b_s1;
+      if (!tmap_bf16(&a_r1, act, Tk, F, 128, Fld) || !tmap_bf16(&b_r1, wdn_r, (uint64_t)E * H, F, bbox, Fld) ||
+          (sh && (!tmap_bf16(&a_s1, act_sh, T, Fs, 128, Fsld) || !tmap_bf16(&b_s1, wdn_s, H, Fs, bbox, Fsld)))) {
+        set_last_error("chain tensor maps", cudaErrorInvalidValue);
+        return FLUX_E_CUDA;
+      }
+      if (!sh) { a_s1 = a_r1; b_s1 = b_r1; }
+      ChainArgs ca{sa.sched_c, sa.mt_base, sa.ready, 8, sa.done_counter + 1};
+      KernelTimer kt(K_GEMM_CHAIN, s);
+      if ((e = launch_gemm_chain(a_r, a_s, b_r, b_s, a_r1, a_s1, b_r1, b_s1, ga, gd, ca, s)) != cudaSuccess) {
+        set_last_error("gemm_chain", e);
+        return FLUX_E_CUDA;
+      }
+    } else {
     {
       KernelTimer kt(K_GEMM_GU, s);
       if ((e = launch_gemm(EPI_SWIGLU, a_r, a_s, b_r, b_s, ga, s)) != cudaSuccess) { set_last_error("gemm_gate_up", e); return FLUX_E_CUDA; }
@@ -457,6 +484,7 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
     if (fuse_combine) {
       KernelTimer kt(K_GEMM_DN_SH_COMBINE, s);
       if ((e = launch_gemm(EPI_COMBINE, a_s, a_s, b_s, b_s, gsc, s)) != cudaSuccess) { set_last_error("gemm_down_shared_combine", e); return FLUX_E_CUDA; }
+    }
     }
   } else {
     // fused dequant: B tiles are built on chip from the canonical quantized weights

@@ -23,7 +23,7 @@ inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_O
 // ---------------------------------------------------------------- per-kernel timing (timing.cpp)
 enum KernelKind {
   K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_PERMUTE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
-  K_GEMM_DN_SH_COMBINE, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, K_COSINE, K_ATTN_HIST, FLUX_NUM_KERNELS
+  K_GEMM_DN_SH_COMBINE, K_GEMM_CHAIN, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, K_COSINE, K_ATTN_HIST, FLUX_NUM_KERNELS
 };
 // RAII: counts one launch; when timing is enabled records CUDA events around it on `st`.
 class KernelTimer {
@@ -126,6 +126,9 @@ struct ScheduleArgs {
   int32_t* grp_row0;        // [n_groups] first A row of each group
   int32_t* grp_rows;        // [n_groups] rows of each group
   int gemm_bm;              // GEMM tile rows (128 or 256)
+  int32_t* sched_c;         // [n_groups+1] chained gate/up + down tile prefix (null = not chained)
+  int32_t* mt_base;         // [n_groups] first global m-tile of each group (chained)
+  int32_t* ready;           // [M_total] per-m-tile act completion counters, zeroed by K2 (chained)
   int32_t* sched_sh;        // [2] tile prefix of the shared-MLP-only down GEMM (fused combine)
   int32_t* grp_row0_sh;     // [1] = 0
   int32_t* grp_rows_sh;     // [1] = T
@@ -182,6 +185,18 @@ struct GemmArgs {
 };
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);
+// K3 + K4 chained in one persistent launch (gemm_chain.cu): gate/up (args g0, maps *0) and down (g1, *1)
+struct ChainArgs {
+  const int32_t* sched_c;  // [n_groups+1] (K2)
+  const int32_t* mt_base;  // [n_groups] (K2)
+  int32_t* ready;          // [M_total], zeroed by K2
+  int D;                   // lag of a group's down tiles behind its gate/up tiles, in m-tiles
+  int32_t* tile_ctr;       // zeroed int
+};
+cudaError_t launch_gemm_chain(const CUtensorMap& a_r0, const CUtensorMap& a_s0, const CUtensorMap& b_r0,
+                              const CUtensorMap& b_s0, const CUtensorMap& a_r1, const CUtensorMap& a_s1,
+                              const CUtensorMap& b_r1, const CUtensorMap& b_s1, const GemmArgs& g0,
+                              const GemmArgs& g1, const ChainArgs& ca, cudaStream_t st);
 
 // Fused-dequant variant (CTA pairs): B comes straight from the quantized weights.
 struct QGemmArgs {

@@ -165,6 +165,29 @@ __global__ void __launch_bounds__(512) permute_kernel(ScheduleArgs a, const int3
   }
   if (threadIdx.x == 0) s_off[E] = carry_rows;
   __syncthreads();
+  if (blockIdx.x == 0 && a.sched_c) {  // chained GEMM (gemm_chain.cu): per-group tile and m-tile prefixes
+    int carry_c = 0, carry_mt = 0;
+    for (int base = 0; base < n_groups; base += 512) {
+      const int g = base + threadIdx.x;
+      int mt = 0, nc = 0;
+      if (g < n_groups) {
+        const int rows = g < E ? __ldcg(&a.grp_rows[g]) : (int)a.T;
+        mt = (rows + a.gemm_bm - 1) / a.gemm_bm;
+        nc = mt * (g < E ? a.n_tiles_gu + a.n_tiles_dn : a.n_tiles_gu_sh + a.n_tiles_dn_sh);
+      }
+      int tot_c, tot_mt;
+      const int ex_c = block_exclusive_scan<16>(nc, sh, tot_c);
+      const int ex_mt = block_exclusive_scan<16>(mt, sh, tot_mt);
+      if (g < n_groups) {
+        a.sched_c[g] = carry_c + ex_c;
+        a.mt_base[g] = carry_mt + ex_mt;
+      }
+      carry_c += tot_c;
+      carry_mt += tot_mt;
+    }
+    if (threadIdx.x == 0) a.sched_c[n_groups] = carry_c;
+    for (int i = threadIdx.x; i < carry_mt; i += 512) a.ready[i] = 0;
+  }
   if (blockIdx.x == 0) {
     if (threadIdx.x == 0) {
       a.sched_gu[n_groups] = carry_gu;

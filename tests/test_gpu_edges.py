@@ -83,7 +83,7 @@ def test_degenerate_cases_on_every_gemm_path(name):
     x = synthetic.tokens(cfg, 0, cfg.tokens)
     outs = []
     import paper_2508_19078_b200 as F
-    for pol in ((2, 0, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (1, 0, 0, 1), (0, 0, 0, 0)):
+    for pol in ((2, 0, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (1, 0, 0, 1), (0, 0, 0, 0), (1, 0, 0, 0, 0, 2)):
         prof = Profiler(shape, cfg.tokens, policy=F.make_policy(*pol))
         prof.run(qm, x)
         torch.cuda.synchronize()

@@ -119,7 +119,7 @@ def test_chunk_and_run_invariance():
 # every flux_policy combination the bit-identity test pins (weight path, routed rows, fused combine, static tiles)
 POLICIES = [(2, 0, 0, 0), (1, 0, 0, 0), (2, 1, 0, 0), (2, 0, 1, 0), (1, 0, 1, 0), (2, 2, 0, 0), (1, 2, 0, 0),
             (1, 1, 0, 0), (1, 0, 0, 1), (1, 0, 1, 1), (1, 1, 0, 1), (0, 0, 0, 0), (1, 0, 0, 0, 0x100 | 7),
-            (1, 0, 0, 0, 0x100 | 0)]
+            (1, 0, 0, 0, 0x100 | 0), (1, 0, 0, 0, 0, 2), (1, 0, 0, 0, 0, 1)]
 
 
 @pytest.mark.parametrize("name", ["int4_shared", "int8_ragged", "int4_e64", "pass_tails", "pass_tails_g64"])
@@ -127,8 +127,8 @@ def test_weight_paths_bit_identical(name):
     """Every flux_policy value — in-GEMM dequantization or the separate dequant pass, the routed A rows
     materialised (x_perm), gathered inside the GEMM with cp.async (the pass-path default) or with TMA
     gather4 (test-only), the combine standalone or fused into the shared down GEMM (test-only), claimed or
-    static tile order (test-only), every L2-hint combination — produces bit-identical layers: the choice is
-    a pure performance policy."""
+    static tile order (test-only), every L2-hint combination, gate/up and down as two launches or chained
+    in one — produces bit-identical layers: the choice is a pure performance policy."""
     import paper_2508_19078_b200 as F
     from paper_2508_19078_b200.driver import ModelShape, Profiler, QuantizedModel
     from paper_2508_19078_b200 import synthetic
