@@ -269,7 +269,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
     # ---- setup (not timed): synthetic master weights, this rank's token shard, buffers, NCCL comm
     masters = synthetic.master_weights(cfg)
     qm = QuantizedModel(shape)
-    prof = Profiler(shape, Tc, with_de=True)
+    prof = Profiler(shape, Tc, with_de=True, policy=F.make_policy(gemm_chain={"auto": 0, "off": 1, "on": 2}[args.chain]))
     t0, _ = shard(rank, world, T_rank)  # this rank's contiguous slice of the global token stream
     x = synthetic.tokens(cfg, t0, T_rank)
     cluster_of = torch.from_numpy(synth.cluster_assignment(cfg, C)).cuda()
@@ -481,8 +481,13 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
 def roofline_gemm(cfg, T_rank, res, peaks, peak_src):
     """The dominant kernel: the gate/up grouped GEMM (routed + shared, one launch per layer per chunk)."""
     H, k = cfg.hidden, cfg.top_k
-    gu_ms, gu_n = res["kern"].get("gemm_gate_up", (0.0, 0))
     flop_gu = 2.0 * res["Tc"] * (k * H * 2 * cfg.ffn + H * 2 * cfg.shared_ffn)  # per launch
+    kname = "gemm_gate_up (K3+K5)"
+    gu_ms, gu_n = res["kern"].get("gemm_gate_up", (0.0, 0))
+    if not gu_n and res["kern"].get("gemm_chain", (0.0, 0))[1]:  # gate/up + down chained in one launch
+        gu_ms, gu_n = res["kern"]["gemm_chain"]
+        flop_gu += 2.0 * res["Tc"] * (k * cfg.ffn * H + cfg.shared_ffn * H)
+        kname = "gemm_chain (K3+K4+K5: gate/up and down in one launch)"
     achieved = flop_gu / (gu_ms / gu_n / 1000.0) / 1e12 if gu_n else None
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     traffic = None
@@ -491,7 +496,7 @@ def roofline_gemm(cfg, T_rank, res, peaks, peak_src):
         # dram read+write bytes per launch from the committed `ncu --set full` capture (profiles/)
         traffic = json.load(open(tp)).get(f"{cfg_key(cfg)}:{res['Tc']}:K3/K5 gate/up GEMM (pair)")
     clk = res["clk"]
-    return {"bound": "tensor", "kernel": "gemm_gate_up (K3+K5)", "achieved": achieved, "peak": peak,
+    return {"bound": "tensor", "kernel": kname, "achieved": achieved, "peak": peak,
             "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "peak_source": peak_src + ", bf16 sustained", "flop_per_launch": flop_gu,
             "share_of_step": (gu_ms / res["steps"]) / (res["ms"] / res["steps"]) if gu_n else None,
@@ -554,6 +559,8 @@ def main():
                     help="pca: §5.2 PCA + K-Means on the GPU inside the step; seeded: a fixed balanced partition")
     ap.add_argument("--other-configs", default="llama_moe",
                     help="comma-separated extra workloads measured in the same run (N = 1 only; '' = none)")
+    ap.add_argument("--chain", default="auto", choices=["auto", "on", "off"],
+                    help="flux_policy.gemm_chain: gate/up + down GEMMs in one launch (on) or two (off)")
     ap.add_argument("--selftest-launcher", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     maybe_relaunch(args)

@@ -133,9 +133,10 @@ enum {
 enum {
   FLUX_CHAIN_AUTO = 0,            /* the measured default                          */
   FLUX_CHAIN_OFF = 1,             /* gate/up and down GEMMs as two launches (act round-trips through HBM) */
-  FLUX_CHAIN_ON = 2               /* one persistent launch: each m-tile's down tiles follow its gate/up
-                                     tiles, act read back from L2 (dequant-pass path with the in-GEMM
-                                     gather, claimed tiles, standalone combine; ignored otherwise)       */
+  FLUX_CHAIN_ON = 2               /* TEST-ONLY: one persistent launch, each m-tile's down tiles 24 m-tiles
+                                     behind its gate/up tiles (dequant-pass path with the in-GEMM gather,
+                                     claimed tiles, standalone combine; ignored otherwise).  Measured no
+                                     faster: act leaves L2 before it is read back */
 };
 typedef struct {
   int32_t weight_path;    /* FLUX_WEIGHTS_*                                                      */

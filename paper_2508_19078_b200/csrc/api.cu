@@ -461,7 +461,7 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
         return FLUX_E_CUDA;
       }
       if (!sh) { a_s1 = a_r1; b_s1 = b_r1; }
-      ChainArgs ca{sa.sched_c, sa.mt_base, sa.ready, 8, sa.done_counter + 1};
+      ChainArgs ca{sa.sched_c, sa.mt_base, sa.ready, 24, sa.done_counter + 1};
       KernelTimer kt(K_GEMM_CHAIN, s);
       if ((e = launch_gemm_chain(a_r, a_s, b_r, b_s, a_r1, a_s1, b_r1, b_s1, ga, gd, ca, s)) != cudaSuccess) {
         set_last_error("gemm_chain", e);

@@ -17,6 +17,13 @@
 // Everything else (tile shape 256 x 256 x 64-K, the 6-stage ring, cp.async gather of the routed A rows
 // of gate/up tiles, TMEM double buffering, TMA-store epilogues, MMA instruction order per tile) is the
 // gemm_pair.cu kernel's, so every output is bit-identical to the two-launch path.
+//
+// Measured (B200): NOT faster.  The lag must be ~24 m-tiles or the down tiles wait
+// (D = 2: 1.7x slower; D = 8 still waits on the LLaMA shape), and at that distance the act lines have
+// left L2 under the gathered x rows and the B tiles (ncu: 27.6 GB of DRAM traffic per DeepSeek layer
+// vs 27.9 GB for the two launches; the dirty act lines are written back either way).  In the bench step
+// DeepSeek ties (781 vs 780 ms of GEMM per step) and LLaMA loses 3%, so the policy default keeps the
+// two launches and this kernel is reachable as FLUX_CHAIN_ON (covered by the bit-identity tests).
 #include "gemm_pair.cuh"
 
 namespace flux {
@@ -32,6 +39,7 @@ struct ChainParams {
   const int32_t* mt_base;  // [n_groups] first global m-tile index of each group
   int32_t* ready;          // [M_total] act slices stored per m-tile (8 per gate/up tile)
   int D;
+  int act_hint;            // 1: act stored with the default L2 policy, read with evict_first; 2: stored evict_first
 };
 
 struct CTile {
@@ -193,6 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kChainThreads, 1)
         tma_prefetch(&mp.a_s[t]);
         tma_prefetch(&mp.b_s[t]);
       }
+    const uint64_t pol_first = policy_evict_first();
     uint32_t it = 0;
     for (int i = 0;; ++i) {
       const int tile = leader ? claim_tile(i) : next_tile(i);
@@ -206,8 +215,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kChainThreads, 1)
         // the act rows of this m-tile: every gate/up epilogue warp of both CTAs of all a_g tiles
         const int want = 8 * (routed ? p0.n_tiles_r : p0.n_tiles_s);
         const int32_t* flag = c.ready + s_mtb[ti.g] + ti.m;
+        if (lane_id() == 0 && ld_acquire_gpu(flag) < want) {
+          const uint64_t t0 = globaltimer_ns();
+          while (ld_acquire_gpu(flag) < want) {  // a wait past 10 s can only be a deadlock: fail loudly
+            __nanosleep(128);
+            if (globaltimer_ns() - t0 > 10000000000ull) __trap();
+          }
+        }
         if (lane_id() == 0) {
-          while (ld_acquire_gpu(flag) < want) __nanosleep(128);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // order the acquire before the TMA reads
         }
         __syncwarp();
@@ -227,7 +242,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kChainThreads, 1)
         if (leader && lane_id() == 0) mbar_arrive_expect_tx(&full[s], gather ? 2 * kBBytes : 2 * kStageBytes);
         __syncwarp();
         if (lane_id() == 0) {
-          if (!gather) tma_load_2d_pair(st, ta, &full[s], kb * kBK, arow);
+          if (ct.type == 1 && c.act_hint)  // act is dead once the m-tile's down tiles read it
+            tma_load_2d_pair_hint(st, ta, &full[s], kb * kBK, arow, pol_first);
+          else if (!gather)
+            tma_load_2d_pair(st, ta, &full[s], kb * kBK, arow);
           tma_load_2d_pair(st + kABytes, tb, &full[s], kb * kBK, brow);
         }
       }
@@ -334,7 +352,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kChainThreads, 1)
       if (ct.type == 0) {
         const int half = pair_tile_cols<EPI_SWIGLU>(p, ti) / 2;
         if (r_warp + 32 <= s_rows[ti.g]) {
-          epilogue_tma<EPI_SWIGLU>(p, taddr, ti, half, sc, tmo, stage_out, s_row0[ti.g] + r_warp, true, pol_store);
+          epilogue_tma<EPI_SWIGLU>(p, taddr, ti, half, sc, tmo, stage_out, s_row0[ti.g] + r_warp, c.act_hint == 2,
+                                   pol_store);
         } else {
           const int r_local = r_warp + (int)lane_id();
           epilogue_slice<EPI_SWIGLU>(p, taddr, ti, r_local < s_rows[ti.g], (int64_t)s_row0[ti.g] + r_local, half,
@@ -387,6 +406,7 @@ cudaError_t launch_gemm_chain(const CUtensorMap& a_r0, const CUtensorMap& a_s0, 
   c.mt_base = ca.mt_base;
   c.ready = ca.ready;
   c.D = ca.D;
+  c.act_hint = 1;
   auto omap = [](CUtensorMap* m, void* base, int64_t rows, int N, int64_t ld) {
     return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)rows, (uint64_t)N, (uint64_t)ld * 2, 64,
                         32, CU_TENSOR_MAP_SWIZZLE_128B);
