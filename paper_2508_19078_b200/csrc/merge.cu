@@ -44,13 +44,11 @@ constexpr int kStages = 6;                    // 6 x 32 KB = 192 KB of HBM reads
 constexpr int kConsumers = kSlice / 16;       // one 16-byte vector per consumer thread
 constexpr int kBThreads = 32 + kConsumers;
 
-struct StageHdr {
+struct __align__(16) StageHdr {  // read by the consumers as two 16-byte shared loads
   float w[kPerStage];
   void* out;       // output vectors of this chunk when the stage holds its last members, else null
   int n;           // member slices in this stage (0: an output without members -> zeros; -1: end)
-  int nvec;        // 16-byte vectors in this chunk
-  int first;       // the chunk's first stage: reset the accumulators
-  int pad;
+  int meta;        // 16-byte vectors in this chunk | (first stage of the chunk: reset the accumulators) << 30
 };
 
 struct BatchSmem {
@@ -180,8 +178,7 @@ __global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_co
           for (int i = 0; i < kPerStage; ++i) h.w[i] = i < n ? t.w[m + i] : 0.f;
           h.out = m + n >= m1 ? out : nullptr;
           h.n = n;
-          h.nvec = (int)(bytes / 16);
-          h.first = m == m0;
+          h.meta = (int)(bytes / 16) | (m == m0 ? 1 << 30 : 0);
           mbar_arrive_expect_tx(&t.full[s], (uint32_t)n * bytes);
           for (int i = 0; i < n; ++i)
             bulk_load_1d(t.data[s][i], (const uint8_t*)job.experts + ((int64_t)t.mem[m + i] * b.numel + e0) * kEsz,
@@ -202,37 +199,45 @@ __global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_co
     const int v = threadIdx.x - 32;  // this thread's 16-byte vector of every chunk
     constexpr int kPairs = 16 / kEsz / 2;
     float2 acc[kPairs];
+    // one member's FMA into the accumulators (bf16 -> fp32 is exact: the bits shifted into place)
+    auto fma_member = [&](const uint4& r, float w) {
+      const float2 w2 = make_float2(w, w);
+      if constexpr (F32) {
+        acc[0] = fma2_rn(w2, make_float2(__uint_as_float(r.x), __uint_as_float(r.y)), acc[0]);
+        acc[1] = fma2_rn(w2, make_float2(__uint_as_float(r.z), __uint_as_float(r.w)), acc[1]);
+      } else {
+        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          acc[i] = fma2_rn(w2, make_float2(__uint_as_float(u[i] << 16), __uint_as_float(u[i] & 0xffff0000u)), acc[i]);
+      }
+    };
     for (int g = 0;; ++g) {
       const int s = g % kStages;
       mbar_wait(&t.full[s], (g / kStages) & 1);
-      const int n = t.hdr[s].n;
+      const uint32_t ha = smem_u32(&t.hdr[s]);
+      const uint4 hw = ld_shared_v4(ha), hm = ld_shared_v4(ha + 16);  // weights; out, n, meta
+      const int n = (int)hm.z;
       if (n < 0) break;
-      const int nvec = t.hdr[s].nvec;
-      void* out = t.hdr[s].out;
-      if (t.hdr[s].first) {
+      const int nvec = (int)(hm.w & 0x3fffffffu);
+      void* out = reinterpret_cast<void*>((uint64_t)hm.x | ((uint64_t)hm.y << 32));
+      if (hm.w >> 30) {
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) acc[i] = make_float2(0.f, 0.f);
       }
       if (v < nvec) {
-        uint4 r[kPerStage];
-#pragma unroll
-        for (int mi = 0; mi < kPerStage; ++mi)
-          if (mi < n) r[mi] = *reinterpret_cast<const uint4*>(t.data[s][mi] + v * 16);
-#pragma unroll
-        for (int mi = 0; mi < kPerStage; ++mi) {
-          if (mi >= n) break;
-          const float w = t.hdr[s].w[mi];
-          const float2 w2 = make_float2(w, w);
-          if constexpr (F32) {
-            acc[0] = fma2_rn(w2, make_float2(__uint_as_float(r[mi].x), __uint_as_float(r[mi].y)), acc[0]);
-            acc[1] = fma2_rn(w2, make_float2(__uint_as_float(r[mi].z), __uint_as_float(r[mi].w)), acc[1]);
-          } else {
-            const uint32_t u[4] = {r[mi].x, r[mi].y, r[mi].z, r[mi].w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i)  // bf16 -> fp32 is exact: the pair's bits shifted into place
-              acc[i] = fma2_rn(w2, make_float2(__uint_as_float(u[i] << 16), __uint_as_float(u[i] & 0xffff0000u)),
-                               acc[i]);
-          }
+        const uint32_t d = smem_u32(t.data[s][0]) + v * 16;
+        if (n == kPerStage) {  // full stage (balanced 4-member clusters): every load first, then the FMAs
+          const uint4 r0 = ld_shared_v4(d), r1 = ld_shared_v4(d + kSlice), r2 = ld_shared_v4(d + 2 * kSlice),
+                      r3 = ld_shared_v4(d + 3 * kSlice);
+          fma_member(r0, __uint_as_float(hw.x));
+          fma_member(r1, __uint_as_float(hw.y));
+          fma_member(r2, __uint_as_float(hw.z));
+          fma_member(r3, __uint_as_float(hw.w));
+        } else {
+          const float ws[4] = {__uint_as_float(hw.x), __uint_as_float(hw.y), __uint_as_float(hw.z),
+                               __uint_as_float(hw.w)};
+          for (int mi = 0; mi < n; ++mi) fma_member(ld_shared_v4(d + mi * kSlice), ws[mi]);
         }
       }
       __syncwarp();

@@ -1,7 +1,7 @@
 """Small workload that calls every libflux entry point once (run under compute-sanitizer by
 tools/sanitize.sh): quantize (INT8/INT4/INT2), the profile pass on every GEMM path (flux_policy: in-GEMM
 dequant, dequant pass with the in-GEMM cp.async gather, materialised x_perm, TMA gather4, fused combine,
-static tiles), features + K-Means, merge, compact model forward with gate re-routing, attention histogram,
+static tiles, chained gate/up + down), features + K-Means, merge, compact model forward with gate re-routing, attention histogram,
 output error.  Sizes are tiny: the sanitizers replay every memory access."""
 import os
 import sys
@@ -19,7 +19,7 @@ from paper_2508_19078_b200.driver import (ModelShape, Profiler, QuantizedModel, 
                                           compact_model, dense_model, expert_features_model, merge_model)
 
 # flux_policy (weight_path, routed_rows, fused_combine, static_tiles)
-PATHS = [(2, 0, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (1, 2, 0, 0), (1, 0, 1, 0), (1, 0, 0, 1)]
+PATHS = [(2, 0, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (1, 2, 0, 0), (1, 0, 1, 0), (1, 0, 0, 1), (1, 0, 0, 0, 0, 2)]
 
 
 def run(cfg, paths):
