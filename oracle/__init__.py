@@ -64,7 +64,7 @@ def lib():
         L.orc_permute.argtypes = [_I64, _I, _I, _P, _P, _P, _P, _P]
         L.orc_moe_tokens.argtypes = [_I64, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I]
         L.orc_moe_tokens.restype = _I
-        L.orc_compact_tokens.argtypes = [_I64, _I, _I, _I, _I, _I, _I, _I] + [_P] * 14
+        L.orc_compact_tokens.argtypes = [_I64, _I, _I, _I, _I, _I, _I, _I] + [_P] * 17
         L.orc_layer_budget.argtypes = [_I, _I, _P, _I64, _I64, _P, _P, _P, _P]
         L.orc_layer_budget.restype = _I64
         L.orc_merge.argtypes = [_I, _I64, _P, _P, _P, _I, _P, _P]
@@ -202,11 +202,13 @@ def moe_tokens(x, wr, experts, shared, *, k: int, group_size: int, norm: int, re
     return y, ids, w, z, m
 
 
-def compact_tokens(x, wr, remap, gate, up, down, shared=None, *, k: int, norm: int):
+def compact_tokens(x, wr, remap, gate, up, down, shared=None, *, k: int, norm: int, residual=None,
+                   with_cond=False):
     """O11 (NEXT-2): gate re-routing through remap + compact-model forward with full-precision weights.
     gate/up [S][F][H], down [S][H][F]; shared = (gate [Fs][H], up [Fs][H], down [H][Fs]) or None.
-    Returns (y, ids (slot or -1), w, z, margin)."""
+    residual / with_cond as in moe_tokens.  Returns (y, ids (slot or -1), w, z, margin[, cond, dmag])."""
     x = _c(x, np.float64)
+    r = None if residual is None else _c(residual, np.float64)
     wr = _c(wr, np.float64)
     n, H = x.shape
     Er = wr.shape[0]
@@ -224,12 +226,16 @@ def compact_tokens(x, wr, remap, gate, up, down, shared=None, *, k: int, norm: i
     w = np.empty((n, k))
     z = np.empty((n, Er))
     m = np.empty(n)
+    cond = np.empty((n, H)) if with_cond else None
+    dmag = np.empty((n, H)) if with_cond else None
     p = lambda a: None if a is None else a.ctypes.data  # noqa: E731
     rc = lib().orc_compact_tokens(n, H, Er, k, S, F, Fs, norm, x.ctypes.data, wr.ctypes.data, rm.ctypes.data,
-                                  g.ctypes.data, u.ctypes.data, d.ctypes.data, p(sg), p(su), p(sd), y.ctypes.data,
-                                  ids.ctypes.data, w.ctypes.data, z.ctypes.data, m.ctypes.data)
+                                  g.ctypes.data, u.ctypes.data, d.ctypes.data, p(sg), p(su), p(sd), p(r), y.ctypes.data,
+                                  ids.ctypes.data, w.ctypes.data, z.ctypes.data, m.ctypes.data, p(cond), p(dmag))
     if rc:
         raise ValueError(f"orc_compact_tokens failed ({rc})")
+    if with_cond:
+        return y, ids, w, z, m, cond, dmag
     return y, ids, w, z, m
 
 

@@ -377,12 +377,14 @@ int orc_moe_tokens(int64_t n, int H, int E, int k, int F, int Fs, int g, int nor
  *   o_{t,j} = SwiGLU_{slot_j}(x_t) (O4) with the given full-precision weights
  *   y_t     = bf16( x_t + sh_t + Σ_{j non-empty} w_tj · o_{t,j} )   (O6)
  * Weights: gate/up [S][F][H], down [S][H][F] (real, bf16-valued); sh_* NULL if F_s == 0.
- * ids/w out: the re-routed picks ([n][k], slot or -1).
+ * ids/w out: the re-routed picks ([n][k], slot or -1).  resid (NULL = x), cond and dmag (NULL = skip)
+ * as in orc_moe_tokens (R6: r is an input; the condition terms of the O6 sum).
  * -------------------------------------------------------------------------- */
 int orc_compact_tokens(int64_t n, int H, int Er, int k, int S, int F, int Fs, int norm, const double* x,
                        const double* wr, const int32_t* remap, const double* gate, const double* up,
                        const double* down, const double* sh_gate, const double* sh_up, const double* sh_down,
-                       double* y, int32_t* ids, double* w, double* z, double* margin) {
+                       const double* resid, double* y, int32_t* ids, double* w, double* z, double* margin,
+                       double* cond, double* dmag) {
   if (S < 1) return 1;
   for (int e = 0; e < Er; ++e)
     if (remap[e] < 0 || remap[e] >= S) return 1;
@@ -402,7 +404,9 @@ int orc_compact_tokens(int64_t n, int H, int Er, int k, int S, int F, int Fs, in
   }
   double* o = (double*)calloc((size_t)n * k * H, sizeof(double)); /* o[t][j][h] */
   double* sh = (double*)calloc((size_t)n * H, sizeof(double));
-  if (!o || !sh) { free(o); free(sh); return 2; }
+  double* om = dmag ? (double*)calloc((size_t)n * k * H, sizeof(double)) : NULL;
+  double* shm = dmag ? (double*)calloc((size_t)n * H, sizeof(double)) : NULL;
+  if (!o || !sh || (dmag && (!om || !shm))) { free(o); free(sh); free(om); free(shm); return 2; }
 #pragma omp parallel for schedule(dynamic, 1)
   for (int s = 0; s < S; ++s) {
     deq_expert d = {(double*)gate + (int64_t)s * F * H, (double*)up + (int64_t)s * F * H,
@@ -410,7 +414,8 @@ int orc_compact_tokens(int64_t n, int H, int Er, int k, int S, int F, int Fs, in
     double* a = (double*)malloc(sizeof(double) * (size_t)F);
     for (int64_t t = 0; t < n; ++t)
       for (int j = 0; j < k; ++j)
-        if (ids[t * k + j] == s) swiglu_expert(H, F, &d, x + t * H, a, o + (t * k + j) * (int64_t)H, NULL);
+        if (ids[t * k + j] == s)
+          swiglu_expert(H, F, &d, x + t * H, a, o + (t * k + j) * (int64_t)H, om ? om + (t * k + j) * (int64_t)H : NULL);
     free(a);
   }
   if (Fs > 0 && sh_gate) {
@@ -418,21 +423,36 @@ int orc_compact_tokens(int64_t n, int H, int Er, int k, int S, int F, int Fs, in
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t t = 0; t < n; ++t) {
       double* a = (double*)malloc(sizeof(double) * (size_t)Fs);
-      swiglu_expert(H, Fs, &d, x + t * H, a, sh + t * H, NULL);
+      swiglu_expert(H, Fs, &d, x + t * H, a, sh + t * H, shm ? shm + t * H : NULL);
       free(a);
     }
   }
 #pragma omp parallel for schedule(static)
   for (int64_t t = 0; t < n; ++t)
     for (int h = 0; h < H; ++h) {
-      double acc = x[t * H + h];
+      const double r = resid ? resid[t * H + h] : x[t * H + h];
+      double acc = r;
       acc += sh[t * H + h];
       for (int j = 0; j < k; ++j)
         if (ids[t * k + j] >= 0) acc += w[t * k + j] * o[(t * k + j) * (int64_t)H + h];
       y[t * H + h] = orc_bf16_round(acc);
+      if (cond) {  /* as in orc_moe_tokens */
+        double m = fabs(r) + fabs(sh[t * H + h]);
+        for (int j = 0; j < k; ++j)
+          if (ids[t * k + j] >= 0) m += w[t * k + j] * fabs(o[(t * k + j) * (int64_t)H + h]);
+        cond[t * H + h] = m;
+      }
+      if (dmag) {
+        double m = shm[t * H + h];
+        for (int j = 0; j < k; ++j)
+          if (ids[t * k + j] >= 0) m += w[t * k + j] * om[(t * k + j) * (int64_t)H + h];
+        dmag[t * H + h] = m;
+      }
     }
   free(o);
   free(sh);
+  free(om);
+  free(shm);
   return 0;
 }
 

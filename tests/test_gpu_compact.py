@@ -10,6 +10,7 @@ D_e == their stable grouping; identity merges reproduce the uncompressed model b
 import numpy as np
 import pytest
 
+import oracle
 import oracle.model as om
 import synth
 
@@ -216,3 +217,44 @@ def test_adaptive_layer_sizes_end_to_end():
         for fam, W in (("gate", model.gate), ("up", model.up), ("down", model.down)):
             got = getattr(merged, fam)[l][:Cl[l]]
             assert torch.equal(got, W[l][n_tun[l]:S[l]]), (l, fam)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_compact_branch_elementwise(name):
+    """The compact model's MoE branch alone (all-zero residual, R6), layer by layer on x_0, element by
+    element against O11 with r = 0, at the bounds of tests/_parity.py (north star and arithmetic): the
+    re-routed picks, the folded weights and the merged bf16 experts are all inside y here."""
+    from _parity import BRANCH_TOL, branch_violations
+    from paper_2508_19078_b200 import synthetic
+    from paper_2508_19078_b200.driver import Profiler, compact_model
+    cfg, C, n_tun, n_sample = CASES[name]
+    co = synth.cluster_assignment(cfg, C, n_tuning=n_tun)
+    alpha = _alpha(cfg)
+    T = cfg.tokens
+    masters = synthetic.master_weights(cfg)
+    model = compact_model(masters, torch.from_numpy(alpha).cuda(), torch.from_numpy(co).cuda(), C, n_tun)
+    prof = Profiler(model.shape, T, with_de=False, with_logits=True)
+    x = synthetic.tokens(cfg, 0, T)
+    zero = torch.zeros_like(x)
+    toks = np.arange(T) if n_sample is None else np.linspace(0, T - 1, n_sample).astype(np.int64)
+    x0 = synth.bf16_bits_to_f32(synth.cpu_rows(synth.spec_x(cfg), toks)).astype(np.float64)
+    compared = 0
+    for l in range(cfg.n_layers):
+        y = prof.run_layer(model, l, x, zero).float().cpu().numpy()[toks].astype(np.float64)
+        ids = prof.ids[l].cpu().numpy()[toks]
+        logits = prof.logits[l].cpu().numpy()[toks]
+        wr, g, u, d, sh, remap = om.compact_layer(om.dense_layer(cfg, l), co[l], alpha[l].astype(np.float64))
+        yr, idr, wref, zr, mr, cond, dmag = oracle.compact_tokens(x0, wr, remap, g, u, d, sh, k=cfg.top_k,
+                                                                   norm=cfg.norm_topk, residual=np.zeros_like(x0),
+                                                                   with_cond=True)
+        for t in range(len(toks)):
+            assert np.all(np.abs(logits[t] - zr[t]) <= LOGIT_TOL * np.abs(zr[t]).max()), (l, t)
+            if mr[t] <= MARGIN:
+                continue  # a near-tie may route (validly) differently
+            assert np.array_equal(ids[t], idr[t]), (l, t, ids[t], idr[t])
+            for tight in (False, True):
+                bad = branch_violations(y[t], yr[t], cond[t], dmag[t], tight)
+                assert not bad.any(), (name, l, t, tight, np.nonzero(bad)[0][:6])
+            compared += 1
+    assert compared >= 0.8 * cfg.n_layers * len(toks)
+    assert BRANCH_TOL == 2e-2

@@ -46,6 +46,12 @@ def test_identity_remap_equals_quantized_forward():
         y_c, ids_c, w_c, _, _ = oracle.compact_tokens(x, wr, np.arange(E), *dense, k=k, norm=norm)
         assert np.array_equal(ids_q, ids_c) and np.array_equal(w_q, w_c)
         assert np.array_equal(y_q, y_c)
+        # the MoE branch alone (r = 0, R6) and its condition terms agree between the two formulations too
+        z0 = np.zeros_like(x)
+        bq = oracle.moe_tokens(x, wr, experts, None, k=k, group_size=0, norm=norm, residual=z0, with_cond=True)
+        bc = oracle.compact_tokens(x, wr, np.arange(E), *dense, k=k, norm=norm, residual=z0, with_cond=True)
+        assert np.array_equal(bq[0], bc[0]) and np.array_equal(bq[5], bc[5]) and np.array_equal(bq[6], bc[6])
+        assert not np.array_equal(bc[0], y_c)  # the residual is really gone
 
 
 def test_identical_experts_fold_to_original():
