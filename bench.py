@@ -334,6 +334,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
         clocks.start()
     F.timing_read(reset=True)
     F.timing_enable(True)
+    F.timing_clocks(reset=True)
     launches0 = F.launch_count()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -345,6 +346,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
     F.timing_enable(False)
     launches = F.launch_count() - launches0
     kern = F.timing_read(reset=True)
+    gemm_mhz = F.timing_clocks(reset=True)  # average SM clock measured inside the expert GEMMs
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -420,6 +422,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
     del x_dev, x_host, off_host, ti_host
 
     out = {"ms": ms, "ms_e2e": ms_e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "kern": kern, "clk": clk,
+           "gemm_mhz": gemm_mhz,
            "T_rank": T_rank, "Tc": Tc, "n_chunks": n_chunks, "C": C, "budget_C": [int(c) for c in state["C"]],
            "steps": steps}
 
@@ -503,7 +506,11 @@ def roofline_gemm(cfg, T_rank, res, peaks, peak_src):
             # context for power-capped runs: the dense bf16 MMA peak at the median SM clock seen under load
             # (148 SMs x 8192 FLOP/clk/SM = 2.25 PFLOP/s at 1.856 GHz)
             "peak_at_clock": (148 * 8192 * clk["sm_mhz"] * 1e6 / 1e12) if clk else None,
-            "frac_at_clock": (achieved / (148 * 8192 * clk["sm_mhz"] * 1e6 / 1e12)) if (clk and achieved) else None}
+            "frac_at_clock": (achieved / (148 * 8192 * clk["sm_mhz"] * 1e6 / 1e12)) if (clk and achieved) else None,
+            # the same against the clock measured inside the GEMM itself (%clock64 / %globaltimer, libflux)
+            "kernel_mhz": res.get("gemm_mhz", {}).get("gemm_gate_up"),
+            "frac_at_kernel_clock": (achieved / (148 * 8192 * res["gemm_mhz"]["gemm_gate_up"] * 1e6 / 1e12))
+            if (achieved and res.get("gemm_mhz", {}).get("gemm_gate_up")) else None}
 
 
 def cfg_key(cfg):

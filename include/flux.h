@@ -326,6 +326,10 @@ void flux_timing_enable(int on);
  * Returns the number of kernel kinds. */
 int flux_timing_read(double* ms_out, long long* count_out, int n, int reset);
 const char* flux_kernel_name(int kind);
+/* Average SM clock in MHz measured INSIDE the probed kernels (the CTA-pair expert GEMMs: one thread
+ * reads %clock64 and %globaltimer at the kernel's start and end) while timing is enabled, per kernel
+ * kind; 0 where nothing was probed.  Synchronises the device.  Returns the number of kernel kinds. */
+int flux_timing_clocks(double* mhz_out, int n, int reset);
 /* Text of the last CUDA error this thread's calls saw ("" if none).  With the
  * environment variable FLUX_DEBUG_SYNC=1 every launch is synchronised and a
  * failure names the kernel that raised it. */

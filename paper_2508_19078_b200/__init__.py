@@ -127,6 +127,8 @@ def _lib():
         L.flux_kernel_name.restype = ctypes.c_char_p
         L.flux_last_error.argtypes = []
         L.flux_last_error.restype = ctypes.c_char_p
+        L.flux_timing_clocks.argtypes = [P, ctypes.c_int, ctypes.c_int]
+        L.flux_timing_clocks.restype = ctypes.c_int
         L.flux_launch_count.argtypes = []
         L.flux_launch_count.restype = ctypes.c_longlong
         _L = L
@@ -145,6 +147,14 @@ def timing_read(reset: bool = True) -> dict:
     cnt = (ctypes.c_longlong * n)()
     k = _lib().flux_timing_read(ms, cnt, n, 1 if reset else 0)
     return {_lib().flux_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(k)}
+
+
+def timing_clocks(reset: bool = True) -> dict:
+    """{kernel name: average SM MHz inside the kernel} for the clock-probed kernels (the expert GEMMs)."""
+    n = 32
+    mhz = (ctypes.c_double * n)()
+    k = _lib().flux_timing_clocks(mhz, n, 1 if reset else 0)
+    return {_lib().flux_kernel_name(i).decode(): mhz[i] for i in range(k) if mhz[i] > 0}
 
 
 def launch_count() -> int:

@@ -404,6 +404,7 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
   ga.gather_idx = gather_a ? token_index : nullptr;
   ga.gather_cp = gmode == GATHER_CP ? 1 : 0;
   ga.l2_hints = pol.l2_hints;
+  ga.clk_probe = clock_probe(K_GEMM_GU);  // null unless flux_timing_enable(1)
   ga.tile_ctr = pol.dynamic_tiles ? sa.done_counter + 1 : nullptr;  // zeroed by K1
   ga.a_src = x;
   ga.a_ld = H;
@@ -411,6 +412,7 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
   gd.gather_idx = nullptr;  // the down GEMM reads act, materialised in permuted order by K3
   gd.gather_cp = 0;
   gd.tile_ctr = ga.tile_ctr ? sa.done_counter + 2 : nullptr;
+  gd.clk_probe = clock_probe(K_GEMM_DN);
   gd.sched = sa.sched_dn;
   gd.n_tiles_r = sa.n_tiles_dn;
   gd.n_tiles_s = sa.n_tiles_dn_sh;

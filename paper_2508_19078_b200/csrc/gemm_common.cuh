@@ -36,6 +36,7 @@ struct Params {
   int a_ld;
   int l2_hints;                // GemmArgs::l2_hints
   int32_t* tile_ctr;           // GemmArgs::tile_ctr
+  unsigned long long* clk_probe;  // GemmArgs::clk_probe
 };
 
 struct TileInfo {
@@ -382,6 +383,7 @@ inline Params make_params(const GemmArgs& g) {
   p.gather_cp = g.gather_cp;
   p.a_src = reinterpret_cast<const __nv_bfloat16*>(g.a_src);
   p.a_ld = g.a_ld;
+  p.clk_probe = g.clk_probe;
   p.l2_hints = g.l2_hints;
   p.tile_ctr = g.tile_ctr;
   return p;

@@ -189,6 +189,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
   uint64_t* tid_empty = tid_full + kTileSlots;  // [kTileSlots], the leader's are the ones used
   int32_t* s_tid = reinterpret_cast<int32_t*>(tid_empty + kTileSlots);  // [kTileSlots]
 
+  ClockProbe probe;
+  probe.start(p.clk_probe);
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -462,6 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
   tc_fence_before();
   cluster_sync();
   if (warp == 2) tmem_dealloc_pair<512>(tmem);
+  probe.stop(p.clk_probe);
 }
 }  // namespace
 

@@ -40,6 +40,8 @@ class KernelTimer {
 };
 
 void set_last_error(const char* what, cudaError_t e);
+// Device slots [Σ clocks, Σ ns] of kernel kind `kind` while timing is enabled, else null (timing.cpp).
+unsigned long long* clock_probe(int kind);
 const char* last_error();
 
 // ---------------------------------------------------------------- launchers
@@ -182,6 +184,7 @@ struct GemmArgs {
   int32_t* tile_ctr;  // CTA-pair kernels: zeroed int the pair leaders claim tiles from (null = static)
   int l2_hints;  // L2 cache policies of the CTA-pair pass kernel: bit 0 = evict_first on the output
                  // stores, bit 1 = evict_last on the B loads, bit 2 = evict_first on the A loads
+  unsigned long long* clk_probe;  // diagnostics: [Σ SM clocks, Σ ns] of this launch added by CTA 0 (or null)
 };
 cudaError_t launch_gemm(GemmEpi epi, const CUtensorMap& a_r, const CUtensorMap& a_s, const CUtensorMap& b_r,
                         const CUtensorMap& b_s, const GemmArgs& a, cudaStream_t st);

@@ -407,4 +407,20 @@ __device__ __forceinline__ float2 add2_rn(float2 a, float2 b) {
   return d;
 }
 
+// Clock probe (diagnostics): thread 0 of block 0 adds this kernel's SM clocks and nanoseconds.
+struct ClockProbe {
+  unsigned long long c0 = 0, t0 = 0;
+  __device__ __forceinline__ void start(const unsigned long long* probe) {
+    if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
+      c0 = clock64();
+      t0 = globaltimer_ns();
+    }
+  }
+  __device__ __forceinline__ void stop(unsigned long long* probe) {
+    if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicAdd(probe, (unsigned long long)clock64() - c0);
+      atomicAdd(probe + 1, globaltimer_ns() - t0);
+    }
+  }
+};
 }  // namespace flux

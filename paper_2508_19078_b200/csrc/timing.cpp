@@ -30,6 +30,7 @@ std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_pool;
 double g_ms[FLUX_NUM_KERNELS] = {0};
 long long g_cnt[FLUX_NUM_KERNELS] = {0};
+unsigned long long* g_probe = nullptr;  // device [FLUX_NUM_KERNELS][2]: Σ SM clocks, Σ ns inside probed kernels
 
 cudaEvent_t get_event() {
   if (!g_pool.empty()) {
@@ -76,6 +77,16 @@ KernelTimer::~KernelTimer() {
   g_pending.push_back({kind_, a_, b_});
 }
 
+unsigned long long* clock_probe(int kind) {
+  if (!g_enabled.load(std::memory_order_relaxed)) return nullptr;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_probe) {
+    if (cudaMalloc(&g_probe, sizeof(unsigned long long) * 2 * FLUX_NUM_KERNELS) != cudaSuccess) return nullptr;
+    cudaMemset(g_probe, 0, sizeof(unsigned long long) * 2 * FLUX_NUM_KERNELS);
+  }
+  return g_probe + 2 * kind;
+}
+
 void set_last_error(const char* what, cudaError_t e) {
   snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, cudaGetErrorString(e));
 }
@@ -114,6 +125,21 @@ int flux_timing_read(double* ms_out, long long* count_out, int n, int reset) {
       g_ms[i] = 0;
       g_cnt[i] = 0;
     }
+  return FLUX_NUM_KERNELS;
+}
+
+// Average SM clock (MHz) inside the probed kernels (the CTA-pair GEMMs) since the last reset: one thread
+// of CTA 0 reads %clock64 and %globaltimer at the kernel's start and end.  0 where nothing was probed.
+int flux_timing_clocks(double* mhz_out, int n, int reset) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  unsigned long long h[2 * FLUX_NUM_KERNELS] = {0};
+  if (g_probe) {
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, g_probe, sizeof(h), cudaMemcpyDeviceToHost);
+    if (reset) cudaMemset(g_probe, 0, sizeof(h));
+  }
+  for (int i = 0; i < n && i < FLUX_NUM_KERNELS; ++i)
+    mhz_out[i] = h[2 * i + 1] ? 1e3 * (double)h[2 * i] / (double)h[2 * i + 1] : 0.0;
   return FLUX_NUM_KERNELS;
 }
 
