@@ -181,8 +181,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsOf<EPI>, 1)
   int32_t* s_sched = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 256);
   int32_t* s_row0 = s_sched + kMaxGroups;
   int32_t* s_rows = s_row0 + kMaxGroups;
-  int32_t* s_idx =  // [128] gathered token ids, 16-byte aligned
-      reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(s_rows + kMaxGroups) + 15) & ~uintptr_t(15));
+  // [128] gathered token ids, 16-byte aligned: byte 256 + 4·(3·kMaxGroups + 1) = 3344 past the 1 KB-aligned
+  // ring end (pointer arithmetic on the shared array keeps LDS/STS instead of generic accesses)
+  static_assert((256 + 4 * (3 * kMaxGroups + 1)) % 16 == 0, "s_idx alignment");
+  int32_t* s_idx = s_rows + kMaxGroups + 1;
   float* s_scales = reinterpret_cast<float*>(s_idx + 128);  // [2][kScaleFloats] (stage_tile_scales)
   uint8_t* s_out = smem + kStages * kStageBytes + kMiscBytes;  // [4 warps][kStageOutBytes]
   uint64_t* tid_full = reinterpret_cast<uint64_t*>(s_out + 4 * kStageOutBytes + 4 * kPickBytes);  // [kTileSlots]

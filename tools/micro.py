@@ -112,14 +112,15 @@ def layer(name="deepseek_moe"):
     qm = QuantizedModel(shape)
     qm.quantize_from(synthetic.master_weights(cfg))
     chain = int(os.environ.get("MICRO_CHAIN", "0"))  # flux_policy.gemm_chain (0 auto, 1 off, 2 on)
-    prof = Profiler(shape, cfg.tokens, with_de=True, policy=F.make_policy(gemm_chain=chain))
+    wp = int(os.environ.get("MICRO_WP", "0"))  # flux_policy.weight_path (0 auto, 1 dequant pass, 2 in-GEMM)
+    prof = Profiler(shape, cfg.tokens, with_de=True, policy=F.make_policy(weight_path=wp, gemm_chain=chain))
     x = synthetic.tokens(cfg, 0, cfg.tokens)
     F.timing_read(reset=True)
     F.timing_enable(True)
     ms = timed(lambda: prof.run(qm, x), reps=5, warm=2)
     F.timing_enable(False)
     k = F.timing_read(reset=True)
-    print(f"one {name} layer, {cfg.tokens} tokens, chain={chain}: {ms:.2f} ms;",
+    print(f"one {name} layer, {cfg.tokens} tokens, weight_path={wp} chain={chain}: {ms:.2f} ms;",
           {n: round(v[0] / max(v[1], 1), 3) for n, v in k.items() if v[1]})
 
 
