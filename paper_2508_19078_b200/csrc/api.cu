@@ -115,7 +115,8 @@ static flux_status validate_policy(const flux_policy* u) {
   if (!u) return FLUX_OK;
   if (u->weight_path < 0 || u->weight_path > 2 || u->routed_rows < 0 || u->routed_rows > 2 ||
       (u->fused_combine != 0 && u->fused_combine != 1) || (u->static_tiles != 0 && u->static_tiles != 1) ||
-      (u->l2_hints != 0 && (u->l2_hints & ~(FLUX_L2_SET | 7)) != 0) || u->gemm_chain < 0 || u->gemm_chain > 2)
+      (u->l2_hints != 0 && (!(u->l2_hints & FLUX_L2_SET) || (u->l2_hints & ~(FLUX_L2_SET | 7)) != 0)) ||
+      u->gemm_chain < 0 || u->gemm_chain > 2)
     return FLUX_E_INVALID;
   return FLUX_OK;
 }

@@ -83,3 +83,48 @@ def test_budget_host_matches_oracle(F):
         C, over = F.layer_budget(hist, T, B_non, n_non)
         Cr, _, _, over_r = oracle.layer_budget(hist, T, B_non, n_non)
         assert np.array_equal(C, Cr) and over == over_r
+
+
+def test_policy_and_batch_validation_without_gpu(F):
+    """flux_policy values are validated on the host (before any launch) and change the workspace only
+    through the paths they select; flux_merge_experts_batch validates every job on the host."""
+    L = F.lib()
+    cfg = F.make_cfg(2048, 1408, 64, 6, 2816, 4, 128, 0)
+    T = 262144
+    ws_default = L.flux_profile_layer_workspace(ctypes.byref(cfg), T)
+    assert ws_default > 0
+    assert L.flux_profile_layer_workspace_ex(ctypes.byref(cfg), None, T) == ws_default
+    assert L.flux_profile_layer_workspace_ex(ctypes.byref(cfg), ctypes.byref(F.make_policy()), T) == ws_default
+    # the materialised routed rows need x_perm (T·k·H·2 bytes more); the in-GEMM dequant materialises the
+    # rows too but needs no bf16 B copies (E·3·F·H + 3·F_s·H bf16 weights)
+    mat = L.flux_profile_layer_workspace_ex(ctypes.byref(cfg), ctypes.byref(F.make_policy(routed_rows=1)), T)
+    assert mat - ws_default >= 2 * T * 6 * 2048
+    ing = L.flux_profile_layer_workspace_ex(ctypes.byref(cfg), ctypes.byref(F.make_policy(weight_path=2)), T)
+    assert mat - ing >= 2 * (64 * 3 * 1408 + 3 * 2816) * 2048
+    chain = L.flux_profile_layer_workspace_ex(ctypes.byref(cfg), ctypes.byref(F.make_policy(gemm_chain=2)), T)
+    assert chain > ws_default  # chained GEMMs: m-tile ready flags and prefixes
+    for bad in (F.make_policy(weight_path=3), F.make_policy(routed_rows=-1), F.make_policy(fused_combine=2),
+                F.make_policy(static_tiles=5), F.make_policy(l2_hints=3), F.make_policy(gemm_chain=7)):
+        assert L.flux_profile_layer_workspace_ex(ctypes.byref(cfg), ctypes.byref(bad), T) == 0
+        out, ql = F.LayerOut(), F.QLayer()
+        assert L.flux_profile_layer_ex(ctypes.byref(cfg), ctypes.byref(bad), ctypes.byref(ql), None, None, 10,
+                                       ctypes.byref(out), None, 0, None) == F.FLUX_E_INVALID
+    assert L.flux_profile_layer_workspace_ex(ctypes.byref(cfg), ctypes.byref(F.make_policy(l2_hints=F.L2_SET | 5)),
+                                             T) == ws_default
+    # batch merge: counts, numel % 8, null pointers, C > E, compact slot bounds
+    jobs = (F.MergeJob * 2)()
+    assert L.flux_merge_experts_batch(0, 4, 16, 0, None, 0, None) == F.FLUX_OK  # nothing to do
+    assert L.flux_merge_experts_batch(0, 4, 16, 2, None, 0, None) == F.FLUX_E_INVALID
+    assert L.flux_merge_experts_batch(0, 4, 12, 2, ctypes.cast(jobs, ctypes.c_void_p), 0, None) == F.FLUX_E_UNSUPPORTED
+    assert L.flux_merge_experts_batch(0, 4, 16, 2, ctypes.cast(jobs, ctypes.c_void_p), 0, None) == F.FLUX_E_INVALID
+    assert L.flux_merge_experts_batch(0, 4, 16, 257, ctypes.cast(jobs, ctypes.c_void_p), 0, None) == F.FLUX_E_INVALID
+    buf = (ctypes.c_uint8 * 64)()
+    p = ctypes.addressof(buf) + (-ctypes.addressof(buf)) % 16  # 16-byte aligned host address (not touched)
+    for j in jobs:
+        j.experts = j.cluster_of = j.alpha = j.out = p
+        j.n_clusters = 5  # > E
+    assert L.flux_merge_experts_batch(0, 4, 16, 2, ctypes.cast(jobs, ctypes.c_void_p), 0, None) == F.FLUX_E_INVALID
+    for j in jobs:
+        j.n_clusters, j.n_tuning = 3, 2  # compact: n_tuning + C > E
+    assert L.flux_merge_experts_batch(0, 4, 16, 2, ctypes.cast(jobs, ctypes.c_void_p), 1, None) == F.FLUX_E_INVALID
+    assert L.flux_merge_experts_batch(0, 4, 16, 2, ctypes.cast(jobs, ctypes.c_void_p), 2, None) == F.FLUX_E_INVALID
