@@ -523,6 +523,11 @@ def kernel_table(cfg, res, peaks):
     hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
     steps = res["steps"]
     by = kernel_bytes(cfg, res["T_rank"], res["C"], res["n_chunks"])
+    # DRAM read + write bytes per launch from the committed `ncu --set full` captures (profiles/traffic.json)
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic = json.load(open(tp)) if os.path.exists(tp) else {}
+    ncu_label = {"router": "K1 router", "permute": "K2 permute (one kernel)", "gemm_gate_up": "K3/K5 gate/up GEMM (pair)",
+                 "gemm_down": "K4/K5 down GEMM (pair)", "combine": "K6 combine"}
     out = {}
     for n, (ms_tot, cnt) in res["kern"].items():
         if not cnt:
@@ -531,6 +536,11 @@ def kernel_table(cfg, res, peaks):
         if n in by and ms_tot > 0:
             gbs = by[n] / (ms_tot / steps / 1e3) / 1e9
             d.update(bytes_per_step=by[n], gbs=gbs, frac_hbm_measured=gbs / hbm, frac_hbm_8tbs=gbs / SPEC_HBM_GBS)
+        t = traffic.get(f"{cfg_key(cfg)}:{res['Tc']}:{ncu_label.get(n, '')}")
+        if t:
+            d["ncu_dram_bytes_per_launch"] = t
+            if n in by:
+                d["ncu_dram_vs_algorithmic"] = t / (by[n] / (cnt / steps))
         out[n] = d
     return out
 
