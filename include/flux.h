@@ -50,9 +50,10 @@ const char* flux_status_string(flux_status s);
 /* ============================================================================
  * Model shape of one MoE layer (Table 1).
  * Supported: hidden % 64 == 0; ffn % 16 == 0 (and shared_ffn); 1 <= top_k <= 8,
- * top_k <= n_experts <= 128; wbits in {4, 8}; group_size == 0 (per output channel) or
- * a multiple of 64 dividing both hidden and ffn (and shared_ffn); INT4 needs
- * every packed row to be a multiple of 16 B (hidden % 32 == 0, ffn % 32 == 0).
+ * top_k <= n_experts <= 128; wbits in {2, 4, 8, 16}; group_size == 0 (per output channel)
+ * or a multiple of 64 dividing both hidden and ffn (and shared_ffn); INT4 needs every
+ * packed row to be a multiple of 16 B (hidden % 32 == 0, ffn % 32 == 0), INT2 hidden, ffn
+ * and shared_ffn % 64 == 0.  (SURVEY §8(b) allowed E <= 256; the BASELINE configs need <= 64.)
  * ========================================================================== */
 typedef struct {
   int32_t hidden;     /* H                                                    */
@@ -131,7 +132,7 @@ enum {
 };
 #define FLUX_L2_SET 0x100         /* l2_hints = FLUX_L2_SET | bits overrides the default (bits 1) */
 enum {
-  FLUX_CHAIN_AUTO = 0,            /* the measured default                          */
+  FLUX_CHAIN_AUTO = 0,            /* the measured default: two launches               */
   FLUX_CHAIN_OFF = 1,             /* gate/up and down GEMMs as two launches (act round-trips through HBM) */
   FLUX_CHAIN_ON = 2               /* TEST-ONLY: one persistent launch, each m-tile's down tiles 24 m-tiles
                                      behind its gate/up tiles (dequant-pass path with the in-GEMM gather,
