@@ -275,9 +275,8 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
     cluster_of = torch.from_numpy(synth.cluster_assignment(cfg, C)).cuda()
     d_feat = feature_dim(E)
     alpha = torch.empty(L, E, dtype=torch.float32, device="cuda")
-    alpha_host = torch.empty(L, E, dtype=torch.float32).pin_memory()
     hist_host = torch.empty(L, E, dtype=torch.int64).pin_memory()
-    ahist_host = torch.empty(L, E, dtype=torch.int64).pin_memory()
+    ev_hist = torch.cuda.Event()
     attn = synthetic.attention_values(cfg, t0, T_rank) if args.alpha == "attn" else None
     if attn is not None and n_chunks > 1:
         raise SystemExit("--alpha attn needs one chunk per rank")
@@ -290,6 +289,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
     comm = F.Comm(uid, world, rank)
 
     def step(xs, before_chunk=None, after_chunk=None):
+        report_budgets()                                          # the previous round's eq.(1), host side
         if args.clustering == "pca":                              # §5.2 C1 (reads the masters only)
             feats, _, _ = expert_features_model(masters, d_feat)
         qm.quantize_from(masters)                                 # a0
@@ -301,23 +301,31 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
             if after_chunk:
                 after_chunk(c)
         comm.reduce_stats(prof.hist)                              # a7
-        if attn is not None:                                      # NEXT-3: Σ_{t∈D_e} a_t, fixed point
+        if attn is None:                                          # α = f = hist / T, on the device
+            F.frequencies(prof.hist, float(T_total), alpha)
+        else:                                                     # NEXT-3: α = f·ā = Σ_{t∈D_e} a_t / T (R15)
             comm.reduce_stats(prof.ahist)
-            ahist_host.copy_(prof.ahist, non_blocking=True)
-        hist_host.copy_(prof.hist, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        h = hist_host.numpy()
-        Cl, _ = budgets(h, T_total, C * L)                        # a8-pre, eq.(1)
-        n_cl = [int(c) for c in Cl] if args.budget == "adaptive" else C
-        state["C"] = Cl
+            F.frequencies(prof.ahist, 16777216.0 * T_total, alpha)
+        hist_host.copy_(prof.hist, non_blocking=True)             # the round's statistics leave the device
+        ev_hist.record(stream)
+        if args.budget == "adaptive":                             # a8-pre, eq.(1) budgets drive this round
+            ev_hist.synchronize()
+            Cl, _ = budgets(hist_host.numpy(), T_total, C * L)
+            state["C"] = Cl
+            n_cl = [int(c) for c in Cl]
+        else:                                                     # uniform C (BASELINE configs[3]): eq.(1)
+            n_cl = C                                              # on the host, off the GPU's critical path
+            state["hist_pending"] = True
         if args.clustering == "pca":                              # §5.2 C2: K-Means from the reduced counts
             state["cluster_of"] = cluster_model(feats, prof.hist, n_cl)
-        if attn is None:
-            alpha_host.copy_(torch.from_numpy((h / float(T_total)).astype(np.float32)))  # α = f
-        else:  # α = f·ā = Σ_{t∈D_e} a_t / T (eq.(2); R15)
-            alpha_host.copy_(torch.from_numpy((ahist_host.numpy() / (16777216.0 * T_total)).astype(np.float32)))
-        alpha.copy_(alpha_host, non_blocking=True)
         state["merged"] = merge_model(masters, alpha, state["cluster_of"], n_cl, state["merged"])  # a8, eq.(2)
+
+    def report_budgets():
+        """a8-pre, eq.(1) on the host from the last round's reduced histogram (uniform mode: the report)."""
+        if state.get("hist_pending"):
+            ev_hist.synchronize()
+            state["C"], _ = budgets(hist_host.numpy(), T_total, C * L)
+            state["hist_pending"] = False
 
     def barrier():
         if world > 1:
@@ -421,6 +429,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
         ms_e2e = float(t.item())
     del x_dev, x_host, off_host, ti_host
 
+    report_budgets()
     out = {"ms": ms, "ms_e2e": ms_e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "kern": kern, "clk": clk,
            "gemm_mhz": gemm_mhz,
            "T_rank": T_rank, "Tc": Tc, "n_chunks": n_chunks, "C": C, "budget_C": [int(c) for c in state["C"]],

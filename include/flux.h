@@ -283,6 +283,12 @@ flux_status flux_cluster_experts(int32_t n_layers, int32_t n_experts, int32_t d,
 flux_status flux_attention_hist(int64_t T, int32_t top_k, int32_t n_experts, const int32_t* ids, const float* attn,
                                 int64_t* attn_hist, void* stream);
 
+/* The merge importance on the device: alpha[i] = fl32(counts[i] / denom) (fp64 quotient, one rounding)
+ * — the activation frequency f = count / T (denom = T_total) or α = f·ā = A / (2^24·T)
+ * (denom = 2^24·T_total, reading R15).  counts: device int64 [n]; alpha: device fp32 [n]; denom > 0.
+ * Lets a round go from the reduced statistics to the merge without a host round trip. */
+flux_status flux_frequencies(int64_t n, const int64_t* counts, double denom, float* alpha, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Statistics all-reduce over the GPUs of one box (NCCL over NVLink/NVSwitch).
  * The counts are additive integers, so the reduced histogram equals the

@@ -101,6 +101,7 @@ def _lib():
         L.flux_compact_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
         L.flux_merge_experts_batch.argtypes = [ctypes.c_int, I32, I64, I32, P, I32, P]
         L.flux_attention_hist.argtypes = [I64, I32, I32, P, P, P, P]
+        L.flux_frequencies.argtypes = [I64, P, ctypes.c_double, P, P]
         L.flux_output_error_workspace.argtypes = []
         L.flux_output_error_workspace.restype = SZ
         L.flux_output_error.argtypes = [I64, I32, P, P, P, P, SZ, P]
@@ -115,7 +116,7 @@ def _lib():
         L.flux_comm_destroy.argtypes = [P]
         for f in ("flux_profile_layer", "flux_profile_layer_ex", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
                   "flux_expert_features", "flux_cluster_experts", "flux_compact_experts", "flux_output_error",
-                  "flux_merge_experts_batch",
+                  "flux_merge_experts_batch", "flux_frequencies",
                   "flux_attention_hist",
                   "flux_comm_unique_id", "flux_comm_init", "flux_reduce_stats", "flux_comm_destroy"):
             getattr(L, f).restype = ctypes.c_int
@@ -246,6 +247,13 @@ def compact_experts(experts, cluster_of, alpha, n_clusters: int, compact, remap=
     st = _lib().flux_compact_experts(dt, E, numel, _ptr(experts), _ptr(cluster_of), _ptr(alpha), n_clusters,
                                      _ptr(compact), _ptr(remap), _stream(stream))
     _check(st, "flux_compact_experts")
+
+
+def frequencies(counts, denom: float, alpha, stream=None):
+    """alpha = fl32(counts / denom) on the device (flux_frequencies): f = hist / T, or α = A / (2^24·T)."""
+    assert counts.dtype == torch.int64 and alpha.dtype == torch.float32 and counts.numel() == alpha.numel()
+    st = _lib().flux_frequencies(counts.numel(), _ptr(counts), float(denom), _ptr(alpha), _stream(stream))
+    _check(st, "flux_frequencies")
 
 
 def attention_hist(ids, attn, n_experts: int, out, stream=None):

@@ -653,6 +653,18 @@ flux_status flux_attention_hist(int64_t T, int32_t top_k, int32_t n_experts, con
   return cuda_status(e);
 }
 
+flux_status flux_frequencies(int64_t n, const int64_t* counts, double denom, float* alpha, void* stream) {
+  if (n < 0 || !(denom > 0.0)) return FLUX_E_INVALID;
+  if (n == 0) return FLUX_OK;
+  if (!counts || !alpha) return FLUX_E_INVALID;
+  flux_status st = check_device();
+  if (st != FLUX_OK) return st;
+  KernelTimer kt(K_FREQ, (cudaStream_t)stream);
+  cudaError_t e = launch_frequencies(n, counts, denom, alpha, (cudaStream_t)stream);
+  if (e != cudaSuccess) set_last_error("frequencies", e);
+  return cuda_status(e);
+}
+
 size_t flux_output_error_workspace(void) { return cosine_workspace(); }
 
 flux_status flux_output_error(int64_t T, int32_t hidden, const void* a, const void* b, double* result, void* ws,

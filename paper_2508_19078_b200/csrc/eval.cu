@@ -86,7 +86,22 @@ __global__ void __launch_bounds__(256) attention_hist_kernel(int64_t T, int k, i
   for (int e = threadIdx.x; e < E; e += blockDim.x)
     if (acc[e]) atomicAdd(&A[e], acc[e]);
 }
+// α_e = fl32(count_e / denom) (fp64 quotient, one rounding): the activation frequency f = count / T
+// (denom = T) or the attention-weighted α = A / (2^24·T) (R15), on the device, so a
+// participant round needs no host round trip between the reduced statistics and the merge.
+__global__ void __launch_bounds__(256) frequencies_kernel(int64_t n, const int64_t* __restrict__ counts, double denom,
+                                                          float* __restrict__ alpha) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    alpha[i] = __double2float_rn((double)counts[i] / denom);
+}
 }  // namespace
+
+cudaError_t launch_frequencies(int64_t n, const int64_t* counts, double denom, float* alpha, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, kNumSMs);
+  frequencies_kernel<<<grid, 256, 0, st>>>(n, counts, denom, alpha);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_attention_hist(int64_t T, int k, int E, const int32_t* ids, const float* attn, int64_t* A,
                                   cudaStream_t st) {

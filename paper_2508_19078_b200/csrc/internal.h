@@ -23,7 +23,7 @@ inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_O
 // ---------------------------------------------------------------- per-kernel timing (timing.cpp)
 enum KernelKind {
   K_QUANTIZE = 0, K_DEQUANT, K_ROUTER, K_PERMUTE, K_SCATTER, K_GEMM_GU, K_GEMM_DN, K_COMBINE, K_MERGE,
-  K_GEMM_DN_SH_COMBINE, K_GEMM_CHAIN, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, K_COSINE, K_ATTN_HIST, FLUX_NUM_KERNELS
+  K_GEMM_DN_SH_COMBINE, K_GEMM_CHAIN, K_GRAM, K_GRAM_REDUCE, K_EIG, K_KMEANS, K_COSINE, K_ATTN_HIST, K_FREQ, FLUX_NUM_KERNELS
 };
 // RAII: counts one launch; when timing is enabled records CUDA events around it on `st`.
 class KernelTimer {
@@ -72,6 +72,7 @@ cudaError_t launch_merge(bool fp32, int E, int64_t numel, const void* experts, c
 cudaError_t launch_attention_hist(int64_t T, int k, int E, const int32_t* ids, const float* attn, int64_t* A,
                                   cudaStream_t st);
 size_t cosine_workspace();
+cudaError_t launch_frequencies(int64_t n, const int64_t* counts, double denom, float* alpha, cudaStream_t st);
 cudaError_t launch_cosine_distance(int64_t T, int H, const void* a, const void* b, double* ws, double* out,
                                    cudaStream_t st);
 

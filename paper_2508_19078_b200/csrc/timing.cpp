@@ -15,7 +15,7 @@ static const char* kernel_name(int kind) {
   static const char* names[FLUX_NUM_KERNELS] = {"quantize", "dequant", "router", "permute", "scatter",
                                                 "gemm_gate_up", "gemm_down", "combine", "merge",
                                                 "gemm_down_shared_combine", "gemm_chain", "gram", "gram_reduce", "eig",
-                                                "kmeans", "cosine_distance", "attention_hist"};
+                                                "kmeans", "cosine_distance", "attention_hist", "frequencies"};
   return kind >= 0 && kind < FLUX_NUM_KERNELS ? names[kind] : "?";
 }
 namespace {

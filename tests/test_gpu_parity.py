@@ -350,3 +350,16 @@ def test_attention_weighted_alpha_through_the_profile(name):
         assert np.array_equal(A_gpu, oracle.attention_hist(ids_gpu, a_ref, cfg.n_experts))
         if np.array_equal(np.sort(ids_gpu, 1), np.sort(ref[l]["ids"], 1)):
             assert np.array_equal(A_gpu, oracle.attention_hist(ref[l]["ids"], a_ref, cfg.n_experts))
+
+
+def test_frequencies_bit_exact():
+    """flux_frequencies: α = fl32(count / denom) with the fp64 quotient — exactly numpy's
+    (count / denom).astype(float32), for f = hist / T (P:296-298) and α = A / (2^24·T) (R15)."""
+    import paper_2508_19078_b200 as F
+    rng = np.random.default_rng(23)
+    for n, hi in ((1, 10), (28 * 64, 262144 * 6), (5000, 2 ** 50)):
+        counts = rng.integers(0, hi, n).astype(np.int64)
+        for denom in (262144.0, 2097152.0, 16777216.0 * 262144, 3.0):
+            a = torch.empty(n, dtype=torch.float32, device="cuda")
+            F.frequencies(torch.from_numpy(counts).cuda(), denom, a)
+            assert np.array_equal(a.cpu().numpy(), (counts / denom).astype(np.float32)), (n, denom)
