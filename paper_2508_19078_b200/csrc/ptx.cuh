@@ -57,15 +57,28 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// The same with a suspend-time hint: a thread whose phase is not complete is suspended (issuing
+// nothing) until the phase completes or ~1 ms passes, instead of spinning through try_wait.
+__device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 // Blocking phase wait.  A wait that has not completed after 10 s can only be a
-// deadlock: trap, so the launch fails loudly instead of hanging the GPU.
+// deadlock: trap, so the launch fails loudly instead of hanging the GPU.  Waiting warps are
+// suspended by the hardware (no spin loop competing for issue slots and power with the warps
+// that work; ncu had counted ~12 instructions per spin iteration of the old loop).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = globaltimer_ns();
-  uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 0x3FF) == 0 && globaltimer_ns() - t0 > 10000000000ull) __trap();
-  }
+  while (!mbar_try_wait_suspend(bar, parity))
+    if (globaltimer_ns() - t0 > 10000000000ull) __trap();
 }
 
 // Same, with cluster-scope acquire: for phases completed by arrivals of the peer CTA.
@@ -83,9 +96,17 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t pa
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait_cluster(bar, parity)) return;
   const uint64_t t0 = globaltimer_ns();
-  uint32_t n = 0;
-  while (!mbar_try_wait_cluster(bar, parity)) {
-    if ((++n & 0x3FF) == 0 && globaltimer_ns() - t0 > 10000000000ull) __trap();
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (ok) return;
+    if (globaltimer_ns() - t0 > 10000000000ull) __trap();
   }
 }
 
