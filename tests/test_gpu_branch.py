@@ -61,7 +61,9 @@ def _host(dev, toks):
                 y=y[t].float().cpu().numpy().astype(np.float64))
 
 
-ALL = {**SMALL, **EDGE}
+# the largest supported routing: E = 128 experts (router N = 128, all 512 TMEM columns), top-8, INT4 g64
+MAXED = {"e128_k8": synth.MoEConfig("e128_k8", 2, 128, 128, 8, 128, 128, 4, 64, 0, 900, S + 33)}
+ALL = {**SMALL, **EDGE, **MAXED}
 
 
 @pytest.mark.parametrize("name", list(ALL))
