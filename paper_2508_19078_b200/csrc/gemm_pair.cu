@@ -1,12 +1,14 @@
 // gemm_pair.cu — K3/K4/K5 grouped expert GEMMs on CTA pairs (tcgen05 cta_group::2).
 //
-// Same math and tile schedule semantics as gemm.cu, but each tile is 256 rows
+// The expert FFNs of the quantized MoE model as grouped GEMMs: gate/up with the SwiGLU
+// epilogue (act = bf16(SiLU(x·ŵgᵀ)·(x·ŵuᵀ)), R4) and down (o = bf16(act·ŵdᵀ)); groups 0..E-1 are the
+// routed experts (A rows = the expert's D_e segment), group E the shared MLP (R5).  Each tile is 256 rows
 // x 256 output columns computed by a cluster of two CTAs on the two SMs of a
 // TPC: every CTA TMA-loads its own 128 A rows and its half (128 rows) of the
 // 256-row B tile per 64-wide K slice; the leader CTA issues
 // tcgen05.mma.cta_group::2 (M=256, N=256, K=16), which reads A and B from both
 // CTAs' shared memory and writes each CTA's 128 accumulator rows to its own
-// TMEM.  Versus the 1-CTA kernel this cuts the shared-memory operand traffic
+// TMEM.  Versus a 1-CTA M=128 kernel (round 1, removed) this cuts the shared-memory operand traffic
 // per MMA FLOP by a third (each SM stages 32 KB per K slice instead of 48 KB).
 //
 // Warp roles (per CTA): 0 = TMA producer (B halves; A when it comes by TMA), 1 = MMA issuer

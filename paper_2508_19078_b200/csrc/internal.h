@@ -149,7 +149,7 @@ cudaError_t launch_combine(int64_t T, int H, int k, const void* residual, const 
                            const float* w, const int32_t* inv_pos, void* y, cudaStream_t st,
                            bool empty_picks = false);
 
-// K3/K4/K5 (gemm.cu)
+// K3/K4/K5 (gemm_pair.cu, gemm_chain.cu; the dequant pass in dequant.cu)
 enum GemmEpi { EPI_SWIGLU = 0, EPI_STORE = 1, EPI_COMBINE = 2 };
 struct GemmArgs {
   // groups 0..E-1: routed experts (A = tm_a_r rows grp_row0.., B = tm_b_r rows g*b_rows_r..);
