@@ -3,6 +3,7 @@
 
 usage: python tools/ncu_summary.py launches <launches.csv> <out.md>
        python tools/ncu_summary.py full <report.ncu-rep> <out.md> [traffic.json key-prefix]
+       python tools/ncu_summary.py conflicts <out.md> <report.ncu-rep>...
 """
 import collections
 import csv
@@ -102,8 +103,62 @@ def full(path, out, traffic_prefix=None):
     return traffic
 
 
+def conflicts(out, paths):
+    """Per-kernel shared-memory wavefronts attributed to SASS instructions (source page: actual vs
+    ideal per instruction) beside the kernel-level l1tex bank-conflict counter, which also counts
+    LSU accesses delayed by the async proxy (TMA writes, tcgen05.mma operand reads) on the same banks."""
+    lines = ["# Shared-memory bank conflicts — per instruction vs kernel counter", "",
+             "`ncu --page source --print-source sass`: for every SASS instruction with shared wavefronts, "
+             "`L1 Wavefronts Shared` (actual) vs `L1 Wavefronts Shared Ideal`; excess = actual − ideal is "
+             "what the instruction's own address pattern costs. The kernel-level "
+             "`l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum` is from the raw page of the same report.", ""]
+    for path in paths:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rr = list(csv.reader(io.StringIO(raw)))
+        counters = {}
+        for r in rr[2:]:
+            d = dict(zip(rr[0], r))
+            get = lambda k: next((v for h, v in d.items() if h == k or h.endswith("." + k)), "?")
+            counters.setdefault(label(d.get("Kernel Name", "?")), (get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+                                                                  get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")))
+        src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                             capture_output=True, text=True).stdout
+        kern, hdr, per = None, None, collections.OrderedDict()
+        for row in csv.reader(io.StringIO(src)):
+            if row and row[0] == "Kernel Name":
+                kern, hdr = row[1], None
+                continue
+            if row and row[0] == "Address":
+                hdr = row
+                continue
+            if hdr is None or len(row) < len(hdr):
+                continue
+            d = dict(zip(hdr, row))
+            try:
+                w = float(d["L1 Wavefronts Shared"] or 0)
+                ideal = float(d["L1 Wavefronts Shared Ideal"] or 0)
+            except (KeyError, ValueError):
+                continue
+            if w > 0:  # one launch per kernel name: later duplicates of an address are other launches
+                per.setdefault(kern, {}).setdefault(d["Address"], (w, ideal, d["Source"].strip()))
+        lines += [f"## {path.split('/')[-1]}", "", "| kernel | counter conflicts / wavefronts | instr. wavefronts | ideal | excess | top excess instruction |",
+                  "|---|---|---:|---:|---:|---|"]
+        for k, v in per.items():
+            v = list(v.values())
+            w, ideal = sum(x[0] for x in v), sum(x[1] for x in v)
+            top = max(v, key=lambda x: x[0] - x[1])
+            c = counters.get(label(k), ("?", "?"))
+            top_s = f"`{top[2][:48]}` ({top[0] - top[1]:.0f})" if top[0] > top[1] else "—"
+            lines.append(f"| {label(k)} | {c[0]} / {c[1]} | {w:.4g} | {ideal:.4g} | {w - ideal:.4g} | {top_s} |")
+        lines.append("")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "conflicts":
+        conflicts(sys.argv[2], sys.argv[3:])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
         tr = full(sys.argv[2], sys.argv[3])
