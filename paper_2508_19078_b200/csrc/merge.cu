@@ -30,25 +30,34 @@ namespace {
 constexpr int kMaxE = 1024;
 // ------------------------------------------------------------------ TMA-bulk pipelined batch kernel
 // Warp 0 (producer, one elected lane) walks this CTA's chunks (dealt round-robin over one CTA per SM, so
-// at any moment the CTAs stream neighbouring addresses) and per chunk issues one 1D bulk copy
-// (cp.async.bulk, evict_first) per member into a ring of kStages stages of up to 4 member slices (8 KB
-// each); a chunk of a cluster with m members takes ceil(m / 4) stages.  The stage header carries the
-// members' weights, whether the stage starts the chunk, and (on its last stage) the output address.
-// Warps 1..16 (consumers, one 16-byte vector of the chunk per thread) accumulate w_e·W_e in fp32
-// (packed FFMA2, bit-identical per lane to fmaf; member order), and after the chunk's last stage round
-// once and store.  The producer keeps the job's member table (every output: members in ascending id,
+// at any moment the CTAs stream neighbouring addresses) and turns each chunk into one 8 KB slice per
+// member (an output without members: one data-less slice).  Slices fill a ring of kStages stages of 4
+// slots in stream order, across chunk boundaries, so every stage carries 32 KB whatever the cluster
+// sizes.  Each slot's descriptor: member weight, whether it starts its chunk (reset the accumulators),
+// the chunk's vector count, and on a chunk's last slice the output address; a stage of four members of
+// one chunk is flagged so the consumers take a straight-line path.  One expect-tx per slice, one arrival
+// per stage once its descriptors are final; lane i of the producer warp issues slice i of a group (a
+// single lane walking the slices was issue-bound at the power-capped clock).  Warps 1..8 (consumers, two
+// 16-byte vectors of every slice per thread: half the per-stage barrier and descriptor work of one)
+// load the stage's slices into registers, release the stage, then accumulate w_e·W_e in fp32 (packed
+// FFMA2, bit-identical per lane to fmaf; member order), rounding once and storing at a chunk's last slice.  The producer keeps the job's member table (every output: members in ascending id,
 // weights α_e / Σα with Σα in ascending id) in shared memory, rebuilt per job.
 constexpr int kSlice = 8192;                  // bytes of one member slice (one chunk of one expert)
-constexpr int kPerStage = 4;                  // member slices per stage
+constexpr int kPerStage = 4;                  // slices per stage
 constexpr int kStages = 6;                    // 6 x 32 KB = 192 KB of HBM reads in flight per SM
-constexpr int kConsumers = kSlice / 16;       // one 16-byte vector per consumer thread
+constexpr int kVpt = 2;                       // 16-byte vectors of every slice per consumer thread
+constexpr int kConsumers = kSlice / 16 / kVpt;
+constexpr int kFast = 1 << 8;                 // stage n field: four data slices of one chunk, in member order
 constexpr int kBThreads = 32 + kConsumers;
+constexpr int kFirst = 1 << 30;               // slot meta: first slice of its chunk
+constexpr int kNoData = 1 << 29;              // slot meta: an output without members (writes zeros)
 
-struct __align__(16) StageHdr {  // read by the consumers as two 16-byte shared loads
+struct __align__(16) StageHdr {  // read by the consumers as five 16-byte shared loads
   float w[kPerStage];
-  void* out;       // output vectors of this chunk when the stage holds its last members, else null
-  int n;           // member slices in this stage (0: an output without members -> zeros; -1: end)
-  int meta;        // 16-byte vectors in this chunk | (first stage of the chunk: reset the accumulators) << 30
+  int meta[kPerStage];  // vectors in the slot's chunk | kFirst | kNoData
+  void* out[kPerStage]; // output vectors of the chunk on its last slice, else null
+  int n;                // slots used | kFast (-1: end)
+  int pad[3];
 };
 
 struct BatchSmem {
@@ -137,15 +146,29 @@ __global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_co
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
     const uint64_t pol = policy_evict_first();
-    const bool leader = (threadIdx.x & 31) == 0;
+    const int lane = threadIdx.x & 31;
+    const bool leader = lane == 0;
     int j = -1, n_out = 0, g = 0;
     int64_t local = 0, c_in = 0;  // chunk index inside job j, inside output o
     int o = 0;
     auto next_stage = [&]() {
-      const int s = g % kStages;
-      mbar_wait(&t.empty[s], ((g / kStages) & 1) ^ 1);
+      const int st = g % kStages;
+      mbar_wait(&t.empty[st], ((g / kStages) & 1) ^ 1);
       ++g;
-      return s;
+      return st;
+    };
+    int s = -1, slot = 0;  // the stage being filled and its next free slot
+    bool fast = false;     // ... and whether it holds four data slices of one chunk
+    auto commit = [&]() {  // the stage's descriptors are final: its single arrival
+      __syncwarp();
+      if (leader) {
+        t.hdr[s].n = slot | (fast ? kFast : 0);
+        mbar_arrive(&t.full[s]);
+      }
+      __syncwarp();
+      s = -1;
+      slot = 0;
+      fast = false;
     };
     for (int64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
       if (j < 0 || ch >= b.chunk_prefix[j + 1]) {  // entering a new job: rebuild the table
@@ -168,27 +191,34 @@ __global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_co
       const uint32_t bytes = (uint32_t)n_elems * kEsz;
       void* out = (uint8_t*)job.merged + ((int64_t)o * b.numel + e0) * kEsz;
       const int m0 = t.start[o], m1 = t.start[o + 1];
-      int m = m0;
-      do {  // one stage per group of up to 4 members (an output with no member still takes one stage)
-        const int s = next_stage();
-        const int n = min(kPerStage, m1 - m);
-        if (leader) {
+      const int nvec = (int)(bytes / 16);
+      // the chunk's slices, up to 4 per stage, lane i issuing slice i of the group (warp-parallel: a single
+      // lane walking the slices is issue-bound at the power-capped clock)
+      const int n_sl = max(m1 - m0, 1);  // an output without members: one data-less slot
+      for (int j0 = 0; j0 < n_sl;) {
+        if (s < 0) s = next_stage();
+        const int take = min(kPerStage - slot, n_sl - j0);
+        if (take == kPerStage && m1 > m0) fast = true;  // a whole stage of one chunk's members
+        if (lane < take) {
+          const int q = j0 + lane, sl = slot + lane;  // slice q of the chunk into slot sl
+          const bool data = m1 > m0;
           StageHdr& h = t.hdr[s];
-#pragma unroll
-          for (int i = 0; i < kPerStage; ++i) h.w[i] = i < n ? t.w[m + i] : 0.f;
-          h.out = m + n >= m1 ? out : nullptr;
-          h.n = n;
-          h.meta = (int)(bytes / 16) | (m == m0 ? 1 << 30 : 0);
-          mbar_arrive_expect_tx(&t.full[s], (uint32_t)n * bytes);
-          for (int i = 0; i < n; ++i)
-            bulk_load_1d(t.data[s][i], (const uint8_t*)job.experts + ((int64_t)t.mem[m + i] * b.numel + e0) * kEsz,
+          h.w[sl] = data ? t.w[m0 + q] : 0.f;
+          h.meta[sl] = nvec | (q == 0 ? kFirst : 0) | (data ? 0 : kNoData);
+          h.out[sl] = q + 1 == n_sl ? out : nullptr;
+          if (data) {
+            mbar_expect_tx(&t.full[s], bytes);
+            bulk_load_1d(t.data[s][sl], (const uint8_t*)job.experts + ((int64_t)t.mem[m0 + q] * b.numel + e0) * kEsz,
                          bytes, &t.full[s], pol);
+          }
         }
-        __syncwarp();
-        m += n;
-      } while (m < m1);
+        j0 += take;
+        slot += take;
+        if (slot == kPerStage) commit();
+      }
     }
-    const int s = next_stage();  // end marker
+    if (s >= 0) commit();
+    s = next_stage();  // end marker
     if (leader) {
       t.hdr[s].n = -1;
       mbar_arrive(&t.full[s]);
@@ -196,64 +226,96 @@ __global__ void __launch_bounds__(kBThreads, 1) merge_tma_kernel(const __grid_co
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- consumers
-    const int v = threadIdx.x - 32;  // this thread's 16-byte vector of every chunk
+    const int v0 = threadIdx.x - 32;  // this thread's 16-byte vectors of every slice: v0 + u·kConsumers
     constexpr int kPairs = 16 / kEsz / 2;
-    float2 acc[kPairs];
+    float2 acc[kVpt][kPairs];
     // one member's FMA into the accumulators (bf16 -> fp32 is exact: the bits shifted into place)
-    auto fma_member = [&](const uint4& r, float w) {
+    auto fma_member = [&](float2 (&a)[kPairs], const uint4& r, float w) {
       const float2 w2 = make_float2(w, w);
       if constexpr (F32) {
-        acc[0] = fma2_rn(w2, make_float2(__uint_as_float(r.x), __uint_as_float(r.y)), acc[0]);
-        acc[1] = fma2_rn(w2, make_float2(__uint_as_float(r.z), __uint_as_float(r.w)), acc[1]);
+        a[0] = fma2_rn(w2, make_float2(__uint_as_float(r.x), __uint_as_float(r.y)), a[0]);
+        a[1] = fma2_rn(w2, make_float2(__uint_as_float(r.z), __uint_as_float(r.w)), a[1]);
       } else {
         const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          acc[i] = fma2_rn(w2, make_float2(__uint_as_float(u[i] << 16), __uint_as_float(u[i] & 0xffff0000u)), acc[i]);
+          a[i] = fma2_rn(w2, make_float2(__uint_as_float(u[i] << 16), __uint_as_float(u[i] & 0xffff0000u)), a[i]);
       }
+    };
+    auto reset = [&](float2 (&a)[kPairs]) {
+#pragma unroll
+      for (int q = 0; q < kPairs; ++q) a[q] = make_float2(0.f, 0.f);
+    };
+    auto store = [&](const float2 (&a)[kPairs], uint64_t out, int v) {
+      uint4 ov;
+      if constexpr (F32) {
+        ov = make_uint4(__float_as_uint(a[0].x), __float_as_uint(a[0].y), __float_as_uint(a[1].x), __float_as_uint(a[1].y));
+      } else {
+        ov.x = pack_bf16x2(a[0].x, a[0].y);
+        ov.y = pack_bf16x2(a[1].x, a[1].y);
+        ov.z = pack_bf16x2(a[2].x, a[2].y);
+        ov.w = pack_bf16x2(a[3].x, a[3].y);
+      }
+      __stcs(reinterpret_cast<uint4*>(out) + v, ov);
     };
     for (int g = 0;; ++g) {
       const int s = g % kStages;
       mbar_wait(&t.full[s], (g / kStages) & 1);
       const uint32_t ha = smem_u32(&t.hdr[s]);
-      const uint4 hw = ld_shared_v4(ha), hm = ld_shared_v4(ha + 16);  // weights; out, n, meta
-      const int n = (int)hm.z;
-      if (n < 0) break;
-      const int nvec = (int)(hm.w & 0x3fffffffu);
-      void* out = reinterpret_cast<void*>((uint64_t)hm.x | ((uint64_t)hm.y << 32));
-      if (hm.w >> 30) {
+      const int nf = (int)ld_shared_v4(ha + 64).x;
+      if (nf < 0) break;
+      const uint32_t d = smem_u32(t.data[s][0]) + v0 * 16;
+      const uint4 hw = ld_shared_v4(ha), hm = ld_shared_v4(ha + 16);
+      const float ws[kPerStage] = {__uint_as_float(hw.x), __uint_as_float(hw.y), __uint_as_float(hw.z),
+                                   __uint_as_float(hw.w)};
+      uint4 r[kPerStage][kVpt];
+      if (nf & kFast) {  // four members of one chunk: straight-line FMAs, reset / store at most once
+        const int nvec = (int)hm.x & (kNoData - 1);
+        const uint4 ho23 = ld_shared_v4(ha + 48);
+        const uint64_t out = (uint64_t)ho23.z | ((uint64_t)ho23.w << 32);
 #pragma unroll
-        for (int i = 0; i < kPairs; ++i) acc[i] = make_float2(0.f, 0.f);
-      }
-      if (v < nvec) {
-        const uint32_t d = smem_u32(t.data[s][0]) + v * 16;
-        if (n == kPerStage) {  // full stage (balanced 4-member clusters): every load first, then the FMAs
-          const uint4 r0 = ld_shared_v4(d), r1 = ld_shared_v4(d + kSlice), r2 = ld_shared_v4(d + 2 * kSlice),
-                      r3 = ld_shared_v4(d + 3 * kSlice);
-          fma_member(r0, __uint_as_float(hw.x));
-          fma_member(r1, __uint_as_float(hw.y));
-          fma_member(r2, __uint_as_float(hw.z));
-          fma_member(r3, __uint_as_float(hw.w));
-        } else {
-          const float ws[4] = {__uint_as_float(hw.x), __uint_as_float(hw.y), __uint_as_float(hw.z),
-                               __uint_as_float(hw.w)};
-          for (int mi = 0; mi < n; ++mi) fma_member(ld_shared_v4(d + mi * kSlice), ws[mi]);
+        for (int i = 0; i < kPerStage; ++i)
+#pragma unroll
+          for (int u = 0; u < kVpt; ++u)
+            if (v0 + u * kConsumers < nvec) r[i][u] = ld_shared_v4(d + i * kSlice + u * kConsumers * 16);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&t.empty[s]);
+#pragma unroll
+        for (int u = 0; u < kVpt; ++u) {
+          if (hm.x & kFirst) reset(acc[u]);
+          if (v0 + u * kConsumers >= nvec) continue;
+#pragma unroll
+          for (int i = 0; i < kPerStage; ++i) fma_member(acc[u], r[i][u], ws[i]);
+          if (out) store(acc[u], out, v0 + u * kConsumers);
         }
+        continue;
       }
+      const int n = nf & (kFast - 1);
+      const uint4 ho01 = ld_shared_v4(ha + 32), ho23 = ld_shared_v4(ha + 48);
+      const int meta[kPerStage] = {(int)hm.x, (int)hm.y, (int)hm.z, (int)hm.w};
+      const uint64_t outs[kPerStage] = {(uint64_t)ho01.x | ((uint64_t)ho01.y << 32), (uint64_t)ho01.z | ((uint64_t)ho01.w << 32),
+                                        (uint64_t)ho23.x | ((uint64_t)ho23.y << 32), (uint64_t)ho23.z | ((uint64_t)ho23.w << 32)};
+      // every slice of the stage into registers first, then release the stage
+#pragma unroll
+      for (int i = 0; i < kPerStage; ++i)
+#pragma unroll
+        for (int u = 0; u < kVpt; ++u)
+          if (i < n && v0 + u * kConsumers < (meta[i] & (kNoData - 1)) && !(meta[i] & kNoData))
+            r[i][u] = ld_shared_v4(d + i * kSlice + u * kConsumers * 16);
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&t.empty[s]);
-      if (out && v < nvec) {
-        uint4 ov;
-        if constexpr (F32) {
-          ov = make_uint4(__float_as_uint(acc[0].x), __float_as_uint(acc[0].y), __float_as_uint(acc[1].x),
-                          __float_as_uint(acc[1].y));
-        } else {
-          ov.x = pack_bf16x2(acc[0].x, acc[0].y);
-          ov.y = pack_bf16x2(acc[1].x, acc[1].y);
-          ov.z = pack_bf16x2(acc[2].x, acc[2].y);
-          ov.w = pack_bf16x2(acc[3].x, acc[3].y);
+#pragma unroll
+      for (int i = 0; i < kPerStage; ++i) {
+        if (i >= n) break;
+        const int nvec = meta[i] & (kNoData - 1);
+#pragma unroll
+        for (int u = 0; u < kVpt; ++u) {
+          if (meta[i] & kFirst) reset(acc[u]);
+          const int v = v0 + u * kConsumers;
+          if (v >= nvec) continue;
+          if (!(meta[i] & kNoData)) fma_member(acc[u], r[i][u], ws[i]);
+          if (outs[i]) store(acc[u], outs[i], v);
         }
-        __stcs(reinterpret_cast<uint4*>(out) + v, ov);
       }
     }
   }

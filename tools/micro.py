@@ -72,7 +72,7 @@ def merge_model():
     g = torch.Generator(device="cuda").manual_seed(1)
     unb = torch.randint(0, C, (L, E), generator=g, device="cuda", dtype=torch.int32)
     unb[:, :C] = torch.arange(C, dtype=torch.int32, device="cuda")
-    out = mm(m, alpha, bal, C)
+    out = mm(m, alpha, unb if os.environ.get("MICRO_MERGE_FIRST") == "unbalanced" else bal, C)  # first launch (ncu -c 1)
     a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
     for name, cl in (("balanced", bal), ("unbalanced", unb)):
         ms = timed(lambda: mm(m, alpha, cl, C, out), reps=5, warm=2)
