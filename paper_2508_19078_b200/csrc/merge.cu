@@ -8,9 +8,9 @@
 // HBM-bound (read Σ|W_e| once, write Σ|W_c| once).  ONE persistent launch
 // covers a batch of jobs (a job = one weight family of one layer: the bench
 // merges all L x 3 families of a model in one launch instead of 3L small ones).
-// The work is cut into chunks of 8 KB of consecutive output elements, dealt
+// The work is cut into chunks of 16 KB of consecutive output elements, dealt
 // round-robin over one CTA per SM, and streamed with TMA bulk copies through a
-// 6-stage shared-memory ring (192 KB of reads in flight per SM; see the kernel).
+// 3-stage shared-memory ring (192 KB of reads in flight per SM; see the kernel).
 //
 // Per output: the member list (ascending expert id) and fp32 weights
 // w_e = α_e / Σα (Σα accumulated in ascending id: deterministic); the FMA chain
@@ -29,23 +29,25 @@ namespace {
 
 constexpr int kMaxE = 1024;
 // ------------------------------------------------------------------ TMA-bulk pipelined batch kernel
-// Warp 0 (producer, one elected lane) walks this CTA's chunks (dealt round-robin over one CTA per SM, so
-// at any moment the CTAs stream neighbouring addresses) and turns each chunk into one 8 KB slice per
-// member (an output without members: one data-less slice).  Slices fill a ring of kStages stages of 4
-// slots in stream order, across chunk boundaries, so every stage carries 32 KB whatever the cluster
-// sizes.  Each slot's descriptor: member weight, whether it starts its chunk (reset the accumulators),
-// the chunk's vector count, and on a chunk's last slice the output address; a stage of four members of
-// one chunk is flagged so the consumers take a straight-line path.  One expect-tx per slice, one arrival
-// per stage once its descriptors are final; lane i of the producer warp issues slice i of a group (a
-// single lane walking the slices was issue-bound at the power-capped clock).  Warps 1..8 (consumers, two
-// 16-byte vectors of every slice per thread: half the per-stage barrier and descriptor work of one)
-// load the stage's slices into registers, release the stage, then accumulate w_e·W_e in fp32 (packed
-// FFMA2, bit-identical per lane to fmaf; member order), rounding once and storing at a chunk's last slice.  The producer keeps the job's member table (every output: members in ascending id,
-// weights α_e / Σα with Σα in ascending id) in shared memory, rebuilt per job.
-constexpr int kSlice = 8192;                  // bytes of one member slice (one chunk of one expert)
+// Warp 0 (producer) walks this CTA's chunks (dealt round-robin over one CTA per SM, so at any moment
+// the CTAs stream neighbouring addresses) and turns each chunk into one 16 KB slice per member (an
+// output without members: one data-less slice).  Slices fill a ring of kStages stages of 4 slots in
+// stream order, across chunk boundaries, so every stage carries 64 KB whatever the cluster sizes (K-Means
+// gives 1-9 members per cluster).  Each slot's descriptor: member weight, whether it starts its chunk
+// (reset the accumulators), the chunk's vector count, and on a chunk's last slice the output address; a
+// stage of four members of one chunk is flagged so the consumers take a straight-line path.  One
+// expect-tx per slice, one arrival per stage once its descriptors are final; lane i of the producer warp
+// issues slice i of a group.  The producer's instruction stream is what bounds the kernel at the
+// power-capped clock (~290 warp instructions per stage with 8 KB slices), hence the 16 KB slices:
+// half the producer work per byte.  Warps 1..8 (consumers, four 16-byte vectors of every slice per
+// thread) load the stage's slices into registers, release the stage, then accumulate w_e·W_e in fp32
+// (packed FFMA2, bit-identical per lane to fmaf; member order), rounding once and storing at a chunk's
+// last slice.  The producer keeps the job's member table (every output: members in ascending id, weights
+// α_e / Σα with Σα in ascending id) in shared memory, rebuilt per job.
+constexpr int kSlice = 16384;                 // bytes of one member slice (one chunk of one expert)
 constexpr int kPerStage = 4;                  // slices per stage
-constexpr int kStages = 6;                    // 6 x 32 KB = 192 KB of HBM reads in flight per SM
-constexpr int kVpt = 2;                       // 16-byte vectors of every slice per consumer thread
+constexpr int kStages = 3;                    // 3 x 64 KB = 192 KB of HBM reads in flight per SM
+constexpr int kVpt = 4;                       // 16-byte vectors of every slice per consumer thread
 constexpr int kConsumers = kSlice / 16 / kVpt;
 constexpr int kFast = 1 << 8;                 // stage n field: four data slices of one chunk, in member order
 constexpr int kBThreads = 32 + kConsumers;

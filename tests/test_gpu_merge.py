@@ -5,8 +5,9 @@ model (BASELINE.json configs[3]: 64 -> 16 merged experts per layer, α = activat
 The oracle (oracle.merge, fp64) is element-wise by definition, so it is evaluated on sampled output
 indices only: the members' master values at those indices come from the CPU twin of the generator,
 α from the ORACLE's own routing of a token sample (never from the CUDA path).  Samples cover every
-output of every job uniformly plus its first / last element and chunk edges; with 444 persistent CTAs
-each walking ~2,000 chunks, they hit every part of every CTA's range.  Variants: tuning experts
+output of every job uniformly plus its first / last element and chunk edges (16 KB = 8,192 bf16
+elements per chunk); with 148 persistent CTAs each walking ~3,200 chunks, and slices packed four per
+stage across chunk boundaries, they hit every part of every CTA's range and every slot position.  Variants: tuning experts
 (cluster_of = -1), a cluster whose α are all zero (plain mean, R10), unbalanced clusters including
 singletons (bit-exact identity), and per-layer budgets B(l) (eq.(1)).  Bound: |Δ| <= 2e-2·Σ_e w_e|W_e|
 (condition-aware, bf16), and >= 99% of outputs equal to the correctly rounded fp64 value."""
@@ -53,8 +54,8 @@ def _variant_clusters(cfg, variant, layer, rng):
 
 
 def _sample_indices(numel, n, rng):
-    chunk = 4096
-    edges = [0, 1, 7, 8, chunk - 1, chunk, 444 * chunk % numel, numel // 2, numel - 8, numel - 1]
+    chunk = 8192  # bf16 elements per 16 KB chunk (merge.cu kSlice)
+    edges = [0, 1, 7, 8, chunk - 1, chunk, chunk + 1, 148 * chunk % numel, numel // 2, numel - 8, numel - 1]
     return np.unique(np.concatenate([edges, rng.integers(0, numel, n)]).astype(np.int64))
 
 
