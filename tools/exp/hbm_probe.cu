@@ -12,6 +12,7 @@
 #include <cublas_v2.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <unistd.h>
 
@@ -188,6 +189,29 @@ __global__ void fill_random(__nv_bfloat16* p, int64_t n, uint32_t seed) {
   }
 }
 
+// bulk (TMA) stores from shared memory: one lane per CTA streams SLICE-byte copies of a zeroed smem
+// buffer to consecutive global addresses, at most DEPTH bulk groups in flight
+template <int SLICE, int DEPTH>
+__global__ void __launch_bounds__(32) write_tma(uint8_t* __restrict__ out, int64_t bytes, Probe* p) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  probe_begin(p);
+  for (int i = threadIdx.x; i < SLICE / 16; i += 32) reinterpret_cast<uint4*>(sm)[i] = make_uint4(1, 2, 3, 4);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    const int64_t n = bytes / SLICE;
+    for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + c * SLICE),
+                   "r"(smem_u32(sm)), "r"(SLICE)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(DEPTH) : "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  probe_end(p);
+}
+
 #define CK(x)                                                                    \
   do {                                                                           \
     cudaError_t e_ = (x);                                                        \
@@ -218,12 +242,21 @@ int main() {
   fill_random<<<1024, 256>>>(gb, (int64_t)N * N, 2);
   CK(cudaDeviceSynchronize());
   cublasHandle_t h;
-  cublasCreate(&h);
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) {
+    fprintf(stderr, "cublasCreate failed\n");
+    return 1;
+  }
   const float one = 1.f, zero = 0.f;
   auto gemm = [&](int n) {
-    for (int i = 0; i < n; ++i)
-      cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, N, N, N, &one, ga, CUDA_R_16BF, N, gb, CUDA_R_16BF, N, &zero, gc,
-                   CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    for (int i = 0; i < n; ++i) {
+      const cublasStatus_t st = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, N, N, N, &one, ga, CUDA_R_16BF, N, gb,
+                                             CUDA_R_16BF, N, &zero, gc, CUDA_R_16BF, N, CUBLAS_COMPUTE_32F,
+                                             CUBLAS_GEMM_DEFAULT);
+      if (st != CUBLAS_STATUS_SUCCESS) {
+        fprintf(stderr, "cublasGemmEx failed: %d\n", (int)st);
+        exit(1);
+      }
+    }
   };
   int nsm = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
@@ -269,8 +302,18 @@ int main() {
     cudaFuncSetAttribute(read_tma<S, P, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     add("read_tma 8KBx1x24", 1.0 * bytes, [&, smem] { read_tma<S, P, ST><<<nsm, 544, smem>>>(a, sink, bytes, pr); });
   }
+  {
+    constexpr int S = 16384;
+    cudaFuncSetAttribute(write_tma<S, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, S);
+    add("write_tma 16KB d8 1/SM", 1.0 * bytes, [&] { write_tma<S, 8><<<nsm, 32, S>>>(b, bytes, pr); });
+    add("write_tma 16KB d8 4/SM", 1.0 * bytes, [&] { write_tma<S, 8><<<nsm * 4, 32, S>>>(b, bytes, pr); });
+    add("write_stg U8", 1.0 * bytes, [&] { write_stg<8><<<nsm * 4, 512>>>((uint4*)b, nv, pr); });
+    add("write_stg U2 2/SM", 1.0 * bytes, [&] { write_stg<2><<<nsm * 2, 512>>>((uint4*)b, nv, pr); });
+  }
   printf("%-22s %5s %9s %9s %8s %10s\n", "kernel", "mode", "ms", "GB/s", "SM MHz", "B/clk/SM");
+  const char* only = getenv("PROBE_ONLY");
   for (auto& k : ks) {
+    if (only && !strstr(k.name, only)) continue;
     for (int hot = 0; hot < 2; ++hot) {
       std::vector<double> ms_v, mhz_v;
       for (int r = 0; r < 5; ++r) {
@@ -279,6 +322,7 @@ int main() {
           CK(cudaDeviceSynchronize());
           usleep(300000);  // idle
         }
+        fprintf(stderr, "%s %s rep %d\n", k.name, hot ? "hot" : "cold", r);
         cudaEventRecord(e0);
         k.run();
         cudaEventRecord(e1);
@@ -295,7 +339,7 @@ int main() {
       std::sort(mhz_v.begin(), mhz_v.end());
       const double ms = ms_v[2], mhz = mhz_v[2];
       const double gbs = k.traffic / ms / 1e6;
-      printf("%-22s %5s %9.3f %9.0f %8.0f %10.1f\n", k.name, hot ? "hot" : "cold", ms, gbs, mhz,
+  printf("%-22s %5s %9.3f %9.0f %8.0f %10.1f\n", k.name, hot ? "hot" : "cold", ms, gbs, mhz,
              gbs * 1e9 / (mhz * 1e6) / nsm);
       fflush(stdout);
     }
