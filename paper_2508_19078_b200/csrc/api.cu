@@ -45,6 +45,23 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype,
   return r == CUDA_SUCCESS;
 }
 
+// X bf16 [rows][cols] seen as [cols/64 blocks][rows][64]: element (c, r, b) at r·cols + 64·b + c.  One
+// box {64, box_rows, n_blocks} lands in shared memory as n_blocks consecutive [box_rows][128 B] tiles
+// (128B-swizzled: the K-major operand layout of the Gram MMA).
+bool make_tmap_gram_blocks(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                           uint32_t n_blocks) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return false;
+  cuuint64_t dims[3] = {64, std::max<uint64_t>(rows, 1), cols / 64};
+  cuuint64_t strides[2] = {cols * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, n_blocks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = f(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 static bool tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                       uint64_t ld = 0 /* row length in elements, default cols */) {
   return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, (ld ? ld : cols) * 2, 64, box_rows,

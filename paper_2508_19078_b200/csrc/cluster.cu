@@ -36,8 +36,10 @@ constexpr int kChunkStages = kChunkSlices / kSlices;
 constexpr int kRing = 8;                   // claimed-chunk ring (producer -> MMA, epilogue)
 
 struct GramMaps {
-  CUtensorMap map[kMaxFam];  // family f of this layer: bf16 [E][P_f], box {64 cols, NPAD rows}
-  int64_t kb_end[kMaxFam];   // cumulative 64-column slice counts
+  CUtensorMap map[kMaxFam];   // family f of this layer: bf16 [E][P_f], box {64 cols, NPAD rows}
+  CUtensorMap map4[kMaxFam];  // the same family as [P_f/64 blocks][E][64]: box {64, NPAD, kSlices} = one stage
+  int64_t kb_end[kMaxFam];    // cumulative 64-column slice counts
+  int64_t nblk[kMaxFam];      // whole 64-column blocks of family f (map4's outer extent)
   int n_fam;
 };
 
@@ -129,13 +131,22 @@ __global__ void __launch_bounds__(192, 1)
           const int s = gs % kStages;
           const uint32_t ph = (gs / kStages) & 1;
           const int n_sl = kb1 - kb < kSlices ? (int)(kb1 - kb) : kSlices;
+          while (kb >= gm.kb_end[f]) ++f;
+          const int64_t local = kb - (f ? gm.kb_end[f - 1] : 0);
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], n_sl * C::kSlice);
-          for (int t = 0; t < n_sl; ++t) {
-            while (kb + t >= gm.kb_end[f]) ++f;
-            const int64_t local = kb + t - (f ? gm.kb_end[f - 1] : 0);
-            tma_load_2d_hint(smem + s * C::kTile + t * C::kSlice, &gm.map[f], &full[s], (int32_t)(local * kBK), 0,
-                             pol);
+          if (n_sl == kSlices && local + kSlices <= gm.nblk[f]) {
+            // the whole stage in one 3D box: kSlices blocks of 64 columns x NPAD rows, written as kSlices
+            // consecutive [NPAD][128 B] slices (a quarter of the producer's instructions per byte)
+            tma_load_3d_hint(smem + s * C::kTile, &gm.map4[f], &full[s], 0, 0, (int32_t)local, pol);
+          } else {
+            int ft = f;
+            for (int t = 0; t < n_sl; ++t) {
+              while (kb + t >= gm.kb_end[ft]) ++ft;
+              const int64_t lt = kb + t - (ft ? gm.kb_end[ft - 1] : 0);
+              tma_load_2d_hint(smem + s * C::kTile + t * C::kSlice, &gm.map[ft], &full[s], (int32_t)(lt * kBK), 0,
+                               pol);
+            }
           }
         }
       }
@@ -232,8 +243,19 @@ __global__ void __launch_bounds__(1024) gram_reduce_kernel(const float* __restri
   const int i = blockIdx.x, j = threadIdx.x % EP, g = threadIdx.x / EP;
   if (i == 0 && threadIdx.x == 0) *counter = 0;  // the Gram kernel that claimed from it has completed
   double acc = 0.0;
-  if (j < E)
-    for (int p = g; p < n_partial; p += NG) acc += partial[(int64_t)p * E * E + i * E + j];
+  if (j < E) {  // ascending p; eight loads in flight before their (in-order) additions
+    const float* src = partial + i * E + j;
+    const int64_t ee = (int64_t)E * E;
+    int p = g;
+    for (; p + 7 * NG < n_partial; p += 8 * NG) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(p + u * NG) * ee);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; p < n_partial; p += NG) acc += __ldcg(src + (int64_t)p * ee);
+  }
   part[g][j] = acc;
   __syncthreads();
   if (g == 0 && j < E) {
@@ -499,6 +521,11 @@ cudaError_t launch_gram(int E, int n_fam, const void* const* X, const int64_t* P
     if (!make_tmap_2d(&gm.map[f], X[f], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)E, (uint64_t)P[f],
                       (uint64_t)P[f] * 2, 64, (uint32_t)npad, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
+    gm.nblk[f] = P[f] / kBK;
+    if (gm.nblk[f] >= kSlices &&
+        !make_tmap_gram_blocks(&gm.map4[f], X[f], (uint64_t)E, (uint64_t)P[f], (uint32_t)npad, kSlices))
+      return cudaErrorInvalidValue;
+    if (gm.nblk[f] < kSlices) gm.nblk[f] = 0;  // too short for a whole stage: per-slice loads only
     acc += (P[f] + kBK - 1) / kBK;
     gm.kb_end[f] = acc;
   }

@@ -17,6 +17,8 @@ constexpr int kRouterTile = 256;  // tokens per router tile: the unit of tile_co
 bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint32_t elem_bytes, uint64_t rows,
                   uint64_t cols, uint64_t row_stride_bytes, uint32_t box_cols, uint32_t box_rows,
                   CUtensorMapSwizzle swizzle);
+bool make_tmap_gram_blocks(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                           uint32_t n_blocks);
 
 inline flux_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FLUX_OK : FLUX_E_CUDA; }
 

@@ -100,6 +100,11 @@ def features():
     by = m.gate.numel() * 2 * 3
     print(f"features 28 layers: {ms:.2f} ms  {by / ms / 1e6:.0f} GB/s ({by / ms / 1e6 / peak():.2f} of HBM); "
           f"kmeans {ms_k:.3f} ms;", {n: round(v[0] / max(v[1], 1), 4) for n, v in k.items() if v[1]})
+    a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    for _ in range(300):  # ~1 s of bf16 GEMMs: power-capped clocks, like inside the bench step
+        a @ a
+    ms = timed(lambda: expert_features_model(m, 16), reps=1, warm=0)
+    print(f"features 28 layers after GEMM load: {ms:.2f} ms  {by / ms / 1e6:.0f} GB/s ({by / ms / 1e6 / peak():.2f})")
 
 
 def layer(name="deepseek_moe"):
