@@ -297,7 +297,9 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
         for c in range(n_chunks):                                 # a1-a6 (hist accumulates over chunks)
             if before_chunk:
                 before_chunk(c)
+            torch.cuda.nvtx.range_push(f"chunk {c}")             # chunk x layer timeline (nsys; no-op otherwise)
             prof.run(qm, xs[c * Tc:(c + 1) * Tc], zero_hist=False, attn=attn)
+            torch.cuda.nvtx.range_pop()
             if after_chunk:
                 after_chunk(c)
         comm.reduce_stats(prof.hist)                              # a7

@@ -8,6 +8,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only: a no-op unless a profiler (nsys) injects itself
+
 #include "internal.h"
 
 namespace flux {
@@ -46,6 +48,7 @@ cudaEvent_t get_event() {
 
 KernelTimer::KernelTimer(int kind, cudaStream_t st) : kind_(kind), st_(st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  nvtxRangePushA(kernel_name(kind));  // host-side range around the launch: the step timeline under nsys
   if (!g_enabled.load(std::memory_order_relaxed)) return;
   std::lock_guard<std::mutex> lk(g_mu);
   a_ = get_event();
@@ -65,6 +68,7 @@ static int debug_sync() {
 }
 
 KernelTimer::~KernelTimer() {
+  nvtxRangePop();
   if (debug_sync()) {  // diagnostics: surface the failing kernel instead of a later, anonymous error
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st_);

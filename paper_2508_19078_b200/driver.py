@@ -230,7 +230,9 @@ class Profiler:
                 self.ahist.zero_()
         cur = x
         for l in range(self.shape.n_layers):
+            torch.cuda.nvtx.range_push(f"layer {l}")  # the chunk x layer timeline under nsys
             profile_layer(self.cfgs[l], qm.qlayer(l), cur, None, self.T, self.out(l), self.ws, stream, self.policy)
+            torch.cuda.nvtx.range_pop()
             if attn is not None:
                 attention_hist(self.ids[l], attn[l], self.shape.n_experts, self.ahist[l], stream)
             cur = self.y[l % 2]
