@@ -23,7 +23,7 @@ NAMES = [("grouped_gemm_pair_kernel<0>", "K3/K5 gate/up GEMM (pair)"), ("grouped
          ("grouped_gemm_kernel<(int)0>", "K3/K5 gate/up GEMM (1-CTA)"), ("grouped_gemm_kernel<(int)1>", "K4/K5 down GEMM (1-CTA)"),
          ("combine_kernel", "K6 combine"), ("quantize_kernel", "K0 quantize"), ("dequant_kernel", "K3/K4 dequant pass"),
          ("merge_tma_kernel", "K7 merge (batched, TMA)"), ("merge_kernel", "K7 merge"), ("gram_reduce_kernel", "K8b Gram reduce"), ("gram_kernel", "K8 Gram (PCA)"),
-         ("eig_kernel", "K8c Jacobi eigen"), ("kmeans_kernel", "K9 K-Means"), ("cosine_distance_kernel", "output error")]
+         ("eig_kernel", "K8c Jacobi eigen"), ("frequencies_kernel", "alpha = f (frequencies)"), ("kmeans_kernel", "K9 K-Means"), ("cosine_distance_kernel", "output error")]
 
 
 def label(name):
