@@ -190,6 +190,52 @@ def test_merge_parity(dtype, variant):
         assert torch.equal(out, dev_W)  # |E_c| = 1 -> identity, bit for bit
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_merge_packed_stages(dtype):
+    """K7's stage packing (merge.cu): slices are packed four per stage ACROSS chunk boundaries, so a
+    stage mixes the tail of one chunk with the head of the next.  Cluster sizes 1..9 (K-Means-like),
+    an empty cluster (zeros, no error), two tuning experts, and outputs spanning several 16 KB chunks
+    with a ragged tail put every slot position, chunk start and chunk end in every combination."""
+    import paper_2508_19078_b200 as F
+    rng = np.random.default_rng(7 if dtype == "bf16" else 8)
+    cfg = synth.CONFIGS["toy"]
+    sizes = [1, 9, 0, 2, 5, 3, 1, 4, 7, 6, 2]      # cluster 2 is empty
+    E, C = sum(sizes) + 2, len(sizes)
+    rows, cols = 41, 488                           # numel 20,008: 2 (bf16) / 4 (fp32) whole chunks + a tail
+    numel = rows * cols
+    W = np.stack([synth.cpu_matrix(synth.Spec(rows, cols, cfg.seed, synth.stream_id(synth.KIND_MASTER_F32, 1, e),
+                                              synth.scale_c(1.0), 0, 0.0), dtype=dtype) for e in range(E)])
+    Wf = (W.astype(np.float32) if dtype == "f32" else synth.bf16_bits_to_f32(W)).reshape(E, numel)
+    perm = rng.permutation(E)
+    cl = np.full(E, -1, np.int32)                  # the last two of perm stay tuning experts
+    i = 0
+    for c, n in enumerate(sizes):
+        cl[perm[i:i + n]] = c
+        i += n
+    alpha = rng.uniform(0.01, 1.0, E).astype(np.float32)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    dev_W = torch.from_numpy(Wf).to("cuda", tdt)
+    out = torch.full((C, numel), 7.0, dtype=tdt, device="cuda")
+    remap = torch.empty(E, dtype=torch.int32, device="cuda")
+    F.merge_experts(dev_W, torch.from_numpy(cl).cuda(), torch.from_numpy(alpha).cuda(), C, out, remap)
+    got = out.float().cpu().numpy().astype(np.float64)
+    assert np.all(got[2] == 0.0)                   # the empty cluster: zeros
+    live = [c for c in range(C) if sizes[c] > 0]   # the oracle rejects empty clusters: relabel the rest
+    relabel = {c: j for j, c in enumerate(live)}
+    cl_live = np.array([relabel.get(int(c), -1) if c >= 0 else -1 for c in cl], np.int32)
+    ref, _ = oracle.merge(Wf.astype(np.float64), cl_live, alpha.astype(np.float64), len(live))
+    tol = 1e-5 if dtype == "f32" else 2e-2
+    for j, c in enumerate(live):
+        mem = np.nonzero(cl == c)[0]
+        wts = alpha[mem].astype(np.float64) / alpha[mem].astype(np.float64).sum()
+        absw = (wts[:, None] * np.abs(Wf[mem].astype(np.float64))).sum(0)
+        assert np.all(np.abs(got[c] - ref[j]) <= tol * absw + 1e-30), c
+        if sizes[c] == 1:
+            assert np.array_equal(got[c], Wf[mem[0]].astype(np.float64))  # singleton: bit for bit
+        if dtype == "bf16":
+            assert np.mean(got[c] == oracle.bf16_round(ref[j])) > 0.99
+
+
 def test_quantizer_ties_and_extremes_bit_exact():
     """Half-integer quotients (ties to even), saturation, zero and tiny groups: the GPU quantizer's
     reciprocal fast path must fall back to the IEEE division exactly where it matters."""
