@@ -289,7 +289,6 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
     comm = F.Comm(uid, world, rank)
 
     def step(xs, before_chunk=None, after_chunk=None):
-        report_budgets()                                          # the previous round's eq.(1), host side
         if args.clustering == "pca":                              # §5.2 C1 (reads the masters only)
             feats, _, _ = expert_features_model(masters, d_feat)
         qm.quantize_from(masters)                                 # a0
@@ -302,6 +301,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
             torch.cuda.nvtx.range_pop()
             if after_chunk:
                 after_chunk(c)
+        report_budgets()  # the previous round's eq.(1) on the host, once this round's profiling is enqueued
         comm.reduce_stats(prof.hist)                              # a7
         if attn is None:                                          # α = f = hist / T, on the device
             F.frequencies(prof.hist, float(T_total), alpha)
@@ -323,7 +323,11 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
         state["merged"] = merge_model(masters, alpha, state["cluster_of"], n_cl, state["merged"])  # a8, eq.(2)
 
     def report_budgets():
-        """a8-pre, eq.(1) on the host from the last round's reduced histogram (uniform mode: the report)."""
+        """a8-pre, eq.(1) on the host from the last round's reduced histogram (uniform mode: the report).
+        Called after this round's profiling launches are enqueued: the wait on the last round's histogram
+        event then never starves the GPU of queued work (called at the top of the step, it held the host
+        until the previous round's profiling had finished, and the launches of the features + quantize
+        phase could not stay ahead of the GPU: LLaMA shape 26 ms of idle GPU per step)."""
         if state.get("hist_pending"):
             ev_hist.synchronize()
             state["C"], _ = budgets(hist_host.numpy(), T_total, C * L)

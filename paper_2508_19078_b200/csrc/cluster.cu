@@ -29,30 +29,35 @@ namespace {
 constexpr int kBM = 128, kBK = 64, kMaxE = 128;
 constexpr int kMaxFam = 4;
 constexpr int kGramInflight = 128 * 1024;  // bytes of expert data in flight per SM (HBM latency x bandwidth / SM)
-constexpr int kSlices = 4;                 // 64-column slices per stage: each row streams 512 contiguous bytes
+// 64-column slices per stage: each row streams 512 contiguous bytes (1 KB for 16 experts, whose eight
+// slices make one 128-row MMA operand)
+constexpr int slices_of(int npad) { return npad <= 16 ? 8 : 4; }
 constexpr int kSubStages = 8;              // TMEM accumulation sub-chunk (32 slices = 128 MMAs), then drained
 constexpr int kChunkSlices = 64;           // work unit claimed dynamically; one partial slot each
-constexpr int kChunkStages = kChunkSlices / kSlices;
 constexpr int kRing = 8;                   // claimed-chunk ring (producer -> MMA, epilogue)
 
 struct GramMaps {
   CUtensorMap map[kMaxFam];   // family f of this layer: bf16 [E][P_f], box {64 cols, NPAD rows}
-  CUtensorMap map4[kMaxFam];  // the same family as [P_f/64 blocks][E][64]: box {64, NPAD, kSlices} = one stage
+  CUtensorMap map4[kMaxFam];  // the same family as [P_f/64 blocks][E][64]: box {64, NPAD, slices} = one stage
   int64_t kb_end[kMaxFam];    // cumulative 64-column slice counts
   int64_t nblk[kMaxFam];      // whole 64-column blocks of family f (map4's outer extent)
   int n_fam;
 };
 
-template <int NPAD, int INFL>
+// GRP = slices per MMA (1, or 128 / NPAD when consecutive slices are paired, see gram_kernel)
+template <int NPAD, int INFL, int GRP>
 struct GramCfg {
   static constexpr int kSlice = NPAD * kBK * 2;  // NPAD expert rows x 64 columns (128 B rows)
-  static constexpr int kTile = kSlices * kSlice;
+  static constexpr int kSl = slices_of(NPAD);
+  static constexpr int kTile = kSl * kSlice;
   static constexpr int kStages = INFL / kTile < 3 ? 3 : (INFL / kTile < 16 ? INFL / kTile : 16);
   // The MMA reads M=128 rows from a slice; rows >= NPAD only feed accumulator rows that are never
   // stored, but they must be readable shared memory: pad the ring by the overhang.
   static constexpr int kPad = (kBM - NPAD) * 128;
   static constexpr int kBarriers = 2 * kStages + 4 + 2 * kRing;
-  static constexpr int kBytes = kStages * kTile + kPad + 1024 + kBarriers * 8 + kRing * 4 + 64;
+  static constexpr int kAccCols = GRP > 1 ? kBM : NPAD;  // accumulator columns (N of the MMA)
+  static constexpr int kXBytes = (GRP - 1) * NPAD * (NPAD + 1) * 4;  // cross-block sums of the epilogue
+  static constexpr int kBytes = kStages * kTile + kPad + 1024 + kBarriers * 8 + kRing * 4 + 64 + kXBytes;
 };
 
 // Split-K Gram of one layer.  The concatenated 64-column slices of every family form chunks of
@@ -64,10 +69,21 @@ struct GramCfg {
 // therefore accumulates sub-chunks of 128 MMAs (two buffers: the MMAs of sub-chunk c+1 overlap the
 // drain of c) and the epilogue sums the sub-chunks of a chunk in registers.
 // The counter is reset by gram_reduce_kernel, which runs after this kernel on the same stream.
-template <int NPAD, int INFL>
+//
+// Paired slices (GRP = 128/NPAD > 1, NPAD 64, 32 or 16): a stage holds kSlices consecutive [NPAD][64]
+// slices, so GRP of them form one 128-row K-major operand.  One M=128, N=128 MMA with that operand as
+// both A and B computes all GRP x GRP slice products; the GRP diagonal NPAD x NPAD blocks are the
+// wanted X_s X_sᵀ (the rest is never read).  Versus one M=128, N=NPAD MMA per slice (whose A rows
+// beyond NPAD are the next slice's, read for nothing) this halves the MMAs' shared-memory operand reads
+// per byte of X (the kernel's bound, ~18 B per SM clock), and the epilogue sums the GRP blocks of
+// a chunk in a fixed order (deterministic).  Needs every stage's slice count to be a multiple of GRP
+// (the launcher checks the layer's total).
+template <int NPAD, int INFL, int GRP>
 __global__ void __launch_bounds__(192, 1)
     gram_kernel(const __grid_constant__ GramMaps gm, int E, float* __restrict__ partial, int* __restrict__ counter) {
-  using C = GramCfg<NPAD, INFL>;
+  using C = GramCfg<NPAD, INFL, GRP>;
+  constexpr int kSlices = C::kSl;
+  static_assert(kSlices % GRP == 0 && kChunkSlices % kSlices == 0 && GRP * NPAD <= kBM, "slice pairing");
   constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still a shared-space pointer
@@ -79,7 +95,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* chunk_empty = chunk_full + kRing;
   int* ring = reinterpret_cast<int*>(chunk_empty + kRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
-  constexpr uint32_t kCols = NPAD <= 16 ? 32 : (NPAD <= 32 ? 64 : (NPAD <= 64 ? 128 : 256));  // two accumulators
+  constexpr uint32_t kCols = 2 * C::kAccCols <= 32 ? 32 : 2 * C::kAccCols;  // two accumulators
+  float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 64);  // [GRP-1][NPAD][NPAD+1]
   const int warp = warp_id();
   const int64_t n_kb = gm.kb_end[gm.n_fam - 1];
   const int n_chunks = (int)((n_kb + kChunkSlices - 1) / kChunkSlices);
@@ -152,7 +169,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = umma_idesc_bf16(kBM, NPAD);
+    constexpr uint32_t idesc = umma_idesc_bf16(kBM, C::kAccCols);
     int gs = 0, gc = 0;  // stages consumed, sub-chunks accumulated
     for (int j = 0;; ++j) {
       const int r = j % kRing;
@@ -173,8 +190,8 @@ __global__ void __launch_bounds__(192, 1)
         if (elect_one()) {
           const int64_t left = n_kb - kb_base - (int64_t)st * kSlices;
           const int n_sl = left < kSlices ? (int)left : kSlices;
-          const uint32_t d = tmem + b * NPAD;
-          for (int t = 0; t < n_sl; ++t) {
+          const uint32_t d = tmem + b * C::kAccCols;
+          for (int t = 0; t < n_sl; t += GRP) {
             const uint64_t desc = umma_desc_sw128(smem_u32(smem + s * C::kTile + t * C::kSlice));
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k)
@@ -190,6 +207,8 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     const int q = warp & 3;
     const int row = q * 32 + lane_id();
+    const int blk = row / NPAD, er = row % NPAD;  // paired slices: diagonal block and its expert row
+    const bool live = GRP > 1 ? (q * 32) % NPAD < E : q * 32 < E;  // warp-uniform
     int gc = 0;
     for (int j = 0;; ++j) {
       const int r = j % kRing;
@@ -204,11 +223,22 @@ __global__ void __launch_bounds__(192, 1)
         const int b = gc & 1;
         mbar_wait(&acc_full[b], (gc >> 1) & 1);
         tc_fence_after();
-        if (q * 32 < E) {
+        if constexpr (GRP > 1 && NPAD < 32) {
+          // 16-row blocks: lanes 0-15 and 16-31 of a warp are rows of two blocks (columns must be
+          // warp-uniform in tcgen05.ld): load both blocks' columns, each lane keeps its own
+          float v[16], w[16];
+          const uint32_t a = tmem + ((uint32_t)(q * 32) << 16) + b * C::kAccCols + (q * 32 / NPAD) * NPAD;
+          tmem_ld16(a, v);
+          tmem_ld16(a + 16, w);
+          tmem_ld_wait();
+          const bool hi = lane_id() >= 16;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] += hi ? w[i] : v[i];
+        } else if (live) {
 #pragma unroll
           for (int col = 0; col < NPAD; col += 16) {
             float v[16];
-            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * NPAD + col, v);
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * C::kAccCols + (GRP > 1 ? blk * NPAD : 0) + col, v);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) acc[col + i] += v[i];
@@ -219,10 +249,27 @@ __global__ void __launch_bounds__(192, 1)
         if (lane_id() == 0) mbar_arrive(&acc_empty[b]);
       }
       float* out = partial + (int64_t)id * E * E;
-      if (row < E)
+      if constexpr (GRP > 1) {
+        // block sums in a fixed order: block 0's rows add blocks 1..GRP-1 (row stride NPAD+1: no conflicts)
+        if (blk > 0 && live)
+#pragma unroll
+          for (int i = 0; i < NPAD; ++i) xbuf[((blk - 1) * NPAD + er) * (NPAD + 1) + i] = acc[i];
+        named_bar_sync(1, 128);
+        if (blk == 0 && er < E) {
+#pragma unroll
+          for (int gb = 1; gb < GRP; ++gb)
+#pragma unroll
+            for (int i = 0; i < NPAD; ++i) acc[i] += xbuf[((gb - 1) * NPAD + er) * (NPAD + 1) + i];
+#pragma unroll
+          for (int i = 0; i < NPAD; ++i)
+            if (i < E) out[er * E + i] = acc[i];
+        }
+        named_bar_sync(1, 128);  // xbuf is rewritten by the next chunk
+      } else if (row < E) {
 #pragma unroll
         for (int i = 0; i < NPAD; ++i)
           if (i < E) out[row * E + i] = acc[i];
+      }
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&chunk_empty[r]);
     }
@@ -498,13 +545,13 @@ int* features_counter(void* ws, int L, int E, int n_fam, const int64_t* P) {
   return reinterpret_cast<int*>((p + 15) & ~uintptr_t(15));
 }
 
-template <int NPAD>
+template <int NPAD, int GRP = 1>
 static cudaError_t launch_gram_n(const GramMaps& gm, int E, float* partial, int* counter, int grid, cudaStream_t st) {
-  const int smem = GramCfg<NPAD, kGramInflight>::kBytes;
+  const int smem = GramCfg<NPAD, kGramInflight, GRP>::kBytes;
   cudaError_t e =
-      cudaFuncSetAttribute(gram_kernel<NPAD, kGramInflight>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(gram_kernel<NPAD, kGramInflight, GRP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  gram_kernel<NPAD, kGramInflight><<<grid, 192, smem, st>>>(gm, E, partial, counter);
+  gram_kernel<NPAD, kGramInflight, GRP><<<grid, 192, smem, st>>>(gm, E, partial, counter);
   return cudaGetLastError();
 }
 
@@ -522,20 +569,27 @@ cudaError_t launch_gram(int E, int n_fam, const void* const* X, const int64_t* P
                       (uint64_t)P[f] * 2, 64, (uint32_t)npad, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
     gm.nblk[f] = P[f] / kBK;
-    if (gm.nblk[f] >= kSlices &&
-        !make_tmap_gram_blocks(&gm.map4[f], X[f], (uint64_t)E, (uint64_t)P[f], (uint32_t)npad, kSlices))
+    if (gm.nblk[f] >= slices_of(npad) &&
+        !make_tmap_gram_blocks(&gm.map4[f], X[f], (uint64_t)E, (uint64_t)P[f], (uint32_t)npad, slices_of(npad)))
       return cudaErrorInvalidValue;
-    if (gm.nblk[f] < kSlices) gm.nblk[f] = 0;  // too short for a whole stage: per-slice loads only
+    if (gm.nblk[f] < slices_of(npad)) gm.nblk[f] = 0;  // too short for a whole stage: per-slice loads only
     acc += (P[f] + kBK - 1) / kBK;
     gm.kb_end[f] = acc;
   }
   const int64_t chunks = gram_chunks(n_fam, P);
   const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
   *n_slots = (int)chunks;
+  // paired slices when every stage's slice count is a multiple of the pair size: stages hold
+  // slices_of(npad) slices except at a chunk's end (chunks are kChunkSlices, a multiple of 8) and the
+  // layer's end
+  const int64_t n_kb = gm.kb_end[n_fam - 1];
   switch (npad) {
-    case 16: return launch_gram_n<16>(gm, E, partial, counter, grid, st);
-    case 32: return launch_gram_n<32>(gm, E, partial, counter, grid, st);
-    case 64: return launch_gram_n<64>(gm, E, partial, counter, grid, st);
+    case 16: return n_kb % 8 == 0 ? launch_gram_n<16, 8>(gm, E, partial, counter, grid, st)
+                                  : launch_gram_n<16>(gm, E, partial, counter, grid, st);
+    case 32: return n_kb % 4 == 0 ? launch_gram_n<32, 4>(gm, E, partial, counter, grid, st)
+                                  : launch_gram_n<32>(gm, E, partial, counter, grid, st);
+    case 64: return n_kb % 2 == 0 ? launch_gram_n<64, 2>(gm, E, partial, counter, grid, st)
+                                  : launch_gram_n<64>(gm, E, partial, counter, grid, st);
     default: return launch_gram_n<128>(gm, E, partial, counter, grid, st);
   }
 }

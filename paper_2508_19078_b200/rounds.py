@@ -13,8 +13,9 @@ Here a round is:
                   pass and the optimizer are outside this path, as is the server's
                   aggregation, whose waiting time is what stale profiling hides on a participant.
   serial (Fig. 7a): profile -> merge(f^r) -> fine-tune, one stream.
-  stale  (Fig. 7b): foreground stream (high priority): merge(f^{r-1}) -> fine-tune;
-                    background stream (low priority): profile -> f^r for the next round.
+  stale  (Fig. 7b): foreground stream: merge(f^{r-1}) -> fine-tune;
+                    background stream: profile -> f^r for the next round, once fine-tuning is done
+                    (during the aggregation wait).
 Both are measured with CUDA events on their streams: the fine-tuning start latency (round start ->
 merged model ready) and the GPU span of the round.
 
@@ -23,7 +24,7 @@ the server ... the participant is idle"): after fine-tuning, the participant upl
 for the aggregated model; that wait W is modelled (agg_wait_s, an input — the paper gives no number) as
 an idle period on the host.  Serial: profile -> merge -> fine-tune -> wait W.  Stale: merge(f^{r-1}) ->
 fine-tune -> wait W on the foreground while the background profile of w_r runs on the GPU, so the
-profile hides inside the wait.  The makespan is host wall-clock from the round start until both the
+profile hides inside the wait (makespan = fine-tune + W when the profile is shorter than W).  The makespan is host wall-clock from the round start until both the
 wait and every GPU stream are done.  Buffers and sequencing only; all arithmetic is in libflux.
 """
 from __future__ import annotations
@@ -125,8 +126,12 @@ class Participant:
         e0.record(self.fg)
         self.merge_and_finetune(self.fg, em)  # foreground first: uses f^{r-1} (self.alpha, self.cluster_of)
         efg.record(self.fg)
-        self.bg.wait_event(e0)
-        self.profile(self.bg)                 # background: f^r for the next round
+        # background: f^r for the next round, started once fine-tuning is done, i.e. inside the wait.  The
+        # expert GEMMs and K1 are persistent kernels that hold every SM until they finish, so a stream
+        # priority cannot keep a concurrent profile from stretching the fine-tuning (measured: fine-tuning
+        # done 0.25-0.65 s after the round start depending on the interleaving, vs ~0.2 s alone)
+        self.bg.wait_event(efg)
+        self.profile(self.bg)
         ebg.record(self.bg)
         efg.synchronize()                     # fine-tuning done: upload, wait for the aggregated model
         time.sleep(self.agg_wait_s)

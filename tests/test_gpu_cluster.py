@@ -43,7 +43,9 @@ def _score_gram(F):
 
 @pytest.mark.parametrize("E,sizes,d", [(16, [4096, 1000, 8], 8), (64, [20000, 7704], 16), (7, [640], 6),
                                        (64, [64 * 148 * 3 + 72], 16), (128, [12000, 3000, 800, 64], 24),
-                                       (100, [9000], 32), (33, [4096 * 40 + 8], 12)])
+                                       (100, [9000], 32), (33, [4096 * 40 + 8], 12),
+                                       (32, [64 * 400], 12), (20, [64 * 202 + 8], 8), (24, [64 * 301, 64 * 99], 8),
+                                       (16, [64 * 400], 8), (12, [64 * 100, 64 * 100], 6)])
 def test_gram_features_vs_oracle(E, sizes, d):
     import paper_2508_19078_b200 as F
     rng = np.random.default_rng(100 + E + len(sizes))
