@@ -20,8 +20,11 @@ __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
 }
 
 // EMPTY: picks may be empty (pos -1, folded by gate re-routing, NEXT-2).  The plain path keeps
-// every load unconditional so all (k + 2) x 2 loads issue before any is used.
-template <bool EMPTY>
+// every load unconditional so all (k + 2) x U loads issue before any is used.  U = 16-byte chunks per
+// lane per iteration: 2, or 4 when a token has few source rows (k <= 4 and k + residual + shared <= 6,
+// e.g. the LLaMA shape's k = 4 without shared experts), so a warp keeps about the same bytes in flight;
+// KMAX sizes the per-pick arrays (registers).
+template <bool EMPTY, int U, int KMAX>
 __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, const uint4* __restrict__ residual,
                                                       const uint4* __restrict__ y_sh, const uint4* __restrict__ y_perm,
                                                       const float* __restrict__ w, const int32_t* __restrict__ inv_pos,
@@ -30,10 +33,10 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
   if (t >= T) return;
   const int lane = threadIdx.x & 31;
   const int nvec = H / 8;
-  int pos[8];
-  float wt[8];
+  int pos[KMAX];
+  float wt[KMAX];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < KMAX; ++j) {
     pos[j] = 0;
     wt[j] = 0.f;
     if (j < k) {
@@ -41,23 +44,23 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
       wt[j] = __ldg(&w[t * k + j]);
     }
   }
-  // two 16-byte chunks per lane per iteration: all (k + 2) x 2 loads are issued before any is used
-  for (int c0 = lane; c0 < nvec; c0 += 64) {
-    uint4 rv[2], sv[2], ov[8][2];
-    bool has[2];
+  // U 16-byte chunks per lane per iteration: all loads are issued before any is used
+  for (int c0 = lane; c0 < nvec; c0 += 32 * U) {
+    uint4 rv[U], sv[U], ov[KMAX][U];
+    bool has[U];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int c = c0 + 32 * u;
       has[u] = c < nvec;
       if (!has[u]) continue;
       rv[u] = __ldg(&residual[t * nvec + c]);
       if (y_sh) sv[u] = __ldg(&y_sh[t * nvec + c]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < KMAX; ++j)
         if (j < k && (!EMPTY || pos[j] >= 0)) ov[j][u] = __ldcs(&y_perm[(int64_t)pos[j] * nvec + c]);  // streaming
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       if (!has[u]) continue;
       float acc[8], f[8];
       unpack8(rv[u], acc);
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t T, int H, int k, c
         for (int i = 0; i < 8; ++i) acc[i] += f[i];
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < KMAX; ++j) {
         if (j < k && (!EMPTY || pos[j] >= 0)) {  // pos -1: a pick folded by gate re-routing
           unpack8(ov[j][u], f);
 #pragma unroll
@@ -89,12 +92,11 @@ cudaError_t launch_combine(int64_t T, int H, int k, const void* residual, const 
                            const float* w, const int32_t* inv_pos, void* y, cudaStream_t st, bool empty_picks) {
   if (T == 0) return cudaSuccess;
   const unsigned grid = (unsigned)((T + 7) / 8);
-  if (empty_picks)
-    combine_kernel<true><<<grid, 256, 0, st>>>(T, H, k, (const uint4*)residual, (const uint4*)y_sh,
-                                               (const uint4*)y_perm, w, inv_pos, (uint4*)y);
-  else
-    combine_kernel<false><<<grid, 256, 0, st>>>(T, H, k, (const uint4*)residual, (const uint4*)y_sh,
-                                                (const uint4*)y_perm, w, inv_pos, (uint4*)y);
+  const bool wide = k <= 4 && k + 1 + (y_sh ? 1 : 0) <= 6;
+  auto kern = empty_picks ? (wide ? combine_kernel<true, 4, 4> : combine_kernel<true, 2, 8>)
+                          : (wide ? combine_kernel<false, 4, 4> : combine_kernel<false, 2, 8>);
+  kern<<<grid, 256, 0, st>>>(T, H, k, (const uint4*)residual, (const uint4*)y_sh, (const uint4*)y_perm, w, inv_pos,
+                             (uint4*)y);
   return cudaGetLastError();
 }
 
