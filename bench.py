@@ -226,9 +226,11 @@ def run_reference(args, cfg, rank, world, T_rank):
 
 
 # ------------------------------------------------------------------------------------------ algorithmic bytes
-def kernel_bytes(cfg, T, C, n_chunks_T):
+def kernel_bytes(cfg, T, C, n_chunks_T, fused_bops=False):
     """Algorithmic HBM bytes per step of each HBM-bound kernel, for T tokens
-    per rank per step.  Keys are flux_kernel_name()s."""
+    per rank per step in n_chunks_T profiling calls per layer.  fused_bops: the quantizer also writes the
+    bf16 B operands (flux_quantize_weights_bops) and no dequantization pass runs.  Keys are
+    flux_kernel_name()s."""
     L, E, H, F, Fs, k = cfg.n_layers, cfg.n_experts, cfg.hidden, cfg.ffn, cfg.shared_ffn, cfg.top_k
     n_w = E * 3 * F * H + 3 * Fs * H                           # quantized weights per layer
     per_w_q = {8: 1.0, 4: 0.5, 2: 0.25}[cfg.wbits]             # code bytes per weight
@@ -238,8 +240,9 @@ def kernel_bytes(cfg, T, C, n_chunks_T):
         "router": L * T * (2 * H + 12 * k),                     # read x, write ids / w / rank
         "permute": L * T * 16 * k,                               # K2: read ids + rank, write inv_pos + token_index
         "combine": L * T * (k * H * 2 + 8 * k + H * 2 * (3 if Fs else 2)),
-        "dequant": L * n_w * (per_w_q + sc + 2.0),              # read codes (+ scales), write bf16
-        "quantize": L * n_w * (2.0 + per_w_q + sc),             # read bf16 masters, write codes + scales
+        "dequant": n_chunks_T * L * n_w * (per_w_q + sc + 2.0),  # per profiling call: read codes (+ scales), write bf16
+        "quantize": L * n_w * (2.0 + per_w_q + sc + (2.0 if fused_bops else 0.0)),  # read masters, write codes + scales
+                                                                                     # (+ the bf16 B operands)
         "merge": L * 3 * F * H * 2 * (E + C),                   # read Σ|W_e|, write Σ|W_c|
         "gram": L * E * 3 * F * H * 2,                          # read every master parameter once
     }
@@ -268,7 +271,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
 
     # ---- setup (not timed): synthetic master weights, this rank's token shard, buffers, NCCL comm
     masters = synthetic.master_weights(cfg)
-    qm = QuantizedModel(shape)
+    qm = QuantizedModel(shape, with_bops=args.fused_dequant == "on")
     prof = Profiler(shape, Tc, with_de=True, policy=F.make_policy(gemm_chain={"auto": 0, "off": 1, "on": 2}[args.chain]))
     t0, _ = shard(rank, world, T_rank)  # this rank's contiguous slice of the global token stream
     x = synthetic.tokens(cfg, t0, T_rank)
@@ -344,7 +347,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
 
     clocks = ClockSampler(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
                                        else "/tmp", f"clocks_rank{rank}.csv"))
-    if rank == 0:
+    if rank == 0 and not os.environ.get("FLUX_BENCH_NO_CLOCKS"):  # diagnostics only: the line then has no clocks
         clocks.start()
     F.timing_read(reset=True)
     F.timing_enable(True)
@@ -438,7 +441,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
     report_budgets()
     out = {"ms": ms, "ms_e2e": ms_e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "kern": kern, "clk": clk,
            "gemm_mhz": gemm_mhz,
-           "T_rank": T_rank, "Tc": Tc, "n_chunks": n_chunks, "C": C, "budget_C": [int(c) for c in state["C"]],
+           "T_rank": T_rank, "Tc": Tc, "n_chunks": n_chunks, "fused_bops": qm.bops is not None, "C": C, "budget_C": [int(c) for c in state["C"]],
            "steps": steps}
 
     # ---- merge quality of the round's merged model (not timed): the paper's output error —
@@ -537,7 +540,7 @@ def kernel_table(cfg, res, peaks):
     peak and the north star's ~8 TB/s."""
     hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
     steps = res["steps"]
-    by = kernel_bytes(cfg, res["T_rank"], res["C"], res["n_chunks"])
+    by = kernel_bytes(cfg, res["T_rank"], res["C"], res["n_chunks"], res.get("fused_bops", False))
     # DRAM read + write bytes per launch from the committed `ncu --set full` captures (profiles/traffic.json)
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = json.load(open(tp)) if os.path.exists(tp) else {}
@@ -593,6 +596,10 @@ def main():
                     help="comma-separated extra workloads measured in the same run (N = 1 only; '' = none)")
     ap.add_argument("--chain", default="auto", choices=["auto", "on", "off"],
                     help="flux_policy.gemm_chain: gate/up + down GEMMs in one launch (on) or two (off)")
+    ap.add_argument("--fused-dequant", default="on", choices=["on", "off"],
+                    help="on: the quantizer writes every layer's bf16 B operands in the same pass "
+                         "(flux_quantize_weights_bops, ~1.1 GB per DeepSeek-shape layer of HBM); off: one "
+                         "dequantization pass per flux_profile_layer call")
     ap.add_argument("--selftest-launcher", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     maybe_relaunch(args)
@@ -650,7 +657,8 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
-            "config": workload_config(cfg, T_rank, world, args.scaling, res["Tc"]),
+            "config": dict(workload_config(cfg, T_rank, world, args.scaling, res["Tc"]),
+                           dequant="fused into the quantizer" if res["fused_bops"] else "one pass per profiling call"),
             "roofline": roofline_gemm(cfg, T_rank, res, peaks, peak_src),
             "e2e": {"value": T_total * args.steps / (res["ms_e2e"] / 1000.0), "unit": "tokens/s",
                     "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"]},

@@ -315,6 +315,36 @@ flux_status flux_comm_destroy(flux_comm* comm);
 flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype in_dtype, const void* w, int64_t R,
                                   int64_t K, void* q, float* s, void* stream);
 
+/* The quantized model's bf16 B operands ("bops"): on the dequant-pass path
+ * (flux_profile_layer_uses_bops == 1) the expert GEMMs stream a layer's weights as bf16,
+ * ŵ = bf16(q·bf16(s)) for grouped codes and bf16(q) per channel (scale in the GEMM epilogue) —
+ * reading R1b.  flux_profile_layer materialises them in its workspace with one dequantization
+ * pass per call; a caller that quantizes once and profiles many times (every chunk of a round) can
+ * instead produce them with the quantizer and hand them in.  A layer's bops buffer is
+ * flux_layer_bops_bytes(cfg) bytes, 16-byte aligned, layout private to the library; rows that pad
+ * F to a multiple of 128 are never written or read as data (zero the buffer once if it must be
+ * deterministic bytewise).
+ *   flux_quantize_weights_bops   one weight family of n_layers consecutive layers, quantized exactly
+ *       as flux_quantize_weights does (w, q, s: the family's [n_layers·rows][K] matrices) AND written
+ *       into bops + l·bops_stride as B operands in the same pass (the bytes flux_dequantize_layer
+ *       would write from q and s).  family: FLUX_FAM_*; rows x K = [E·F][H] (gate, up), [E·H][F]
+ *       (down), [F_s][H] / [H][F_s] (shared).  wbits 2, 4 or 8.
+ *   flux_dequantize_layer         the dequantization pass alone: w's q, s -> bops.
+ *   flux_profile_layer_bops       flux_profile_layer_ex with this layer's bops (NULL = dequantize in
+ *       the workspace as usual); bit-identical outputs.  ws >= flux_profile_layer_workspace_bops.
+ *   flux_profile_layer_uses_bops  1 / 0: whether T tokens take the dequant-pass path; -1 invalid. */
+enum { FLUX_FAM_GATE = 0, FLUX_FAM_UP = 1, FLUX_FAM_DOWN = 2, FLUX_FAM_SH_GATE = 3, FLUX_FAM_SH_UP = 4, FLUX_FAM_SH_DOWN = 5 };
+size_t flux_layer_bops_bytes(const flux_moe_cfg* cfg);
+flux_status flux_quantize_weights_bops(const flux_moe_cfg* cfg, int32_t family, flux_dtype in_dtype, const void* w,
+                                       int32_t n_layers, void* q, float* s, void* bops, size_t bops_stride,
+                                       void* stream);
+flux_status flux_dequantize_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, void* bops, void* stream);
+int32_t flux_profile_layer_uses_bops(const flux_moe_cfg* cfg, const flux_policy* policy, int64_t T);
+size_t flux_profile_layer_workspace_bops(const flux_moe_cfg* cfg, const flux_policy* policy, int64_t T);
+flux_status flux_profile_layer_bops(const flux_moe_cfg* cfg, const flux_policy* policy, const flux_qlayer* w,
+                                    const void* bops, const void* x, const void* residual, int64_t T,
+                                    const flux_layer_out* out, void* ws, size_t ws_bytes, void* stream);
+
 /* Adaptive expert layer size, eq.(1), reading R9 (host function):
  *   f_l = hist[l][·]/T, v_l = population variance of f_l, b_l = (L-l+1)/max(v_l,1e-12) (l = 1..L),
  *   C_l = clamp(floor(b_l/Σ_k b_k · B_non), 1, n_non[l]).

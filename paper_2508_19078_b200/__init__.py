@@ -96,6 +96,16 @@ def _lib():
         L.flux_profile_layer_workspace_ex.restype = SZ
         L.flux_profile_layer_ex.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(Policy), ctypes.POINTER(QLayer),
                                             P, P, I64, ctypes.POINTER(LayerOut), P, SZ, P]
+        L.flux_layer_bops_bytes.argtypes = [ctypes.POINTER(MoECfg)]
+        L.flux_layer_bops_bytes.restype = SZ
+        L.flux_quantize_weights_bops.argtypes = [ctypes.POINTER(MoECfg), I32, ctypes.c_int, P, I32, P, P, P, SZ, P]
+        L.flux_dequantize_layer.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(QLayer), P, P]
+        L.flux_profile_layer_uses_bops.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(Policy), I64]
+        L.flux_profile_layer_uses_bops.restype = I32
+        L.flux_profile_layer_workspace_bops.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(Policy), I64]
+        L.flux_profile_layer_workspace_bops.restype = SZ
+        L.flux_profile_layer_bops.argtypes = [ctypes.POINTER(MoECfg), ctypes.POINTER(Policy), ctypes.POINTER(QLayer),
+                                              P, P, P, I64, ctypes.POINTER(LayerOut), P, SZ, P]
         L.flux_merge_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
         L.flux_quantize_weights.argtypes = [I32, I32, ctypes.c_int, P, I64, I64, P, P, P]
         L.flux_compact_experts.argtypes = [ctypes.c_int, I32, I64, P, P, P, I32, P, P, P]
@@ -114,7 +124,8 @@ def _lib():
         L.flux_comm_init.argtypes = [ctypes.POINTER(P), P, I32, I32]
         L.flux_reduce_stats.argtypes = [P, P, SZ, P]
         L.flux_comm_destroy.argtypes = [P]
-        for f in ("flux_profile_layer", "flux_profile_layer_ex", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
+        for f in ("flux_profile_layer", "flux_profile_layer_ex", "flux_profile_layer_bops", "flux_dequantize_layer",
+                  "flux_quantize_weights_bops", "flux_merge_experts", "flux_quantize_weights", "flux_layer_budget",
                   "flux_expert_features", "flux_cluster_experts", "flux_compact_experts", "flux_output_error",
                   "flux_merge_experts_batch", "flux_frequencies",
                   "flux_attention_hist",
@@ -282,6 +293,49 @@ def quantize_weights(w, wbits: int, group_size: int, q, s, stream=None):
     R = w.numel() // K
     st = _lib().flux_quantize_weights(wbits, group_size, dt, _ptr(w), R, K, _ptr(q), _ptr(s), _stream(stream))
     _check(st, "flux_quantize_weights")
+
+
+FAM_GATE, FAM_UP, FAM_DOWN, FAM_SH_GATE, FAM_SH_UP, FAM_SH_DOWN = range(6)
+
+
+def layer_bops_bytes(cfg: MoECfg) -> int:
+    """Bytes of one layer's bf16 B operands (flux_layer_bops_bytes)."""
+    return int(_lib().flux_layer_bops_bytes(ctypes.byref(cfg)))
+
+
+def quantize_weights_bops(cfg: MoECfg, family: int, w, n_layers: int, q, s, bops, stream=None):
+    """flux_quantize_weights_bops: quantize one family of n_layers layers (w [n_layers·rows][K]) into q, s and
+    write each layer's bf16 B operands of that family into bops [n_layers][layer_bops_bytes] (uint8 CUDA)."""
+    dt = FLUX_FP32 if w.dtype == torch.float32 else FLUX_BF16
+    st = _lib().flux_quantize_weights_bops(ctypes.byref(cfg), family, dt, _ptr(w), n_layers, _ptr(q), _ptr(s),
+                                           _ptr(bops), bops.stride(0) * bops.element_size(), _stream(stream))
+    _check(st, "flux_quantize_weights_bops")
+
+
+def dequantize_layer(cfg: MoECfg, qlayer: QLayer, bops, stream=None):
+    """flux_dequantize_layer: the layer's bf16 B operands from its q, s into bops (uint8 CUDA tensor)."""
+    _check(_lib().flux_dequantize_layer(ctypes.byref(cfg), ctypes.byref(qlayer), _ptr(bops), _stream(stream)),
+           "flux_dequantize_layer")
+
+
+def profile_layer_uses_bops(cfg: MoECfg, T: int, policy: Policy | None = None) -> bool:
+    r = int(_lib().flux_profile_layer_uses_bops(ctypes.byref(cfg), _pol(policy), T))
+    if r < 0:
+        raise ValueError("flux_profile_layer_uses_bops: invalid arguments")
+    return r == 1
+
+
+def profile_layer_workspace_bops(cfg: MoECfg, T: int, policy: Policy | None = None) -> int:
+    return int(_lib().flux_profile_layer_workspace_bops(ctypes.byref(cfg), _pol(policy), T))
+
+
+def profile_layer_bops(cfg: MoECfg, qlayer: QLayer, bops, x, residual, T: int, out: LayerOut, ws, stream=None,
+                       policy: Policy | None = None):
+    """flux_profile_layer_bops: profile_layer with this layer's B operands already dequantized."""
+    st = _lib().flux_profile_layer_bops(ctypes.byref(cfg), _pol(policy), ctypes.byref(qlayer), _ptr(bops), _ptr(x),
+                                        _ptr(residual), T, ctypes.byref(out), _ptr(ws),
+                                        ws.numel() * ws.element_size() if ws is not None else 0, _stream(stream))
+    _check(st, "flux_profile_layer_bops")
 
 
 def layer_budget(hist, T: int, B_non: int, n_non=None):

@@ -172,7 +172,26 @@ int pad128(int v) { return (v + 127) / 128 * 128; }
 // The tensor maps keep the logical width F, so the pad columns are never read (no zeroing needed).
 int pad64(int v) { return (v + 63) / 64 * 64; }
 
-WsPlan plan(const flux_moe_cfg& c, const Policy& pol, int64_t T) {
+// The bf16 B operands of one layer (the dequantization pass's output).  The caller-owned buffer of
+// flux_quantize_weights_bops / flux_dequantize_layer / flux_profile_layer_bops has this layout,
+// sized by flux_layer_bops_bytes.
+struct BopsPlan {
+  size_t gu_r, dn_r, gu_s, dn_s, total;
+};
+BopsPlan bops_plan(const flux_moe_cfg& c, bool present = true) {
+  Layout L;
+  BopsPlan b;
+  const size_t on = present ? 1 : 0;
+  b.gu_r = L.take(on * 2ull * c.n_experts * 2 * pad128(c.ffn) * c.hidden);
+  b.dn_r = L.take(on * 2ull * c.n_experts * c.hidden * pad64(c.ffn));
+  b.gu_s = L.take(on * 2ull * 2 * pad128(c.shared_ffn) * c.hidden);
+  b.dn_s = L.take(on * 2ull * c.hidden * pad64(c.shared_ffn));
+  b.total = L.off;
+  return b;
+}
+
+// ext_bops: the caller supplies the B operands (flux_profile_layer_bops): none in the workspace
+WsPlan plan(const flux_moe_cfg& c, const Policy& pol, int64_t T, bool ext_bops = false) {
   Layout L;
   WsPlan p;
   const int64_t n_rt = (T + kRouterTile - 1) / kRouterTile;
@@ -196,11 +215,13 @@ WsPlan plan(const flux_moe_cfg& c, const Policy& pol, int64_t T) {
   p.act_sh = L.take(2ull * T * pad64(c.shared_ffn));
   p.sh_sched = L.take(4 * sizeof(int32_t));  // sched_sh[2], row0_sh[1], rows_sh[1]
   p.y_sh = L.take(c.shared_ffn && !pol.fused_combine ? 2ull * T * c.hidden : 0);
-  const size_t pass = pol.pass ? 1 : 0;  // bf16 B operands only for the separate-pass path
-  p.wgu_r = L.take(pass * 2ull * c.n_experts * 2 * pad128(c.ffn) * c.hidden);
-  p.wdn_r = L.take(pass * 2ull * c.n_experts * c.hidden * pad64(c.ffn));
-  p.wgu_s = L.take(pass * 2ull * 2 * pad128(c.shared_ffn) * c.hidden);
-  p.wdn_s = L.take(pass * 2ull * c.hidden * pad64(c.shared_ffn));
+  // bf16 B operands only for the separate-pass path, unless the caller supplies them
+  const BopsPlan b = bops_plan(c, pol.pass && !ext_bops);
+  const size_t b0 = L.take(b.total);
+  p.wgu_r = b0 + b.gu_r;
+  p.wdn_r = b0 + b.dn_r;
+  p.wgu_s = b0 + b.gu_s;
+  p.wdn_s = b0 + b.dn_s;
   const size_t ch = pol.chain ? 1 : 0;  // chained GEMMs: tile / m-tile prefixes and the act ready flags
   p.sched_c = L.take(ch * sizeof(int32_t) * (n_groups + 1));
   p.mt_base = L.take(ch * sizeof(int32_t) * n_groups);
@@ -229,6 +250,51 @@ flux_status validate_cfg(const flux_moe_cfg* c) {
   }
   if (c->wbits == 4 && (c->hidden % 32 || c->ffn % 32 || c->shared_ffn % 32)) return FLUX_E_UNSUPPORTED;
   if (c->wbits == 2 && (c->hidden % 64 || c->ffn % 64 || c->shared_ffn % 64)) return FLUX_E_UNSUPPORTED;
+  return FLUX_OK;
+}
+
+// The dequantization pass of one layer (R1b; launch_dequant) into B-operand buffers.
+struct Bops {
+  void *gu_r, *dn_r, *gu_s, *dn_s;
+};
+Bops bops_at(const flux_moe_cfg& c, void* base) {
+  const BopsPlan b = bops_plan(c);
+  uint8_t* p = (uint8_t*)base;
+  return {p + b.gu_r, p + b.dn_r, p + b.gu_s, p + b.dn_s};
+}
+cudaError_t dequant_layer(const flux_moe_cfg& c, const flux_qlayer* w, const Bops& b, cudaStream_t s) {
+  const bool per_channel = c.group_size == 0 && c.wbits != 16;
+  const int H = c.hidden, F = c.ffn, Fs = c.shared_ffn, E = c.n_experts;
+  const int g_h = per_channel ? H : c.group_size, g_f = per_channel ? F : c.group_size,
+            g_fs = per_channel ? Fs : c.group_size;
+  const int pc = per_channel ? 1 : 0;
+  KernelTimer kt(K_DEQUANT, s);
+  cudaError_t e = launch_dequant(c.wbits, (const uint8_t*)w->gate_q, w->gate_s, (const uint8_t*)w->up_q, w->up_s, E, F,
+                                 H, pad128(F), 1, g_h, pc, H, b.gu_r, s);
+  if (e == cudaSuccess)
+    e = launch_dequant(c.wbits, (const uint8_t*)w->down_q, w->down_s, nullptr, nullptr, E, H, F, 0, 0, g_f, pc,
+                       pad64(F), b.dn_r, s);
+  if (e == cudaSuccess && Fs > 0)
+    e = launch_dequant(c.wbits, (const uint8_t*)w->sh_gate_q, w->sh_gate_s, (const uint8_t*)w->sh_up_q, w->sh_up_s, 1,
+                       Fs, H, pad128(Fs), 1, g_h, pc, H, b.gu_s, s);
+  if (e == cudaSuccess && Fs > 0)
+    e = launch_dequant(c.wbits, (const uint8_t*)w->sh_down_q, w->sh_down_s, nullptr, nullptr, 1, H, Fs, 0, 0, g_fs, pc,
+                       pad64(Fs), b.dn_s, s);
+  return e;
+}
+// the weight pointers flux_profile_layer requires of a layer
+flux_status check_qlayer(const flux_moe_cfg& c, const flux_qlayer* w) {
+  const bool quantized = c.wbits != 16;
+  if (!w || !w->router_w || !w->gate_q || !w->up_q || !w->down_q ||
+      (quantized && (!w->gate_s || !w->up_s || !w->down_s)))
+    return FLUX_E_INVALID;
+  if (c.shared_ffn > 0 && (!w->sh_gate_q || !w->sh_up_q || !w->sh_down_q ||
+                           (quantized && (!w->sh_gate_s || !w->sh_up_s || !w->sh_down_s))))
+    return FLUX_E_INVALID;
+  if (c.n_router > 0 && !w->remap) return FLUX_E_INVALID;
+  const void* ptrs16[] = {w->router_w, w->gate_q, w->up_q, w->down_q, w->sh_gate_q, w->sh_up_q, w->sh_down_q};
+  for (const void* p : ptrs16)
+    if (p && !aligned16(p)) return FLUX_E_INVALID;
   return FLUX_OK;
 }
 }  // namespace
@@ -265,31 +331,29 @@ flux_status flux_profile_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, co
   return flux_profile_layer_ex(cfg, nullptr, w, x, residual, T, out, ws, ws_bytes, stream);
 }
 
-flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* policy, const flux_qlayer* w,
-                                  const void* x, const void* residual, int64_t T, const flux_layer_out* out, void* ws,
-                                  size_t ws_bytes, void* stream) {
+// flux_profile_layer_ex / flux_profile_layer_bops.  bops: this layer's B operands already
+// dequantized (used on the dequant-pass path, ignored otherwise).
+static flux_status profile_impl(const flux_moe_cfg* cfg, const flux_policy* policy, const flux_qlayer* w,
+                                const void* bops, const void* x, const void* residual, int64_t T,
+                                const flux_layer_out* out, void* ws, size_t ws_bytes, void* stream) {
   flux_status st = validate_cfg(cfg);
   if (st != FLUX_OK) return st;
   if ((st = validate_policy(policy)) != FLUX_OK) return st;
   if (!w || !out || T < 0) return FLUX_E_INVALID;
+  if (bops && !aligned16(bops)) return FLUX_E_INVALID;
   if (T == 0) return FLUX_OK;
   if (T * cfg->top_k >= (int64_t)1 << 31) return FLUX_E_UNSUPPORTED;
   const flux_moe_cfg& c = *cfg;
   const bool sh = c.shared_ffn > 0;
   const bool quantized = c.wbits != 16;
-  if (!x || !out->y || !out->topk_ids || !out->topk_w || !out->hist || !w->router_w || !w->gate_q || !w->up_q ||
-      !w->down_q || (quantized && (!w->gate_s || !w->up_s || !w->down_s)))
-    return FLUX_E_INVALID;
-  if (sh && (!w->sh_gate_q || !w->sh_up_q || !w->sh_down_q ||
-             (quantized && (!w->sh_gate_s || !w->sh_up_s || !w->sh_down_s))))
-    return FLUX_E_INVALID;
-  if (c.n_router > 0 && !w->remap) return FLUX_E_INVALID;
-  const void* ptrs16[] = {x, residual, out->y, w->router_w, w->gate_q, w->up_q, w->down_q,
-                          w->sh_gate_q, w->sh_up_q, w->sh_down_q, ws};
+  if (!x || !out->y || !out->topk_ids || !out->topk_w || !out->hist) return FLUX_E_INVALID;
+  if ((st = check_qlayer(c, w)) != FLUX_OK) return st;
+  const void* ptrs16[] = {x, residual, out->y, ws};
   for (const void* p : ptrs16)
     if (p && !aligned16(p)) return FLUX_E_INVALID;
   const Policy pol = resolve_policy(c, policy, T);
-  const WsPlan P = plan(c, pol, T);
+  const bool ext_bops = bops != nullptr && pol.pass;
+  const WsPlan P = plan(c, pol, T, ext_bops);
   if (!ws || ws_bytes < P.total) return FLUX_E_WORKSPACE;
   if ((st = check_device()) != FLUX_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
@@ -320,28 +384,16 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
   int32_t* sh_sched = (int32_t*)(W + P.sh_sched);
   const bool fuse_combine = sh && pol.fused_combine;
   void* y_sh = W + P.y_sh;  // shared-MLP output (unused when the combine is fused into its down GEMM)
-  void* wgu_r = W + P.wgu_r;
-  void* wdn_r = W + P.wdn_r;
-  void* wgu_s = W + P.wgu_s;
-  void* wdn_s = W + P.wdn_s;
+  const Bops ob = ext_bops ? bops_at(c, const_cast<void*>(bops)) : Bops{W + P.wgu_r, W + P.wdn_r, W + P.wgu_s, W + P.wdn_s};
+  void* wgu_r = ob.gu_r;
+  void* wdn_r = ob.dn_r;
+  void* wgu_s = ob.gu_s;
+  void* wdn_s = ob.dn_s;
 
   // ---- (a) weights -> bf16 B operands (scale folded for grouped quantization)
   cudaError_t e = cudaSuccess;
   const bool pass = pol.pass;
-  if (pass) {
-  KernelTimer kt(K_DEQUANT, s);
-  e = launch_dequant(c.wbits, (const uint8_t*)w->gate_q, w->gate_s, (const uint8_t*)w->up_q, w->up_s, E, F, H, Fp, 1,
-                     g_h, per_channel, H, wgu_r, s);
-  if (e == cudaSuccess)
-    e = launch_dequant(c.wbits, (const uint8_t*)w->down_q, w->down_s, nullptr, nullptr, E, H, F, 0, 0, g_f,
-                       per_channel, Fld, wdn_r, s);
-  if (e == cudaSuccess && sh)
-    e = launch_dequant(c.wbits, (const uint8_t*)w->sh_gate_q, w->sh_gate_s, (const uint8_t*)w->sh_up_q, w->sh_up_s,
-                       1, Fs, H, Fsp, 1, g_h, per_channel, H, wgu_s, s);
-  if (e == cudaSuccess && sh)
-    e = launch_dequant(c.wbits, (const uint8_t*)w->sh_down_q, w->sh_down_s, nullptr, nullptr, 1, H, Fs, 0, 0, g_fs,
-                       per_channel, Fsld, wdn_s, s);
-  }
+  if (pass && !ext_bops) e = dequant_layer(c, w, ob, s);
   if (e != cudaSuccess) { set_last_error("dequant", e); return FLUX_E_CUDA; }
 
   // ---- (b) K1 router + top-k + histogram
@@ -577,6 +629,44 @@ flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* po
   return FLUX_OK;
 }
 
+flux_status flux_profile_layer_ex(const flux_moe_cfg* cfg, const flux_policy* policy, const flux_qlayer* w,
+                                  const void* x, const void* residual, int64_t T, const flux_layer_out* out, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  return profile_impl(cfg, policy, w, nullptr, x, residual, T, out, ws, ws_bytes, stream);
+}
+
+flux_status flux_profile_layer_bops(const flux_moe_cfg* cfg, const flux_policy* policy, const flux_qlayer* w,
+                                    const void* bops, const void* x, const void* residual, int64_t T,
+                                    const flux_layer_out* out, void* ws, size_t ws_bytes, void* stream) {
+  return profile_impl(cfg, policy, w, bops, x, residual, T, out, ws, ws_bytes, stream);
+}
+
+size_t flux_profile_layer_workspace_bops(const flux_moe_cfg* cfg, const flux_policy* policy, int64_t T) {
+  if (validate_cfg(cfg) != FLUX_OK || validate_policy(policy) != FLUX_OK || T < 0) return 0;
+  return plan(*cfg, resolve_policy(*cfg, policy, T), T, true).total;
+}
+
+int32_t flux_profile_layer_uses_bops(const flux_moe_cfg* cfg, const flux_policy* policy, int64_t T) {
+  if (validate_cfg(cfg) != FLUX_OK || validate_policy(policy) != FLUX_OK || T < 0) return -1;
+  return resolve_policy(*cfg, policy, T).pass ? 1 : 0;
+}
+
+size_t flux_layer_bops_bytes(const flux_moe_cfg* cfg) {
+  if (validate_cfg(cfg) != FLUX_OK) return 0;
+  return bops_plan(*cfg).total;
+}
+
+flux_status flux_dequantize_layer(const flux_moe_cfg* cfg, const flux_qlayer* w, void* bops, void* stream) {
+  flux_status st = validate_cfg(cfg);
+  if (st != FLUX_OK) return st;
+  if ((st = check_qlayer(*cfg, w)) != FLUX_OK) return st;
+  if (!bops || !aligned16(bops)) return FLUX_E_INVALID;
+  if ((st = check_device()) != FLUX_OK) return st;
+  const cudaError_t e = dequant_layer(*cfg, w, bops_at(*cfg, bops), (cudaStream_t)stream);
+  if (e != cudaSuccess) set_last_error("dequant", e);
+  return cuda_status(e);
+}
+
 flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype in_dtype, const void* w, int64_t R,
                                   int64_t K, void* q, float* s, void* stream) {
   if (wbits != 2 && wbits != 4 && wbits != 8) return FLUX_E_UNSUPPORTED;
@@ -591,6 +681,48 @@ flux_status flux_quantize_weights(int32_t wbits, int32_t group_size, flux_dtype 
   if (st != FLUX_OK) return st;
   KernelTimer kt(K_QUANTIZE, (cudaStream_t)stream);
   return cuda_status(launch_quantize(wbits, g, in_dtype == FLUX_FP32, w, R, K, q, s, (cudaStream_t)stream));
+}
+
+flux_status flux_quantize_weights_bops(const flux_moe_cfg* cfg, int32_t family, flux_dtype in_dtype, const void* w,
+                                       int32_t n_layers, void* q, float* s, void* bops, size_t bops_stride,
+                                       void* stream) {
+  flux_status st = validate_cfg(cfg);
+  if (st != FLUX_OK) return st;
+  const flux_moe_cfg& c = *cfg;
+  if (c.wbits == 16) return FLUX_E_UNSUPPORTED;
+  if (family < FLUX_FAM_GATE || family > FLUX_FAM_SH_DOWN || n_layers < 0) return FLUX_E_INVALID;
+  const bool shared = family >= FLUX_FAM_SH_GATE;
+  if (shared && c.shared_ffn == 0) return FLUX_E_INVALID;
+  if (in_dtype != FLUX_BF16 && in_dtype != FLUX_FP32) return FLUX_E_INVALID;
+  if (!bops || !aligned16(bops) || bops_stride % 16 || bops_stride < bops_plan(c).total) return FLUX_E_INVALID;
+  const int H = c.hidden, F = shared ? c.shared_ffn : c.ffn, G = shared ? 1 : c.n_experts;
+  const bool down = family == FLUX_FAM_DOWN || family == FLUX_FAM_SH_DOWN;
+  const int N = down ? H : F, K = down ? F : H;  // rows and contraction of this family's matrices
+  const int64_t rows = (int64_t)G * N;
+  const int64_t g = c.group_size ? c.group_size : K;
+  if (n_layers == 0) return FLUX_OK;
+  if (!w || !q || !s || !aligned16(w) || !aligned16(q) || (reinterpret_cast<uintptr_t>(s) & 3)) return FLUX_E_INVALID;
+  if ((st = check_device()) != FLUX_OK) return st;
+  const BopsPlan b = bops_plan(c);
+  BopsOut bo{};
+  const size_t off = family == FLUX_FAM_GATE || family == FLUX_FAM_UP ? b.gu_r
+                     : family == FLUX_FAM_DOWN                        ? b.dn_r
+                     : family == FLUX_FAM_SH_DOWN                     ? b.dn_s
+                                                                      : b.gu_s;
+  bo.out = (uint8_t*)bops + off;
+  bo.layer_stride = (int64_t)bops_stride;
+  if (rows * n_layers * (K / g) >= (int64_t)1 << 31) return FLUX_E_UNSUPPORTED;  // 32-bit item arithmetic in the kernel
+  bo.ipr = make_fastdiv((uint32_t)(K / g));
+  bo.layer_rows = make_fastdiv((uint32_t)rows);
+  bo.n = make_fastdiv((uint32_t)N);
+  bo.Fp = pad128(F);
+  bo.interleave = down ? 0 : 1;
+  bo.up = family == FLUX_FAM_UP || family == FLUX_FAM_SH_UP;
+  bo.ldo = down ? pad64(F) : H;
+  bo.per_channel = c.group_size == 0;
+  KernelTimer kt(K_QUANTIZE, (cudaStream_t)stream);
+  return cuda_status(
+      launch_quantize(c.wbits, g, in_dtype == FLUX_FP32, w, rows * n_layers, K, q, s, (cudaStream_t)stream, &bo));
 }
 
 flux_status flux_merge_experts(flux_dtype dtype, int32_t n_experts, int64_t numel, const void* experts,

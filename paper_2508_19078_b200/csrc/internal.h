@@ -48,8 +48,28 @@ const char* last_error();
 
 // ---------------------------------------------------------------- launchers
 // K0 (quantize.cu)
+// Optional fused output of the quantizer: the family's bf16 B operands exactly as launch_dequant writes
+// them (ŵ = bf16(q·bf16(s)) grouped, bf16(q) per channel), for the rows of n consecutive layers.
+// Unsigned division by a run-time constant d >= 1 for n < 2^31 (Granlund-Montgomery): q = (umulhi(n, m) + n) >> l.
+struct FastDiv {
+  uint32_t d, m, l;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  const uint64_t m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
+  return {d, (uint32_t)m, l};
+}
+struct BopsOut {
+  void* out;              // this family's B-operand region in layer 0's buffer (null = no fused output)
+  int64_t layer_stride;   // bytes between consecutive layers' buffers
+  FastDiv ipr;            // quantization groups per row (K / g)
+  FastDiv layer_rows;     // rows of this family per layer (G·N)
+  FastDiv n;              // N, rows per expert
+  int Fp, interleave, up, ldo, per_channel;  // launch_dequant's row mapping; up: the up half of gate/up
+};
 cudaError_t launch_quantize(int wbits, int64_t g, bool in_fp32, const void* w, int64_t R, int64_t K, void* q, float* s,
-                            cudaStream_t st);
+                            cudaStream_t st, const BopsOut* bo = nullptr);
 // K7 (merge.cu)
 constexpr int kMergeMaxJobs = 256;
 struct MergeJob {           // one weight family of one layer

@@ -18,8 +18,8 @@ import numpy as np
 import torch
 
 from . import (FLUX_OK, Comm, LayerOut, QLayer, attention_hist, cluster_experts, expert_features, layer_budget,
-               make_cfg, merge_experts_batch, output_error, profile_layer, profile_layer_workspace,
-               quantize_weights)
+               layer_bops_bytes, make_cfg, merge_experts_batch, output_error, profile_layer, profile_layer_bops,
+               profile_layer_uses_bops, profile_layer_workspace, quantize_weights, quantize_weights_bops)
 
 
 @dataclass
@@ -76,7 +76,10 @@ class MasterWeights:
 class QuantizedModel:
     """Canonical quantized weights (include/flux.h flux_qlayer) for all layers, on the device."""
 
-    def __init__(self, shape: ModelShape, device="cuda"):
+    def __init__(self, shape: ModelShape, device="cuda", with_bops: bool = False):
+        """with_bops: also keep every layer's bf16 B operands (flux_layer_bops_bytes each, ~1.1 GB per
+        DeepSeek-shape layer), written by the quantizer in the same pass (flux_quantize_weights_bops), so
+        that profiling skips the per-call dequantization pass."""
         self.shape = s = shape
         L, E, H, F, Fs = s.n_layers, s.n_experts, s.hidden, s.ffn, s.shared_ffn
         qdiv = {2: 4, 4: 2}.get(s.wbits, 1)  # codes per byte
@@ -101,17 +104,25 @@ class QuantizedModel:
         else:
             self.sh_gate_q = self.sh_up_q = self.sh_down_q = None
             self.sh_gate_s = self.sh_up_s = self.sh_down_s = None
+        self.bops = None
+        if with_bops and s.wbits != 16 and s.layer_experts is None:
+            # zeroed once: the rows padding F to a multiple of 128 are never written
+            self.bops = torch.zeros(L, layer_bops_bytes(s.ccfg(0)), dtype=torch.uint8, device=device)
 
     def quantize_from(self, m: MasterWeights, stream=None):
-        """a0: quantize every expert matrix of the master model (router copied: not quantized, R1)."""
+        """a0: quantize every expert matrix of the master model (router copied: not quantized, R1); with
+        bops, each family's bf16 B operands are written in the same pass."""
         s = self.shape
         self.router.copy_(m.router)
         pairs = [(m.gate, self.gate_q, self.gate_s), (m.up, self.up_q, self.up_s), (m.down, self.down_q, self.down_s)]
         if s.shared_ffn:
             pairs += [(m.sh_gate, self.sh_gate_q, self.sh_gate_s), (m.sh_up, self.sh_up_q, self.sh_up_s),
                       (m.sh_down, self.sh_down_q, self.sh_down_s)]
-        for w, q, sc in pairs:
-            quantize_weights(w, s.wbits, s.group_size, q, sc, stream)
+        for fam, (w, q, sc) in enumerate(pairs):
+            if self.bops is not None:
+                quantize_weights_bops(s.ccfg(0), fam, w, s.n_layers, q, sc, self.bops, stream)
+            else:
+                quantize_weights(w, s.wbits, s.group_size, q, sc, stream)
 
     def qlayer(self, l: int) -> QLayer:
         p = lambda t: None if t is None else t[l].data_ptr()  # noqa: E731
@@ -210,10 +221,19 @@ class Profiler:
         return LayerOut(self.y[l % 2].data_ptr(), p(self.ids), p(self.w), p(self.hist), p(self.offsets),
                         p(self.token_index), p(self.logits))
 
+    def _layer(self, qm, l: int, x: torch.Tensor, residual, stream):
+        bops = getattr(qm, "bops", None)
+        if bops is not None and profile_layer_uses_bops(self.cfgs[l], self.T, self.policy):
+            # the quantizer already wrote this layer's bf16 B operands: no dequantization pass per call
+            profile_layer_bops(self.cfgs[l], qm.qlayer(l), bops[l], x, residual, self.T, self.out(l), self.ws, stream,
+                               self.policy)
+        else:
+            profile_layer(self.cfgs[l], qm.qlayer(l), x, residual, self.T, self.out(l), self.ws, stream, self.policy)
+
     def run_layer(self, qm, l: int, x: torch.Tensor, residual: torch.Tensor | None = None, stream=None):
         """One flux_profile_layer call with layer l's weights on x (no chaining); residual None = x (R6),
         e.g. a zero buffer so that y is the MoE branch alone.  Accumulates into hist[l]; returns y."""
-        profile_layer(self.cfgs[l], qm.qlayer(l), x, residual, self.T, self.out(l), self.ws, stream, self.policy)
+        self._layer(qm, l, x, residual, stream)
         return self.y[l % 2]
 
     def run(self, qm: QuantizedModel, x: torch.Tensor, stream=None, on_layer=None, zero_hist: bool = True,
@@ -231,7 +251,7 @@ class Profiler:
         cur = x
         for l in range(self.shape.n_layers):
             torch.cuda.nvtx.range_push(f"layer {l}")  # the chunk x layer timeline under nsys
-            profile_layer(self.cfgs[l], qm.qlayer(l), cur, None, self.T, self.out(l), self.ws, stream, self.policy)
+            self._layer(qm, l, cur, None, stream)
             torch.cuda.nvtx.range_pop()
             if attn is not None:
                 attention_hist(self.ids[l], attn[l], self.shape.n_experts, self.ahist[l], stream)
