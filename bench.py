@@ -356,8 +356,11 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    h0 = time.perf_counter()
+    host_ms = []  # host time to enqueue each step (diagnostic: a step whose host time reaches the GPU's starves it)
     for _ in range(steps):
         step(x)
+        host_ms.append(1e3 * (time.perf_counter() - h0))
     ev1.record(stream)
     barrier()
     F.timing_enable(False)
@@ -440,6 +443,7 @@ def measure(args, cfg, T_rank, rank, world, stream_extras=True, steps=None, warm
 
     report_budgets()
     out = {"ms": ms, "ms_e2e": ms_e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "kern": kern, "clk": clk,
+           "host_ms": host_ms,
            "gemm_mhz": gemm_mhz,
            "T_rank": T_rank, "Tc": Tc, "n_chunks": n_chunks, "fused_bops": qm.bops is not None, "C": C, "budget_C": [int(c) for c in state["C"]],
            "steps": steps}
@@ -665,6 +669,7 @@ def main():
             "gpu_launches": res["launches"],
             "clocks": res["clk"],
             "kernels": kernel_table(cfg, res, peaks),
+            "host_enqueue_ms": [round(t, 1) for t in res["host_ms"]],  # cumulative, per timed step (diagnostic)
             "budget": args.budget,
             "budget_C": res["budget_C"],
             "merge_output_error": res.get("merge_output_error"),
