@@ -700,6 +700,7 @@ flux_status flux_quantize_weights_bops(const flux_moe_cfg* cfg, int32_t family, 
   const int N = down ? H : F, K = down ? F : H;  // rows and contraction of this family's matrices
   const int64_t rows = (int64_t)G * N;
   const int64_t g = c.group_size ? c.group_size : K;
+  if (K % g || g % 8 || g > 4096) return FLUX_E_UNSUPPORTED;  // the quantizer's team shapes (as flux_quantize_weights)
   if (n_layers == 0) return FLUX_OK;
   if (!w || !q || !s || !aligned16(w) || !aligned16(q) || (reinterpret_cast<uintptr_t>(s) & 3)) return FLUX_E_INVALID;
   if ((st = check_device()) != FLUX_OK) return st;
