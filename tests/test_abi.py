@@ -128,3 +128,32 @@ def test_policy_and_batch_validation_without_gpu(F):
         j.n_clusters, j.n_tuning = 3, 2  # compact: n_tuning + C > E
     assert L.flux_merge_experts_batch(0, 4, 16, 2, ctypes.cast(jobs, ctypes.c_void_p), 1, None) == F.FLUX_E_INVALID
     assert L.flux_merge_experts_batch(0, 4, 16, 2, ctypes.cast(jobs, ctypes.c_void_p), 2, None) == F.FLUX_E_INVALID
+
+
+def test_bops_host_functions_without_gpu(F):
+    """The quantizer-written B operands (flux_layer_bops_bytes & co.): sizes and path queries are host
+    functions; the fused quantizer validates its arguments before touching the device."""
+    ds = F.make_cfg(2048, 1408, 64, 6, 2816, 4, 128, 0)
+    pad64 = lambda v: (v + 63) // 64 * 64  # noqa: E731
+    pad128 = lambda v: (v + 127) // 128 * 128  # noqa: E731
+    r256 = lambda b: (b + 255) // 256 * 256  # noqa: E731
+    want = (r256(2 * 64 * 2 * pad128(1408) * 2048) + r256(2 * 64 * 2048 * pad64(1408)) +
+            r256(2 * 2 * pad128(2816) * 2048) + r256(2 * 2048 * pad64(2816)))
+    assert F.layer_bops_bytes(ds) == want
+    # the dequant-pass path from T·k >= 2048·E (auto policy), always with the pass policy
+    assert F.profile_layer_uses_bops(ds, 262144) and not F.profile_layer_uses_bops(ds, 1024)
+    assert F.profile_layer_uses_bops(ds, 1024, F.make_policy(F.WEIGHTS_DEQUANT_PASS))
+    with pytest.raises(ValueError):
+        F.profile_layer_uses_bops(F.make_cfg(2048, 1408, 64, 6, 2816, 3, 128, 0), 1024)  # wbits 3
+    # with caller-supplied operands the workspace holds none of them
+    T = 262144
+    assert F.profile_layer_workspace(ds, T) - F.profile_layer_workspace_bops(ds, T) == want
+    lib = F.lib()
+    bad_family = lib.flux_quantize_weights_bops(ctypes.byref(ds), 7, F.FLUX_BF16, None, 1, None, None, None, 0, None)
+    assert bad_family == 1  # FLUX_E_INVALID
+    small_stride = lib.flux_quantize_weights_bops(ctypes.byref(ds), F.FAM_GATE, F.FLUX_BF16, None, 1, None, None,
+                                                  ctypes.c_void_p(256), 64, None)
+    assert small_stride == 1
+    bf16_model = F.make_cfg(2048, 1408, 64, 6, 2816, 16, 0, 0)
+    assert lib.flux_quantize_weights_bops(ctypes.byref(bf16_model), F.FAM_GATE, F.FLUX_BF16, None, 1, None, None,
+                                          None, 0, None) == 2  # FLUX_E_UNSUPPORTED
