@@ -179,6 +179,78 @@ __global__ void __launch_bounds__(544, 1) read_tma(const uint8_t* __restrict__ i
   probe_end(p);
 }
 
+// TMA tensor-box ring read: one CTA per SM, a producer lane issues 2D boxes {64 columns (128 B, SW128),
+// BOX_ROWS rows} of a bf16 [rows][cols] tensor into STAGES stages; 16 consumer warps touch one word per
+// 512 B and release.  Box order: for each row block (row_blocks of BOX_ROWS rows, dealt round-robin to
+// the CTAs), every 64-column slice in turn — the router's x stream (rows = tokens) or, with few rows
+// far apart, the Gram's expert stream.
+template <int BOX_ROWS, int STAGES>
+__global__ void __launch_bounds__(544, 1) read_tma2d(const __grid_constant__ CUtensorMap map, int row_blocks,
+                                                     int col_slices, uint32_t* __restrict__ sink, Probe* p) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  constexpr int kBox = BOX_ROWS * 128;
+  uint8_t* data = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);  // SW128 boxes: 1 KB aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(data + STAGES * kBox);
+  uint64_t* empty = full + STAGES;
+  probe_begin(p);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 16);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // work = row_blocks x col_slices boxes in chunks of 64 consecutive column slices of one row block,
+  // chunks dealt round-robin to the CTAs (the Gram's order; the router's tiles when col_slices = 32)
+  const int per_rb = (col_slices + 63) / 64, n_chunks = row_blocks * per_rb;
+  const int my_chunks = (n_chunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int csz = col_slices < 64 ? col_slices : 64;
+  const int my = my_chunks * csz;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int g = 0; g < my; ++g) {
+        const int s = g % STAGES;
+        mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        const int ch = (int)blockIdx.x + (g / csz) * (int)gridDim.x;
+        const int rb = ch / per_rb, cs = (ch % per_rb) * 64 + g % csz;  // (col_slices % 64 == 0 or < 64)
+        mbar_arrive_expect_tx(&full[s], (uint32_t)kBox);
+        tma_load_2d_hint(data + s * kBox, &map, &full[s], cs * 64, rb * BOX_ROWS, pol);
+      }
+    }
+  } else {
+    uint32_t acc = 0;
+    const int v = threadIdx.x - 32;
+    for (int g = 0; g < my; ++g) {
+      const int s = g % STAGES;
+      mbar_wait(&full[s], (g / STAGES) & 1);
+      for (int o = v * 16; o < kBox; o += 512 * 16) acc ^= *reinterpret_cast<const uint32_t*>(data + s * kBox + o);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+  }
+  probe_end(p);
+}
+
+static CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = cuTensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "cuTensorMapEncodeTiled failed: %d\n", (int)r);
+    exit(1);
+  }
+  return m;
+}
+
 __global__ void fill_random(__nv_bfloat16* p, int64_t n, uint32_t seed) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t x = (uint32_t)i * 2654435761u ^ seed;
@@ -309,6 +381,39 @@ int main() {
     add("write_tma 16KB d8 4/SM", 1.0 * bytes, [&] { write_tma<S, 8><<<nsm * 4, 32, S>>>(b, bytes, pr); });
     add("write_stg U8", 1.0 * bytes, [&] { write_stg<8><<<nsm * 4, 512>>>((uint4*)b, nv, pr); });
     add("write_stg U2 2/SM", 1.0 * bytes, [&] { write_stg<2><<<nsm * 2, 512>>>((uint4*)b, nv, pr); });
+  }
+  {
+    // router-like: [1M tokens][2048] bf16 (4 KB rows), boxes of 256 token rows x 64 columns
+    static const CUtensorMap m_router = make_map_2d(a, (uint64_t)(bytes / 4096), 2048, 256);
+    constexpr int R = 256, ST = 5;
+    const int smem = R * 128 * ST + 2 * ST * 8 + 1024;
+    cudaFuncSetAttribute(read_tma2d<R, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    add("tma2d router 256r", 1.0 * bytes, [&, smem] {
+      read_tma2d<R, ST><<<nsm, 544, smem>>>(m_router, (int)(bytes / 4096 / R), 32, sink, pr);
+    });
+    // gram-like: [704 = 11 layers x 64 experts][2,883,584] bf16 (expert rows 5.77 MB apart, the DeepSeek
+    // family size), boxes of 64 expert rows x 64 columns, 64-slice chunks
+    const uint64_t gcols = 2883584, grows = 704;
+    static const CUtensorMap m_gram = make_map_2d(a, grows, gcols, 64);
+    constexpr int G = 64, SG = 16;
+    const int smemg = G * 128 * SG + 2 * SG * 8 + 1024;
+    cudaFuncSetAttribute(read_tma2d<G, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemg);
+    add("tma2d gram 64r 5.8MB", 2.0 * grows * gcols, [&, smemg] {
+      read_tma2d<G, SG><<<nsm, 544, smemg>>>(m_gram, (int)(grows / 64), (int)(gcols / 64), sink, pr);
+    });
+    // the same with 16-row boxes (16 experts per box: a quarter of the pages touched per box)
+    static const CUtensorMap m_gram16 = make_map_2d(a, grows, gcols, 16);
+    constexpr int G16 = 16, SG16 = 64;
+    const int smemg16 = G16 * 128 * SG16 + 2 * SG16 * 8 + 1024;
+    cudaFuncSetAttribute(read_tma2d<G16, SG16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemg16);
+    add("tma2d gram 16r 5.8MB", 2.0 * grows * gcols, [&, smemg16] {
+      read_tma2d<G16, SG16><<<nsm, 544, smemg16>>>(m_gram16, (int)(grows / 16), (int)(gcols / 64), sink, pr);
+    });
+    // contiguous: [32M rows][64] bf16 (128 B rows back to back), boxes of 256 rows = 32 KB contiguous
+    static const CUtensorMap m_cont = make_map_2d(a, (uint64_t)(bytes / 128), 64, 256);
+    add("tma2d contiguous 256r", 1.0 * bytes, [&, smem] {
+      read_tma2d<R, ST><<<nsm, 544, smem>>>(m_cont, (int)(bytes / 128 / R), 1, sink, pr);
+    });
   }
   printf("%-22s %5s %9s %9s %8s %10s\n", "kernel", "mode", "ms", "GB/s", "SM MHz", "B/clk/SM");
   const char* only = getenv("PROBE_ONLY");
