@@ -25,13 +25,15 @@ PATHS = [(2, 0, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (1, 2, 0, 0), (1, 0, 1, 0), (
 def run(cfg, paths):
     shape = ModelShape.of(cfg)
     masters = synthetic.master_weights(cfg)
-    qm = QuantizedModel(shape)
-    qm.quantize_from(masters)
     x = synthetic.tokens(cfg, 0, cfg.tokens)
-    for pol in paths:
-        prof = Profiler(shape, cfg.tokens, with_de=True, with_logits=True, policy=F.make_policy(*pol))
-        prof.run(qm, x)
-        torch.cuda.synchronize()
+    # plain quantizer + per-call dequantization, then the quantizer that also writes the bf16 operands
+    for with_bops in (False, True):
+        qm = QuantizedModel(shape, with_bops=with_bops)
+        qm.quantize_from(masters)
+        for pol in paths:
+            prof = Profiler(shape, cfg.tokens, with_de=True, with_logits=True, policy=F.make_policy(*pol))
+            prof.run(qm, x)
+            torch.cuda.synchronize()
     return masters, prof
 
 
